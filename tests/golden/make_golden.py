@@ -1,0 +1,141 @@
+"""Generate golden fixtures by running the REFERENCE package itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports ``vlgp`` from /root/reference/pkg/src, runs the reference's own
+public API (make_factor / factor_gradient / find_mode / make_probes /
+neg_marginal_loglik / gradient / VecchiaFactor.solve_B) on small seeded
+datasets and writes ``tests/golden/*.npz``.  The GPU box never reads
+/root/reference: the tests only read these committed fixtures.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _import_ref():
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    import vlgp  # noqa: F401
+    return vlgp
+
+
+def simulate(n, seed, rho, nu=1.5, family="bernoulli-logit", shape=2.0, F=None):
+    """Dense-Cholesky GP draw + responses (same recipe as pkg/tests/util.py:11-42)."""
+    from vlgp.covariance import CovarianceSpec, cov_matrix
+    from vlgp.likelihoods import get_likelihood
+
+    rng = np.random.default_rng(seed)
+    coords = rng.uniform(size=(n, 2))
+    spec = CovarianceSpec(1.0, rho, nu)
+    b = np.linalg.cholesky(cov_matrix(spec, coords)) @ rng.standard_normal(n)
+    lik = get_likelihood(family, **({"shape": shape} if family == "gamma" else {}))
+    F = np.zeros(n) if F is None else F
+    y = lik.sample(F + b, rng)
+    return coords, y, lik
+
+
+def _csr(prefix, M):
+    M = M.tocsr()
+    return {f"{prefix}_data": M.data, f"{prefix}_indices": M.indices.astype(np.int64),
+            f"{prefix}_indptr": M.indptr.astype(np.int64)}
+
+
+def laplace_case(name, n, seed, rho, m, t, precond="vadu", family="bernoulli-logit",
+                 shape=2.0, rank=None, p=0, ordering_seed=7, probe_seed=3, theta=None,
+                 nu=1.5, kernel_rhs=0):
+    from vlgp.covariance import CovarianceSpec
+    from vlgp.laplace import BackendConfig, find_mode, gradient, make_probes, neg_marginal_loglik
+    from vlgp.vecchia import build_factor, factor_gradient, find_neighbors, order_random
+
+    rng_x = np.random.default_rng(seed + 99)
+    X = None
+    F = np.zeros(n)
+    if p:
+        X = np.column_stack([np.ones(n)] + [rng_x.standard_normal(n) for _ in range(p - 1)])
+        beta = np.linspace(0.2, -0.3, p)
+        F = X @ beta
+    else:
+        beta = np.zeros(0)
+    coords, y, lik = simulate(n, seed, rho, nu=nu, family=family, shape=shape, F=F)
+    theta = (1.0, rho) if theta is None else theta
+    spec = CovarianceSpec(theta[0], theta[1], nu)
+    perm = order_random(n, ordering_seed)
+    nb = find_neighbors(coords, perm, m)
+    f = build_factor(coords, spec, nb, perm)
+    g_sig = factor_gradient(f, 0)
+    g_rho = factor_gradient(f, 1)
+    cfg = BackendConfig(preconditioner=precond, t=t, probe_seed=probe_seed, rank=rank)
+    y_f = y[perm]
+    F_f = F[perm]
+    X_f = X[perm] if X is not None else np.zeros((n, 0))
+    st = find_mode(f, lik, y_f, F_f, cfg)
+    probes, P = make_probes(f, st, cfg)
+    val = neg_marginal_loglik(st, f, cfg, probes=probes, P=P)
+    grad = gradient(st, f, lik, X_f, cfg, probes=probes, P=P)
+    nbr = np.full((n, m), -1, dtype=np.int64)
+    for i, s in enumerate(nb):
+        nbr[i, : len(s)] = s
+    out = dict(
+        n=n, m=m, t=t, seed=seed, rho=rho, nu=nu, sigma2=theta[0], theta=np.array(theta),
+        family=family, shape=shape, precond=precond, rank=-1 if rank is None else rank,
+        ordering_seed=ordering_seed, probe_seed=probe_seed, coords=coords, y=y, F=F,
+        X=np.zeros((n, 0)) if X is None else X, beta=beta, perm=perm, nbr=nbr,
+        D=f.D, dD_sig=g_sig.dD, dD_rho=g_rho.dD, b=st.b, W=st.W, logp=st.logp, quad=st.quad,
+        newton_iters=st.newton_iters, Z=probes.Z, solves=probes.solves, psolves=probes.psolves,
+        tri_diag=np.concatenate([tr.diag for tr in probes.tridiags]),
+        tri_len=np.array([tr.order for tr in probes.tridiags]),
+        tri_off=np.concatenate([tr.off for tr in probes.tridiags]),
+        logdet_P=P.logdet(), nll=val, dtheta=grad["dtheta"], dbeta=grad["dbeta"],
+        dxi=grad["dxi"],
+    )
+    out.update(_csr("B", f.B))
+    out.update(_csr("dB_rho", g_rho.dB))
+    if kernel_rhs:
+        Xr = np.random.default_rng(seed + 5).standard_normal((n, kernel_rhs))
+        out.update(kx=Xr, kBx=f.B @ Xr, kBtx=f.B.T @ Xr, kBinvx=f.solve_B(Xr),
+                   kBtinvx=f.solve_B(Xr, transpose=True), kQx=f.apply_precision(Xr),
+                   kSx=f.apply_sigma_tilde(Xr))
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(f"{name}: n={n} nll={val:.12g} dtheta={grad['dtheta']} newton={st.newton_iters}")
+
+
+def knn_case(name, n, m, seed, ordering_seed):
+    from vlgp.vecchia import find_neighbors, order_random
+
+    coords = np.random.default_rng(seed).uniform(size=(n, 2))
+    perm = order_random(n, ordering_seed)
+    nb = find_neighbors(coords, perm, m)
+    nbr = np.full((n, m), -1, dtype=np.int32)
+    for i, s in enumerate(nb):
+        nbr[i, : len(s)] = s
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), coords=coords, perm=perm,
+                        nbr=nbr, m=m)
+    print(f"{name}: n={n} m={m}")
+
+
+def main():
+    _import_ref()
+    # configs[0]-shaped (scaled down): bernoulli-logit, nu=1.5, VADU
+    laplace_case("logit_vadu_n400", 400, seed=11, rho=0.1, m=10, t=8, kernel_rhs=3)
+    laplace_case("logit_vadu_n1500", 1500, seed=12, rho=0.05, m=20, t=16, kernel_rhs=2)
+    laplace_case("logit_vadu_cov_n300", 300, seed=13, rho=0.1, m=8, t=6, p=2)
+    laplace_case("probit_vadu_n300", 300, seed=14, rho=0.1, m=8, t=6,
+                 family="bernoulli-probit", nu=2.5)
+    laplace_case("gamma_vadu_n300", 300, seed=15, rho=0.1, m=8, t=6, family="gamma",
+                 shape=2.0, nu=0.5)
+    laplace_case("logit_lrac_n300", 300, seed=16, rho=0.1, m=8, t=6, precond="lrac", rank=30)
+    knn_case("knn_n6000_m12", 6000, 12, seed=21, ordering_seed=22)
+
+
+if __name__ == "__main__":
+    main()

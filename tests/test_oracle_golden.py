@@ -1,0 +1,88 @@
+"""Pin the CPU oracle (oracle/vl_oracle.py) against reference-generated fixtures."""
+
+import numpy as np
+import pytest
+
+from oracle import vl_oracle as O
+from _golden import LAPLACE_CASES, csr, load, scal, tridiags
+
+
+def _cfg(g):
+    rank = int(g["rank"])
+    return O.Cfg(preconditioner=str(g["precond"]), t=int(g["t"]),
+                 probe_seed=int(g["probe_seed"]), rank=None if rank < 0 else rank)
+
+
+@pytest.mark.parametrize("name", LAPLACE_CASES)
+def test_factor_matches_reference(name):
+    g = load(name)
+    xy = g["coords"][g["perm"]]
+    f = O.vecchia_factor(xy, g["nbr"], scal(g, "sigma2"), scal(g, "rho"), scal(g, "nu"))
+    B = csr(g, "B")
+    assert np.array_equal(f.B.indptr, B.indptr) and np.array_equal(f.B.indices, B.indices)
+    assert np.abs(f.B.data - B.data).max() <= 1e-13
+    assert np.abs(f.D - g["D"]).max() <= 1e-13
+    (dB0, dD0), (dB1, dD1) = O.vecchia_grads(f)
+    assert np.abs(dD0 - g["dD_sig"]).max() <= 1e-13
+    assert np.abs(dD1 - g["dD_rho"]).max() <= 1e-12 * max(1.0, np.abs(g["dD_rho"]).max())
+    assert np.abs(dB1.data - csr(g, "dB_rho").data).max() <= 1e-12 * max(1, np.abs(dB1.data).max())
+
+
+@pytest.mark.parametrize("name", LAPLACE_CASES)
+def test_evaluation_matches_reference(name):
+    g = load(name)
+    perm = g["perm"]
+    xy = g["coords"][perm]
+    lik = O.Lik(str(g["family"]), float(g["shape"]))
+    cfg = _cfg(g)
+    val, grad, info = O.evaluate(xy, g["nbr"], g["y"][perm], g["F"][perm], g["X"][perm],
+                                 scal(g, "sigma2"), scal(g, "rho"), scal(g, "nu"), lik, cfg)
+    st, pr = info["state"], info["probes"]
+    assert st.newton_iters == int(g["newton_iters"])
+    assert np.abs(st.b - g["b"]).max() <= 1e-10 * max(1.0, np.abs(g["b"]).max())
+    assert np.abs(pr.Z - g["Z"]).max() <= 1e-12 * np.abs(g["Z"]).max()
+    ref_tri = tridiags(g)
+    assert [len(d) for d, _ in pr.tri] == [len(d) for d, _ in ref_tri]
+    assert val == pytest.approx(float(g["nll"]), rel=1e-11)
+    np.testing.assert_allclose(grad["dtheta"], g["dtheta"], rtol=1e-8, atol=1e-10)
+    np.testing.assert_allclose(grad["dbeta"], g["dbeta"], rtol=1e-8, atol=1e-10)
+    np.testing.assert_allclose(grad["dxi"], g["dxi"], rtol=1e-8, atol=1e-10)
+
+
+@pytest.mark.parametrize("name", ["logit_vadu_n400", "logit_vadu_n1500"])
+def test_kernel_ops_match_reference(name):
+    g = load(name)
+    B = csr(g, "B")
+    f = O.Factor(g["coords"][g["perm"]], g["nbr"], 1.0, 0.1, 1.5, B, g["D"])
+    X = g["kx"]
+    np.testing.assert_allclose(f.Bmul(X), g["kBx"], rtol=0, atol=1e-13)
+    np.testing.assert_allclose(f.BTmul(X), g["kBtx"], rtol=0, atol=1e-13)
+    np.testing.assert_allclose(f.solve_B(X), g["kBinvx"], rtol=0, atol=1e-12 * np.abs(g["kBinvx"]).max())
+    np.testing.assert_allclose(f.solve_B(X, True), g["kBtinvx"], rtol=0,
+                               atol=1e-12 * np.abs(g["kBtinvx"]).max())
+    np.testing.assert_allclose(f.precision(X), g["kQx"], rtol=0, atol=1e-10 * np.abs(g["kQx"]).max())
+
+
+def test_knn_matches_reference():
+    g = load("knn_n6000_m12")
+    nbr = O.knn_previous(g["coords"][g["perm"]], int(g["m"]))
+    assert np.array_equal(nbr, g["nbr"].astype(np.int64))
+
+
+def test_three_point_known_answer():
+    # pkg/tests/test_vecchia.py:90-104 hand case: nu=0.5, sigma2=1.5, rho=2
+    xy = np.array([[0.0], [1.0], [3.0]])
+    nbr = O.knn_previous(xy, 1)
+    f = O.vecchia_factor(xy, nbr, 1.5, 2.0, 0.5)
+    c01, c12 = 1.5 * np.exp(-0.5), 1.5 * np.exp(-1.0)
+    assert f.B[1, 0] == pytest.approx(-c01 / 1.5, rel=1e-14)
+    assert f.B[2, 1] == pytest.approx(-c12 / 1.5, rel=1e-14)
+    np.testing.assert_allclose(f.D, [1.5, 1.5 - c01 * c01 / 1.5, 1.5 - c12 * c12 / 1.5], rtol=1e-14)
+
+
+def test_matern_anchors():
+    # pkg/tests/test_covariance.py:27-31,73-76
+    assert O.matern(0.3, 1.0, 0.3 * np.sqrt(3.0), 1.5) == pytest.approx(2 * np.exp(-1.0), rel=1e-14)
+    r = 0.2
+    assert O.matern(r, 1.0, r, 1.5) == pytest.approx((1 + np.sqrt(3)) * np.exp(-np.sqrt(3)), rel=1e-14)
+    assert O.matern_drho(r, 1.0, r, 1.5) == pytest.approx(3 * np.exp(-np.sqrt(3)) / r, rel=1e-14)
