@@ -1,0 +1,30 @@
+"""B200-native Vecchia-Laplace hot path (drop-in for the iterative path of vlgp).
+
+The public names mirror the reference package's re-exports
+(vlgp/__init__.py:10-64).  All heavy arithmetic runs in the in-tree sm_100a
+library ``libvlgpx.so``; there is no CPU fallback.
+"""
+
+from .covariance import CovarianceSpec, Locations, cov_grad, cov_submatrix, cov_value
+from .errors import (
+    BreakdownError,
+    CapabilityError,
+    CapacityError,
+    ConfigError,
+    ConvergenceError,
+    DataError,
+    DeviceError,
+    FactorizationError,
+    NumericalError,
+    VlgpError,
+)
+from .vecchia import (
+    VecchiaFactor,
+    build_factor,
+    factor_gradient,
+    find_neighbors,
+    make_factor,
+    order_random,
+)
+
+__version__ = "0.1.0"

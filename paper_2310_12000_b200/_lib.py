@@ -1,0 +1,90 @@
+"""ctypes binding of the in-tree CUDA library libvlgpx.so (include/vlgpx.h).
+
+There is no CPU fallback: if the library or a CUDA device is missing, every
+compute entry point raises DeviceError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import STATUS, DeviceError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvlgpx.so")
+
+_lock = threading.Lock()
+_lib = None
+
+c_int, c_int64, c_double, c_void_p = C.c_int, C.c_int64, C.c_double, C.c_void_p
+P_int32 = C.POINTER(C.c_int32)
+P_int64 = C.POINTER(C.c_int64)
+P_double = C.POINTER(C.c_double)
+
+# name -> (argtypes); every function returns int status unless listed in _RET
+_SIGS = {
+    "vl_version": [],
+    "vl_last_error": [],
+    "vl_ctx_create": [c_int, c_void_p, C.POINTER(c_void_p)],
+    "vl_ctx_destroy": [c_void_p],
+    "vl_ctx_sync": [c_void_p],
+    "vl_ctx_info": [c_void_p, P_int64],
+    "vl_knn_previous": [c_void_p, c_int64, c_int, c_int, c_void_p, c_int],
+    "vl_pattern_create": [c_void_p, c_int64, c_int, c_int, c_void_p, c_void_p, c_int, C.POINTER(c_void_p)],
+    "vl_pattern_destroy": [c_void_p],
+    "vl_pattern_perm": [c_void_p, c_void_p],
+    "vl_pattern_info": [c_void_p, P_int64],
+    "vl_factor_build": [c_void_p, c_void_p, c_double, c_double, c_double, c_int, C.POINTER(c_void_p)],
+    "vl_factor_destroy": [c_void_p],
+    "vl_factor_get": [c_void_p, c_void_p, c_int, c_void_p],
+    "vl_spmm": [c_void_p, c_void_p, c_int, c_int64, c_void_p, c_void_p],
+    "vl_sptrsv": [c_void_p, c_void_p, c_int, c_int64, c_void_p, c_void_p],
+}
+_RET = {"vl_last_error": C.c_char_p}
+
+# functions declared in include/vlgpx.h (tests check the export table)
+EXPORTED = sorted(_SIGS)
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(
+                f"native library {LIB_PATH} is missing; run `python -m paper_2310_12000_b200.build` "
+                "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = _RET.get(name, c_int)
+        _lib = L
+    return _lib
+
+
+def check(status):
+    if status != 0:
+        msg = lib().vl_last_error()
+        msg = msg.decode() if msg else f"status {status}"
+        raise STATUS.get(status, DeviceError)(msg)
+
+
+def call(name, *args):
+    check(getattr(lib(), name)(*args))
+
+
+def ptr(a):
+    """Raw pointer of a numpy array or torch tensor (contiguity checked)."""
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return C.c_void_p(a.data_ptr())
+    if not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("array must be C-contiguous")
+    return a.ctypes.data_as(c_void_p)

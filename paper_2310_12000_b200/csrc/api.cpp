@@ -1,0 +1,272 @@
+// C-ABI entry points (include/vlgpx.h).  Exceptions never cross the ABI:
+// every call maps failures onto a status code + thread-local message.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/vlgpx.h"
+#include "ops.h"
+
+struct vl_ctx {
+  vl::Ctx c;
+};
+struct vl_pattern {
+  vl::Pattern p;
+  vl_ctx* ctx;
+};
+struct vl_factor {
+  vl::Factor f;
+};
+
+namespace vl {
+
+static thread_local std::string g_last_error;
+
+struct VlException : std::runtime_error {
+  int code;
+  VlException(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw VlException(code, msg); }
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    std::string m = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ") in " + what +
+                    " at " + file + ":" + std::to_string(line);
+    throw VlException(kECuda, m);
+  }
+}
+
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+void DevBuf::alloc(size_t nbytes) {
+  if (nbytes <= bytes && p) return;
+  release();
+  if (nbytes == 0) nbytes = 8;
+  VL_CUDA(cudaMalloc(&p, nbytes));
+  bytes = nbytes;
+}
+
+template <class F>
+static int guard(F&& f) {
+  try {
+    f();
+    return kOk;
+  } catch (const VlException& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host out of memory";
+    return kECapacity;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return kEInternal;
+  }
+}
+
+template <class T>
+static void upload(Ctx& C, DevBuf& dst, const std::vector<T>& src) {
+  dst.alloc(sizeof(T) * std::max<size_t>(src.size(), 1));
+  if (!src.empty())
+    VL_CUDA(cudaMemcpyAsync(dst.p, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, C.stream));
+}
+
+void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
+  std::vector<int32_t> ell, cnt, fwd, bwd, tptr, tidx, tmap;
+  pattern_build_host(P, xy, nbr, ell, cnt, fwd, bwd, tptr, tidx, tmap);
+  std::vector<double> xys((size_t)P.n * P.d);
+  for (int64_t s = 0; s < P.n; ++s)
+    for (int k = 0; k < P.d; ++k) xys[s * P.d + k] = xy[(int64_t)P.sperm[s] * P.d + k];
+  upload(C, P.xy, xys);
+  upload(C, P.nbr, ell);
+  upload(C, P.cnt, cnt);
+  upload(C, P.fidx, P.sperm);
+  upload(C, P.fwd_order, fwd);
+  upload(C, P.bwd_order, bwd);
+  upload(C, P.tptr, tptr);
+  upload(C, P.tidx, tidx);
+  upload(C, P.tmap, tmap);
+  ensure_flags(C, P.n);
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+}
+
+}  // namespace vl
+
+using namespace vl;
+
+extern "C" {
+
+int vl_version(void) { return 100; }
+const char* vl_last_error(void) { return g_last_error.c_str(); }
+
+int vl_ctx_create(int device, void* stream, vl_ctx** out) {
+  return guard([&] {
+    if (!out) fail(kEConfig, "null output handle");
+    int ndev = 0;
+    VL_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) fail(kEConfig, "invalid CUDA device ordinal " + std::to_string(device));
+    VL_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    VL_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) fail(kECapability, std::string("vlgpx is built for sm_100a (B200); found ") + prop.name);
+    auto* h = new vl_ctx();
+    Ctx& C = h->c;
+    C.device = device;
+    C.num_sms = prop.multiProcessorCount;
+    try {
+      // NULL selects the legacy default stream (same as torch's default stream)
+      C.stream = (cudaStream_t)stream;
+      C.own_stream = false;
+      C.red_partial.alloc(16u << 20);
+      C.red_counter.alloc(64 * sizeof(unsigned));
+      VL_CUDA(cudaMemsetAsync(C.red_counter.p, 0, 64 * sizeof(unsigned), C.stream));
+      C.dev_scalars.alloc(4096);
+      VL_CUDA(cudaMallocHost(&C.host_scalars, 4096));
+      VL_CUDA(cudaStreamSynchronize(C.stream));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int vl_ctx_destroy(vl_ctx* h) {
+  return guard([&] {
+    if (!h) return;
+    cudaSetDevice(h->c.device);
+    if (h->c.stream) cudaStreamSynchronize(h->c.stream);
+    if (h->c.host_scalars) cudaFreeHost(h->c.host_scalars);
+    if (h->c.own_stream) cudaStreamDestroy(h->c.stream);
+    delete h;
+  });
+}
+
+int vl_ctx_sync(vl_ctx* h) {
+  return guard([&] { VL_CUDA(cudaStreamSynchronize(h->c.stream)); });
+}
+
+int vl_ctx_info(vl_ctx* h, int64_t* info) {
+  return guard([&] {
+    info[0] = h->c.device;
+    info[1] = h->c.num_sms;
+  });
+}
+
+int vl_knn_previous(const double* xy, int64_t n, int d, int m, int32_t* out, int n_threads) {
+  return guard([&] {
+    if (n < 1 || d < 1 || m < 0) fail(kEConfig, "invalid knn sizes");
+    knn_previous(xy, n, d, m, out, n_threads);
+  });
+}
+
+int vl_pattern_create(vl_ctx* h, int64_t n, int d, int m, const double* xy, const int32_t* nbr, int order_kind,
+                      vl_pattern** out) {
+  return guard([&] {
+    if (!h || !out) fail(kEConfig, "null handle");
+    if (n < 1 || d < 1 || m < 0) fail(kEConfig, "invalid pattern sizes");
+    if (order_kind < 0 || order_kind > 2) fail(kEConfig, "unknown storage order");
+    VL_CUDA(cudaSetDevice(h->c.device));
+    auto* p = new vl_pattern();
+    p->ctx = h;
+    p->p.n = n;
+    p->p.d = d;
+    p->p.m = m;
+    p->p.order_kind = order_kind;
+    try {
+      std::vector<int32_t> empty;
+      const int32_t* nb = nbr;
+      if (m == 0) nb = empty.data();
+      pattern_upload(h->c, p->p, xy, nb);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
+int vl_pattern_destroy(vl_pattern* p) {
+  return guard([&] { delete p; });
+}
+
+int vl_pattern_perm(const vl_pattern* p, int32_t* out) {
+  return guard([&] { std::memcpy(out, p->p.sperm.data(), sizeof(int32_t) * p->p.n); });
+}
+
+int vl_pattern_info(const vl_pattern* p, int64_t* info) {
+  return guard([&] {
+    const Pattern& P = p->p;
+    info[0] = P.n;
+    info[1] = P.d;
+    info[2] = P.m;
+    info[3] = P.nnz_off;
+    info[4] = P.nlev_fwd;
+    info[5] = P.nlev_bwd;
+    info[6] = P.max_children;
+    info[7] = P.order_kind;
+  });
+}
+
+int vl_factor_build(vl_ctx* h, const vl_pattern* p, double sigma2, double rho, double nu, int want_grad,
+                    vl_factor** out) {
+  return guard([&] {
+    if (!h || !p || !out) fail(kEConfig, "null handle");
+    VL_CUDA(cudaSetDevice(h->c.device));
+    auto* f = new vl_factor();
+    try {
+      factor_build(h->c, p->p, f->f, sigma2, rho, nu, want_grad != 0);
+    } catch (...) {
+      delete f;
+      throw;
+    }
+    *out = f;
+  });
+}
+
+int vl_factor_destroy(vl_factor* f) {
+  return guard([&] { delete f; });
+}
+
+int vl_factor_get(vl_ctx* h, const vl_factor* f, int which, double* out) {
+  return guard([&] {
+    const Factor& F = f->f;
+    const Pattern& P = *F.pat;
+    const DevBuf* src = nullptr;
+    size_t cnt = P.n;
+    switch (which) {
+      case 0: src = &F.D; break;
+      case 1: src = &F.dD_sig; break;
+      case 2: src = &F.dD_rho; break;
+      case 3: src = &F.val; cnt = (size_t)P.n * P.m; break;
+      case 4: src = &F.dval; cnt = (size_t)P.n * P.m; break;
+      default: fail(kEConfig, "unknown factor field");
+    }
+    if ((which == 1 || which == 2 || which == 4) && !F.has_grad) fail(kEConfig, "factor was built without gradient");
+    if (cnt == 0) return;
+    VL_CUDA(cudaMemcpyAsync(out, src->p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, h->c.stream));
+    VL_CUDA(cudaStreamSynchronize(h->c.stream));
+  });
+}
+
+int vl_spmm(vl_ctx* h, const vl_factor* f, int op, int64_t t, const double* x, double* y) {
+  return guard([&] {
+    if (t < 1 || t > (1 << 20)) fail(kEConfig, "invalid column count");
+    op_spmm(h->c, f->f, op, (int)t, x, y);
+  });
+}
+
+int vl_sptrsv(vl_ctx* h, const vl_factor* f, int transpose, int64_t t, const double* x, double* y) {
+  return guard([&] {
+    if (t < 1 || t > (1 << 20)) fail(kEConfig, "invalid column count");
+    op_trsv(h->c, f->f, transpose != 0, (int)t, x, y);
+  });
+}
+
+}  // extern "C"

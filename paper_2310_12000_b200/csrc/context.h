@@ -1,0 +1,93 @@
+// Internal objects behind the opaque C-ABI handles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace vl {
+
+// Device buffer with RAII (the library owns its workspace; callers hand in
+// plain device pointers for inputs/outputs).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release();
+  void alloc(size_t nbytes);          // no-op when already large enough
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  std::string last_error;
+  // dependency flags for the triangular solves (epoch-tagged, never reset)
+  DevBuf flags;
+  int flag_epoch = 0;
+  // deterministic reduction scratch: per-block partials + ticket counters
+  DevBuf red_partial;   // doubles
+  DevBuf red_counter;   // unsigned ints (ring of slots)
+  int red_slot = 0;
+  // small pinned host staging for scalar read-back
+  double* host_scalars = nullptr;
+  DevBuf dev_scalars;
+  int next_flag_epoch() { return ++flag_epoch; }
+};
+
+// Sparsity pattern of the Vecchia factor + solve schedules (once per dataset).
+// Everything device-side is in STORAGE order: storage position s holds the
+// factor row sperm[s].  Vectors passed to kernels are n x t row-major in
+// storage order.
+struct Pattern {
+  int64_t n = 0;
+  int d = 0;
+  int m = 0;                // ELL width (max neighbour count)
+  int64_t nnz_off = 0;      // number of stored off-diagonal entries
+  int order_kind = 0;
+  std::vector<int32_t> sperm;   // storage -> factor
+  std::vector<int32_t> iperm;   // factor -> storage
+  std::vector<int32_t> fwd_level_ptr, bwd_level_ptr;
+  int nlev_fwd = 0, nlev_bwd = 0;
+  int max_children = 0;
+  // device
+  DevBuf xy;        // n*d  coords (storage order)
+  DevBuf nbr;       // n*m  int32 storage index of neighbour k (reference in-row order)
+  DevBuf cnt;       // n    int32 neighbour count
+  DevBuf fidx;      // n    int32 factor index of storage row
+  DevBuf fwd_order; // n    int32 storage rows in (level, position) order
+  DevBuf bwd_order; // n    int32 storage rows in (height, position) order
+  DevBuf tptr;      // n+1  int32 children CSR (= CSR of B^T) in storage order
+  DevBuf tidx;      // nnz  int32 child storage row
+  DevBuf tmap;      // nnz  int32 ELL slot (child*m + k) holding B[child, s]
+};
+
+// Factor values at one theta (device resident, storage order).
+struct Factor {
+  const Pattern* pat = nullptr;
+  double sigma2 = 0, rho = 0, nu = 0;
+  bool has_grad = false;
+  DevBuf val;     // n*m  ELL values of B's off-diagonal (-A_i), zero padded
+  DevBuf valT;    // nnz  values of B^T in children-CSR order
+  DevBuf D;       // n
+  DevBuf dval;    // n*m  d B / d rho (off-diagonal, zero padded)
+  DevBuf dD_rho;  // n
+  DevBuf dD_sig;  // n    d D / d sigma2 = D / sigma2
+  DevBuf err;     // 4 ints: [code, row(factor idx) ...]
+};
+
+}  // namespace vl

@@ -1,0 +1,334 @@
+// Vecchia factor build + theta-gradient (fused), one warp per row.
+//
+// Reference: vecchia.py:101-127 (_submatrices, Cholesky PD check),
+// vecchia.py:220-283 (build_factor: A = K^-1 k, D = sigma2 - k.A, D floor),
+// vecchia.py:286-337 (factor_gradient: dA = K^-1 (dk - dK A),
+// dD = dc(0) - dA.k - A.dk; sigma2: dB = 0, dD = D / sigma2).
+//
+// The reference solves with LU (np.linalg.solve) and uses Cholesky only as
+// a PD check; here the Cholesky factor is reused for both solves (the two
+// differ by rounding only).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "context.h"
+
+namespace vl {
+
+struct Matern {
+  double s2, rho, c;  // c = sqrt(3)/rho or sqrt(5)/rho or 1/rho (nu = 0.5 uses r / rho)
+  int nu;             // 0: 0.5, 1: 1.5, 2: 2.5
+  VL_D double val(double r) const {
+    if (nu == 0) return s2 * exp(-r / rho);
+    double u = c * r;
+    if (nu == 1) return s2 * (1.0 + u) * exp(-u);
+    return s2 * (1.0 + u + u * u / 3.0) * exp(-u);
+  }
+  VL_D double drho(double r) const {
+    if (nu == 0) {
+      double u = r / rho;
+      return s2 * exp(-u) * u / rho;
+    }
+    double u = c * r;
+    if (nu == 1) return s2 * u * u * exp(-u) / rho;
+    return s2 * u * u * (1.0 + u) * exp(-u) / (3.0 * rho);
+  }
+};
+
+template <int DIM>
+VL_D double pdist(const double* a, const double* b, int d) {
+  double s = 0.0;
+  if (DIM > 0) {
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) { double t = a[k] - b[k]; s += t * t; }
+  } else {
+    for (int k = 0; k < d; ++k) { double t = a[k] - b[k]; s += t * t; }
+  }
+  return sqrt(s);
+}
+
+// Per-warp scratch layout (doubles): X[mp*d] | L[mp*(mp+1)] | kv | dk | A | y | rhs | dA  (mp each)
+VL_HD size_t warp_scratch_doubles(int mp, int d) { return (size_t)mp * d + (size_t)mp * (mp + 1) + 6 * (size_t)mp; }
+
+// Forward then backward substitution with the Cholesky factor in Ls (row
+// stride ld): solves (L L^T) x = b.  b in bv (smem), x written to xv.  Lanes
+// own rows j = lane + 32 q.
+template <int Q>
+VL_D void chol_solve(const double* Ls, int ld, int c, const double* bv, double* yv, double* xv, int lane) {
+  double acc[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) acc[q] = 0.0;
+  for (int col = 0; col < c; ++col) {
+    // lane owning col finalises y_col
+    if ((col & 31) == lane) {
+      int q = col >> 5;
+      double a = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < Q; ++qq) if (qq == q) a = acc[qq];
+      yv[col] = (bv[col] - a) / Ls[col * ld + col];
+    }
+    __syncwarp();
+    double ycol = yv[col];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      int j = lane + 32 * q;
+      if (j > col && j < c) acc[q] += Ls[j * ld + col] * ycol;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < Q; ++q) acc[q] = 0.0;
+  for (int col = c - 1; col >= 0; --col) {
+    if ((col & 31) == lane) {
+      int q = col >> 5;
+      double a = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < Q; ++qq) if (qq == q) a = acc[qq];
+      xv[col] = (yv[col] - a) / Ls[col * ld + col];
+    }
+    __syncwarp();
+    double xcol = xv[col];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      int l = lane + 32 * q;
+      if (l < col) acc[q] += Ls[col * ld + l] * xcol;
+    }
+  }
+  __syncwarp();
+}
+
+template <int Q, int DIM>
+__global__ void __launch_bounds__(128) factor_build_kernel(
+    int64_t n, int d, int m, const double* __restrict__ xy, const int32_t* __restrict__ nbr,
+    const int32_t* __restrict__ cnt, const int32_t* __restrict__ fidx, Matern K, int want_grad,
+    double* __restrict__ val, double* __restrict__ Dout, double* __restrict__ dval,
+    double* __restrict__ dD_rho, double* __restrict__ dD_sig, int* __restrict__ err,
+    double* __restrict__ gscratch, int use_smem) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int mp = m > 0 ? m : 1;
+  const size_t per = warp_scratch_doubles(mp, d);
+  double* base = use_smem ? (smem + per * wib) : (gscratch + per * gw);
+  double* X = base;
+  double* L = X + (size_t)mp * d;
+  const int ld = mp + 1;
+  double* kv = L + (size_t)mp * ld;
+  double* dk = kv + mp;
+  double* A = dk + mp;
+  double* yv = A + mp;
+  double* rhs = yv + mp;
+  double* dA = rhs + mp;
+  const double dc0 = K.drho(0.0);
+
+  for (int64_t s = gw; s < n; s += nw) {
+    const int c = cnt[s];
+    const double* xi = xy + s * d;
+    if (c == 0) {
+      if (lane == 0) {
+        Dout[s] = K.s2;
+        if (want_grad) { dD_rho[s] = dc0; dD_sig[s] = K.s2 / K.s2; }
+      }
+      for (int j = lane; j < m; j += 32) {
+        val[s * m + j] = 0.0;
+        if (want_grad) dval[s * m + j] = 0.0;
+      }
+      continue;
+    }
+    // gather neighbour coordinates
+    for (int j = lane; j < c; j += 32) {
+      const double* xj = xy + (int64_t)nbr[s * m + j] * d;
+      for (int k = 0; k < d; ++k) X[j * d + k] = xj[k];
+    }
+    __syncwarp();
+    // K (lower triangle incl. diagonal) and k
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      int j = lane + 32 * q;
+      if (j < c) {
+        for (int l = 0; l <= j; ++l) L[j * ld + l] = K.val(pdist<DIM>(X + j * d, X + l * d, d));
+        double r = pdist<DIM>(X + j * d, xi, d);
+        kv[j] = K.val(r);
+        if (want_grad) dk[j] = K.drho(r);
+      }
+    }
+    __syncwarp();
+    // right-looking Cholesky
+    bool ok = true;
+    for (int col = 0; col < c; ++col) {
+      double piv = L[col * ld + col];
+      if (!(piv > 0.0)) { ok = false; break; }  // warp-uniform (same smem value)
+      double dp = sqrt(piv);
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        int j = lane + 32 * q;
+        if (j == col) L[j * ld + col] = dp;
+        else if (j > col && j < c) L[j * ld + col] /= dp;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        int j = lane + 32 * q;
+        if (j > col && j < c) {
+          double ljc = L[j * ld + col];
+          for (int l = col + 1; l <= j; ++l) L[j * ld + l] -= ljc * L[l * ld + col];
+        }
+      }
+      __syncwarp();
+    }
+    if (!ok) {
+      if (lane == 0) {
+        atomicMin(err + 1, fidx[s]);
+        atomicMax(err + 0, 1);
+      }
+      __syncwarp();
+      continue;
+    }
+    // A = K^-1 k ; D = sigma2 - k.A
+    chol_solve<Q>(L, ld, c, kv, yv, A, lane);
+    double part = 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      int j = lane + 32 * q;
+      if (j < c) part += kv[j] * A[j];
+    }
+    double kA = warp_sum(part);
+    double Ds = K.s2 - kA;
+    if (lane == 0) {
+      Dout[s] = Ds;
+      if (!(Ds >= 1e-10 * K.s2)) { atomicMin(err + 2, fidx[s]); atomicMax(err + 0, 1); }
+    }
+    for (int j = lane; j < m; j += 32) val[s * m + j] = (j < c) ? -A[j] : 0.0;
+    if (want_grad) {
+      // rhs_j = dk_j - sum_l dK[j,l] A_l   (full symmetric row; vecchia.py:318-321)
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        int j = lane + 32 * q;
+        if (j < c) {
+          double acc = 0.0;
+          for (int l = 0; l < c; ++l) acc += K.drho(pdist<DIM>(X + j * d, X + l * d, d)) * A[l];
+          rhs[j] = dk[j] - acc;
+        }
+      }
+      __syncwarp();
+      chol_solve<Q>(L, ld, c, rhs, yv, dA, lane);
+      double p1 = 0.0, p2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        int j = lane + 32 * q;
+        if (j < c) { p1 += dA[j] * kv[j]; p2 += A[j] * dk[j]; }
+      }
+      p1 = warp_sum(p1);
+      p2 = warp_sum(p2);
+      if (lane == 0) {
+        dD_rho[s] = dc0 + (-p1 - p2);
+        dD_sig[s] = Ds / K.s2;
+      }
+      for (int j = lane; j < m; j += 32) dval[s * m + j] = (j < c) ? -dA[j] : 0.0;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void gather_values_kernel(int64_t nnz, const int32_t* __restrict__ map, const double* __restrict__ src,
+                                     double* __restrict__ dst) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
+    dst[p] = src[map[p]];
+}
+
+template <int Q, int DIM>
+static void launch_build(Ctx& C, const Pattern& P, Factor& F, const Matern& K, int want_grad, double* gscr,
+                         int use_smem, size_t per) {
+  const int threads = 128;
+  const int wpb = threads / 32;
+  size_t smem = use_smem ? per * wpb * sizeof(double) : 0;
+  if (use_smem && smem > 48 * 1024)
+    VL_CUDA(cudaFuncSetAttribute(factor_build_kernel<Q, DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int blocks;
+  if (use_smem) {
+    int occ = 0;
+    VL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_build_kernel<Q, DIM>, threads, smem));
+    occ = occ > 0 ? occ : 1;
+    int64_t need = (P.n + wpb - 1) / wpb;
+    blocks = (int)std::min<int64_t>(need, (int64_t)occ * C.num_sms);
+  } else {
+    blocks = C.num_sms * 2;
+  }
+  if (blocks < 1) blocks = 1;
+  factor_build_kernel<Q, DIM><<<blocks, threads, smem, C.stream>>>(
+      P.n, P.d, P.m, P.xy.as<double>(), P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), P.fidx.as<int32_t>(), K, want_grad,
+      F.val.as<double>(), F.D.as<double>(), want_grad ? F.dval.as<double>() : nullptr,
+      want_grad ? F.dD_rho.as<double>() : nullptr, want_grad ? F.dD_sig.as<double>() : nullptr, F.err.as<int>(), gscr,
+      use_smem);
+  VL_LAUNCH_CHECK();
+}
+
+template <int Q>
+static void launch_build_q(Ctx& C, const Pattern& P, Factor& F, const Matern& K, int want_grad, double* gscr,
+                           int use_smem, size_t per) {
+  if (P.d == 2) launch_build<Q, 2>(C, P, F, K, want_grad, gscr, use_smem, per);
+  else if (P.d == 1) launch_build<Q, 1>(C, P, F, K, want_grad, gscr, use_smem, per);
+  else launch_build<Q, 0>(C, P, F, K, want_grad, gscr, use_smem, per);
+}
+
+// Build (B, D) and optionally d/d(sigma2, rho); errors -> FactorizationError
+void factor_build(Ctx& C, const Pattern& P, Factor& F, double sigma2, double rho, double nu, bool want_grad) {
+  Matern K;
+  K.s2 = sigma2;
+  K.rho = rho;
+  if (nu == 0.5) { K.nu = 0; K.c = 1.0 / rho; }
+  else if (nu == 1.5) { K.nu = 1; K.c = sqrt(3.0) / rho; }
+  else if (nu == 2.5) { K.nu = 2; K.c = sqrt(5.0) / rho; }
+  else fail(kEConfig, "smoothness nu must be one of (0.5, 1.5, 2.5)");
+  if (!(sigma2 > 0)) fail(kEConfig, "sigma2 must be > 0");
+  if (!(rho > 0)) fail(kEConfig, "rho must be > 0");
+  F.pat = &P;
+  F.sigma2 = sigma2;
+  F.rho = rho;
+  F.nu = nu;
+  F.has_grad = want_grad;
+  const int64_t n = P.n;
+  const int mm = std::max(P.m, 1);
+  F.val.alloc(sizeof(double) * n * mm);
+  F.D.alloc(sizeof(double) * n);
+  F.valT.alloc(sizeof(double) * std::max<int64_t>(P.nnz_off, 1));
+  F.err.alloc(sizeof(int) * 4);
+  if (want_grad) {
+    F.dval.alloc(sizeof(double) * n * mm);
+    F.dD_rho.alloc(sizeof(double) * n);
+    F.dD_sig.alloc(sizeof(double) * n);
+  }
+  int h_err[4] = {0, INT32_MAX, INT32_MAX, 0};
+  VL_CUDA(cudaMemcpyAsync(F.err.p, h_err, sizeof(h_err), cudaMemcpyHostToDevice, C.stream));
+  const int mp = mm;
+  const size_t per = warp_scratch_doubles(mp, P.d);
+  const int use_smem = (per * 4 * sizeof(double) <= 200 * 1024) ? 1 : 0;
+  DevBuf gscr;
+  if (!use_smem) gscr.alloc(per * sizeof(double) * (size_t)C.num_sms * 2 * 4);
+  double* g = gscr.as<double>();
+  if (mp <= 32) launch_build_q<1>(C, P, F, K, want_grad, g, use_smem, per);
+  else if (mp <= 64) launch_build_q<2>(C, P, F, K, want_grad, g, use_smem, per);
+  else if (mp <= 128) launch_build_q<4>(C, P, F, K, want_grad, g, use_smem, per);
+  else if (mp <= 256) launch_build_q<8>(C, P, F, K, want_grad, g, use_smem, per);
+  else fail(kECapacity, "m > 256 neighbours is not supported");
+  if (P.nnz_off > 0) {
+    int blocks = C.num_sms * 8;
+    gather_values_kernel<<<blocks, 256, 0, C.stream>>>(P.nnz_off, P.tmap.as<int32_t>(), F.val.as<double>(),
+                                                       F.valT.as<double>());
+    VL_LAUNCH_CHECK();
+  }
+  VL_CUDA(cudaMemcpyAsync(h_err, F.err.p, sizeof(h_err), cudaMemcpyDeviceToHost, C.stream));
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+  if (h_err[0]) {
+    if (h_err[1] != INT32_MAX)
+      fail(kEFactorization, "neighbor covariance submatrix of point " + std::to_string(h_err[1]) +
+                                " (factor order) is not positive definite (near-duplicate locations?)");
+    fail(kEFactorization, "conditional variance D_" + std::to_string(h_err[2]) +
+                              " below 1e-10 * sigma2 (near-duplicate inputs)");
+  }
+}
+
+}  // namespace vl

@@ -1,0 +1,84 @@
+// Kernel-level operators on a factor: B x, B^T x, dB x, B^-1 x, B^-T x.
+// (vecchia.py:161-192 solve_B / apply_precision / apply_sigma_tilde and the
+//  csr/csc matvecs they call.)  All vectors are n x t row-major, storage order.
+#include <map>
+#include <mutex>
+
+#include "bodies.cuh"
+#include "launch.cuh"
+#include "ops.h"
+
+namespace vl {
+
+unsigned* next_counter(Ctx& C) {
+  unsigned* base = C.red_counter.as<unsigned>();
+  int slot = C.red_slot;
+  C.red_slot = (C.red_slot + 1) & 63;
+  return base + slot;
+}
+
+void ensure_flags(Ctx& C, int64_t n) {
+  size_t need = sizeof(int) * (size_t)std::max<int64_t>(n, 1);
+  if (C.flags.bytes < need) {
+    C.flags.alloc(need);
+    VL_CUDA(cudaMemsetAsync(C.flags.p, 0, need, C.stream));
+    C.flag_epoch = 0;
+  }
+}
+
+int coop_grid(Ctx& C, const void* func, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, size_t>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(func, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int occ = 0;
+  VL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, func, kRowsThreads, smem));
+  if (occ < 1) fail(kEInternal, "triangular-solve kernel cannot be made resident");
+  int g = occ * C.num_sms;
+  cache[key] = g;
+  return g;
+}
+
+BView bview(const Factor& F, bool grad) {
+  const Pattern& P = *F.pat;
+  BView v;
+  v.nbr = P.nbr.as<int32_t>();
+  v.cnt = P.cnt.as<int32_t>();
+  v.val = grad ? F.dval.as<double>() : F.val.as<double>();
+  v.tptr = P.tptr.as<int32_t>();
+  v.tidx = P.tidx.as<int32_t>();
+  v.valT = F.valT.as<double>();
+  v.m = P.m;
+  return v;
+}
+
+void op_spmm(Ctx& C, const Factor& F, int op, int t, const double* x, double* y) {
+  const Pattern& P = *F.pat;
+  if (op == 2 && !F.has_grad) fail(kEConfig, "factor was built without gradient");
+  dispatch_t(t, [&](auto g, auto nc) {
+    constexpr int G = decltype(g)::value, NC = decltype(nc)::value;
+    if (op == 0) launch_rows<G, NC, 0, 0>(C, P.n, t, BodyBx{bview(F, false), x, y}, Fin0<0>{});
+    else if (op == 1) launch_rows<G, NC, 0, 0>(C, P.n, t, BodyBtx{bview(F, false), x, y}, Fin0<0>{});
+    else if (op == 2) launch_rows<G, NC, 0, 0>(C, P.n, t, BodyDBx{bview(F, true), x, y}, Fin0<0>{});
+    else fail(kEConfig, "unknown product op");
+  });
+}
+
+void op_trsv(Ctx& C, const Factor& F, bool transpose, int t, const double* b, double* x) {
+  const Pattern& P = *F.pat;
+  if (b == x) fail(kEConfig, "triangular solve cannot run in place");
+  dispatch_t(t, [&](auto g, auto nc) {
+    constexpr int G = decltype(g)::value, NC = decltype(nc)::value;
+    if (!transpose) {
+      DepsEll deps{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
+      launch_trsv<G, NC, 0>(C, P.n, t, P.fwd_order.as<int32_t>(), deps, x, TrsvPlain{b, t}, Fin0<0>{});
+    } else {
+      DepsCsr deps{P.tptr.as<int32_t>(), P.tidx.as<int32_t>(), F.valT.as<double>()};
+      launch_trsv<G, NC, 0>(C, P.n, t, P.bwd_order.as<int32_t>(), deps, x, TrsvPlain{b, t}, Fin0<0>{});
+    }
+  });
+}
+
+}  // namespace vl
