@@ -86,6 +86,9 @@ int vl_factor_destroy(vl_factor* f);
 /* which: 0 D, 1 dD/dsigma2, 2 dD/drho (n doubles); 3 B off-diagonal ELL values,
  * 4 dB/drho ELL values (n*m doubles, storage order, zero padded) */
 int vl_factor_get(vl_ctx* ctx, const vl_factor* f, int which, double* host_out);
+/* overwrite one field from host values (same layout as vl_factor_get); used to
+ * replay externally computed factors (kernel-level parity on identical B). */
+int vl_factor_set(vl_ctx* ctx, vl_factor* f, int which, const double* host_in);
 
 /* ---- kernel-level operators (device pointers, n x t, storage order) -------
  * op: 0 -> y = B x, 1 -> y = B^T x, 2 -> y = (dB/drho) x

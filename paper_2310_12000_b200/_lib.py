@@ -13,7 +13,7 @@ import threading
 from .errors import STATUS, DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvlgpx.so")
+LIB_PATH = os.environ.get("VLGPX_LIB") or os.path.join(_HERE, "libvlgpx.so")
 
 _lock = threading.Lock()
 _lib = None
@@ -39,6 +39,7 @@ _SIGS = {
     "vl_factor_build": [c_void_p, c_void_p, c_double, c_double, c_double, c_int, C.POINTER(c_void_p)],
     "vl_factor_destroy": [c_void_p],
     "vl_factor_get": [c_void_p, c_void_p, c_int, c_void_p],
+    "vl_factor_set": [c_void_p, c_void_p, c_int, c_void_p],
     "vl_spmm": [c_void_p, c_void_p, c_int, c_int64, c_void_p, c_void_p],
     "vl_sptrsv": [c_void_p, c_void_p, c_int, c_int64, c_void_p, c_void_p],
 }

@@ -35,14 +35,14 @@ def sources():
     return sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
 
 
-def _compile(src, verbose_ptxas=False):
-    obj = os.path.join(OUT_DIR, src + ".o")
+def _compile(src, verbose_ptxas=False, defines=(), out_dir=OUT_DIR):
+    obj = os.path.join(out_dir, src + ".o")
     path = os.path.join(CSRC, src)
     deps = [path] + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))]
     deps.append(os.path.join(HERE, "..", "include", "vlgpx.h"))
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj, ""
-    cmd = [nvcc(), *ARCH, *COMMON, "-c", path, "-o", obj]
+    cmd = [nvcc(), *ARCH, *COMMON, *[f"-D{d}" for d in defines], "-c", path, "-o", obj]
     if src.endswith(".cpp"):
         cmd[1:1] = ["-x", "cu"]  # host sources share the device headers
     if verbose_ptxas and src.endswith(".cu"):
@@ -53,24 +53,25 @@ def _compile(src, verbose_ptxas=False):
     return obj, r.stderr
 
 
-def build(verbose=False, jobs=None):
-    os.makedirs(OUT_DIR, exist_ok=True)
+def build(verbose=False, jobs=None, defines=(), lib=LIB):
+    out_dir = OUT_DIR if not defines else OUT_DIR + "_" + "_".join(d.replace("=", "") for d in defines)
+    os.makedirs(out_dir, exist_ok=True)
     srcs = sources()
     jobs = jobs or min(len(srcs), os.cpu_count() or 4)
     with cf.ThreadPoolExecutor(jobs) as ex:
-        results = list(ex.map(lambda s: _compile(s, verbose), srcs))
+        results = list(ex.map(lambda s: _compile(s, verbose, defines, out_dir), srcs))
     objs = [o for o, _ in results]
     if verbose:
         for (o, log), s in zip(results, srcs):
             if log:
                 print(f"--- {s}\n{log}")
     newest = max(os.path.getmtime(o) for o in objs)
-    if not (os.path.exists(LIB) and os.path.getmtime(LIB) >= newest):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-Xcompiler", "-pthread"]
+    if not (os.path.exists(lib) and os.path.getmtime(lib) >= newest):
+        cmd = [nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-lcudart", "-Xcompiler", "-pthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -40,17 +42,65 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
   }
 }
 
+// Caching device allocator: factor / workspace buffers are re-created for
+// every theta of a fit, so blocks go back to a per-(device, size) free list
+// instead of cudaFree (which would synchronise the device).  All library work
+// is ordered on one stream, so stream-ordered reuse is safe.
+namespace {
+std::mutex g_pool_mu;
+std::multimap<std::pair<int, size_t>, void*> g_pool;
+
+void* pool_get(size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto it = g_pool.find({dev, bytes});
+    if (it != g_pool.end()) {
+      void* p = it->second;
+      g_pool.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    // release cached blocks of this device and retry once
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (auto it = g_pool.begin(); it != g_pool.end();) {
+      if (it->first.first == dev) { cudaFree(it->second); it = g_pool.erase(it); }
+      else ++it;
+    }
+    VL_CUDA(cudaMalloc(&p, bytes));
+  }
+  return p;
+}
+
+void pool_put(void* p, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  g_pool.insert({{dev, bytes}, p});
+}
+
+size_t round_bytes(size_t b) {
+  if (b <= 4096) return 4096;
+  return (b + (1u << 20) - 1) & ~(size_t)((1u << 20) - 1);  // 1 MiB granularity
+}
+}  // namespace
+
 void DevBuf::release() {
-  if (p) cudaFree(p);
+  if (p) pool_put(p, bytes);
   p = nullptr;
   bytes = 0;
 }
 void DevBuf::alloc(size_t nbytes) {
   if (nbytes <= bytes && p) return;
   release();
-  if (nbytes == 0) nbytes = 8;
-  VL_CUDA(cudaMalloc(&p, nbytes));
-  bytes = nbytes;
+  size_t r = round_bytes(nbytes);
+  p = pool_get(r);
+  bytes = r;
 }
 
 template <class F>
@@ -92,7 +142,8 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
   upload(C, P.tptr, tptr);
   upload(C, P.tidx, tidx);
   upload(C, P.tmap, tmap);
-  ensure_flags(C, P.n);
+  P.fwd_len = (int64_t)fwd.size();
+  P.bwd_len = (int64_t)bwd.size();
   VL_CUDA(cudaStreamSynchronize(C.stream));
 }
 
@@ -119,6 +170,8 @@ int vl_ctx_create(int device, void* stream, vl_ctx** out) {
     Ctx& C = h->c;
     C.device = device;
     C.num_sms = prop.multiProcessorCount;
+    if (const char* e = std::getenv("VL_TRSV_BPS")) C.trsv_blocks_per_sm = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("VL_SPIN_MAX_NS")) C.spin_max_ns = std::max(0, std::atoi(e));
     try {
       // NULL selects the legacy default stream (same as torch's default stream)
       C.stream = (cudaStream_t)stream;
@@ -255,17 +308,45 @@ int vl_factor_get(vl_ctx* h, const vl_factor* f, int which, double* out) {
   });
 }
 
+int vl_factor_set(vl_ctx* h, vl_factor* f, int which, const double* in) {
+  return guard([&] {
+    Factor& F = f->f;
+    const Pattern& P = *F.pat;
+    DevBuf* dst = nullptr;
+    size_t cnt = P.n;
+    switch (which) {
+      case 0: dst = &F.D; break;
+      case 1: dst = &F.dD_sig; break;
+      case 2: dst = &F.dD_rho; break;
+      case 3: dst = &F.val; cnt = (size_t)P.n * P.m; break;
+      case 4: dst = &F.dval; cnt = (size_t)P.n * P.m; break;
+      default: fail(kEConfig, "unknown factor field");
+    }
+    if ((which == 1 || which == 2 || which == 4) && !F.has_grad) fail(kEConfig, "factor was built without gradient");
+    if (cnt == 0) return;
+    VL_CUDA(cudaMemcpyAsync(dst->p, in, sizeof(double) * cnt, cudaMemcpyHostToDevice, h->c.stream));
+    if (which == 3) factor_refresh_transpose(h->c, F);
+    VL_CUDA(cudaStreamSynchronize(h->c.stream));
+  });
+}
+
+// debug hook (not in the public header): record per-row completion times of
+// subsequent triangular solves into a device buffer of n int64 (NULL disables)
+int vl_debug_set_tstamp(vl_ctx* h, void* dev_buf) {
+  return guard([&] { h->c.debug_tstamp = (long long*)dev_buf; });
+}
+
 int vl_spmm(vl_ctx* h, const vl_factor* f, int op, int64_t t, const double* x, double* y) {
   return guard([&] {
     if (t < 1 || t > (1 << 20)) fail(kEConfig, "invalid column count");
-    op_spmm(h->c, f->f, op, (int)t, x, y);
+    op_spmm(h->c, f->f, op, (int)t, (int)t, x, y);
   });
 }
 
 int vl_sptrsv(vl_ctx* h, const vl_factor* f, int transpose, int64_t t, const double* x, double* y) {
   return guard([&] {
     if (t < 1 || t > (1 << 20)) fail(kEConfig, "invalid column count");
-    op_trsv(h->c, f->f, transpose != 0, (int)t, x, y);
+    op_trsv(h->c, f->f, transpose != 0, (int)t, (int)t, x, y);
   });
 }
 

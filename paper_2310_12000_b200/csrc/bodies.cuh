@@ -1,8 +1,12 @@
 // Row bodies shared by the kernels: gathers over the rows of B (ELL, storage
-// order) and over the children CSR of B^T.
+// order) and over the children CSR of B^T, with 16-byte column units and a
+// 4-way unrolled entry loop (4 x NU independent gathers in flight per lane;
+// index/weight loads are uniform across the G lanes of a group -> L1
+// broadcast).
 #pragma once
 
 #include "common.cuh"
+#include "rows.cuh"
 
 namespace vl {
 
@@ -17,61 +21,135 @@ struct BView {
   int m;
 };
 
-// acc[k] += sum_e B[s, j_e] * load(j_e, c)   (off-diagonal part only)
-template <int G, int NC, class Load>
-VL_D void gather_B(const BView& B, int64_t s, int gl, int t, const Load& load, double (&acc)[NC]) {
-  const int cs = B.cnt[s];
-  const int32_t* nb = B.nbr + s * B.m;
-  const double* vv = B.val + s * B.m;
-  for (int e = 0; e < cs; ++e) {
-    const int32_t j = nb[e];
-    const double w = vv[e];
-#pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      int c = gl + G * k;
-      if (c < t) acc[k] += w * load(j, c);
-    }
-  }
-}
-
-// acc[k] += sum_{children i of s} B[i, s] * load(i, c)
-template <int G, int NC, class Load>
-VL_D void gather_Bt(const BView& B, int64_t s, int gl, int t, const Load& load, double (&acc)[NC]) {
-  const int e0 = B.tptr[s], e1 = B.tptr[s + 1];
-  for (int e = e0; e < e1; ++e) {
-    const int32_t i = B.tidx[e];
-    const double w = B.valT[e];
-#pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      int c = gl + G * k;
-      if (c < t) acc[k] += w * load(i, c);
-    }
-  }
-}
-
-struct LoadVec {
+// Strided vector view: x[row * ld + col]
+struct VecView {
   const double* x;
-  int t;
-  VL_D double operator()(int64_t j, int c) const { return x[j * t + c]; }
+  int ld;
 };
 
+// acc[i] += sum_e w_e * X[j_e, col(i)] over entries [0, cs) given by idx/wt.
+template <int G, int NU, int U, class Idx, class Wt, class Load>
+VL_D void gather(int cs, int gl, int t, const Idx& idx, const Wt& wt, const Load& load, double (&acc)[NU * U]) {
+  int e = 0;
+  for (; e + 4 <= cs; e += 4) {
+    int32_t j[4];
+    double w[4];
+    double v[4][NU * U];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { j[q] = idx(e + q); w[q] = wt(e + q); }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int k = 0; k < NU; ++k) {
+        const int c = U * (gl + G * k);
+        if (c < t) load(j[q], c, &v[q][U * k]);
+        else
+#pragma unroll
+          for (int i = 0; i < U; ++i) v[q][U * k + i] = 0.0;
+      }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int i = 0; i < NU * U; ++i) acc[i] += w[q] * v[q][i];
+  }
+  for (; e < cs; ++e) {
+    const int32_t j = idx(e);
+    const double w = wt(e);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+      const int c = U * (gl + G * k);
+      if (c < t) {
+        double v[U];
+        load(j, c, v);
+#pragma unroll
+        for (int i = 0; i < U; ++i) acc[U * k + i] += w * v[i];
+      }
+    }
+  }
+}
+
+// unit loader from a strided vector (read-only path)
+template <int U>
+struct LoadU {
+  const double* x;
+  int ld;
+  VL_D void operator()(int64_t j, int c, double* out) const { load_unit<U>(x + j * ld + c, out); }
+};
+
+// acc += (off-diagonal of B row s) . X      (B row: ELL, in reference order)
+template <int G, int NU, int U, class Load>
+VL_D void gather_B(const BView& B, const double* vals, int64_t s, bool valid, int gl, int t, const Load& load,
+                   double (&acc)[NU * U]) {
+  const int cs = valid ? B.cnt[s] : 0;
+  const int32_t* nb = B.nbr + (valid ? s : 0) * B.m;
+  const double* vv = vals + (valid ? s : 0) * B.m;
+  gather<G, NU, U>(
+      cs, gl, t, [&](int e) { return nb[e]; }, [&](int e) { return vv[e]; }, load, acc);
+}
+
+// acc += (column s of B's off-diagonal) . X   (children CSR)
+template <int G, int NU, int U, class Load>
+VL_D void gather_Bt(const BView& B, int64_t s, bool valid, int gl, int t, const Load& load, double (&acc)[NU * U]) {
+  const int e0 = valid ? B.tptr[s] : 0;
+  const int cs = valid ? B.tptr[s + 1] - e0 : 0;
+  const int32_t* ti = B.tidx + e0;
+  const double* tv = B.valT + e0;
+  gather<G, NU, U>(
+      cs, gl, t, [&](int e) { return ti[e]; }, [&](int e) { return tv[e]; }, load, acc);
+}
+
+template <int NC>
+VL_D void zero(double (&a)[NC]) {
+#pragma unroll
+  for (int k = 0; k < NC; ++k) a[k] = 0.0;
+}
+
+// store the lane's columns of row s
+template <int G, int NU, int U>
+VL_D void store_row(double* y, int ld, int64_t s, int gl, int t, const double (&a)[NU * U]) {
+#pragma unroll
+  for (int k = 0; k < NU; ++k) {
+    const int c = U * (gl + G * k);
+    if (c < t) {
+      if constexpr (U == 2) *reinterpret_cast<double2*>(y + s * ld + c) = make_double2(a[2 * k], a[2 * k + 1]);
+      else y[s * ld + c] = a[k];
+    }
+  }
+}
+
+template <int G, int NU, int U>
+VL_D void load_row(const double* x, int ld, int64_t s, int gl, int t, double (&a)[NU * U]) {
+#pragma unroll
+  for (int k = 0; k < NU; ++k) {
+    const int c = U * (gl + G * k);
+    if (c < t) load_unit<U>(x + s * ld + c, &a[U * k]);
+    else
+#pragma unroll
+      for (int i = 0; i < U; ++i) a[U * k + i] = 0.0;
+  }
+}
+
 // ---- plain products ---------------------------------------------------------
-struct BodyBx {  // y = B x
+struct BodyBx {  // y = B x  (op 0) or y = dB x (op 2: no unit diagonal)
   BView B;
+  const double* vals;
   const double* x;
   double* y;
-  template <int G, int NC, int NR>
-  VL_D void run(int64_t s, bool valid, int gl, int t, double (&)[NR][NC]) const {
+  int ld;
+  int unit_diag;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&)[NR][NU * U]) const {
+    double a[NU * U];
+    zero(a);
+    gather_B<G, NU, U>(B, vals, s, valid, gl, t, LoadU<U>{x, ld}, a);
     if (!valid) return;
-    double a[NC];
+    if (unit_diag) {
+      double xs[NU * U];
+      load_row<G, NU, U>(x, ld, s, gl, t, xs);
 #pragma unroll
-    for (int k = 0; k < NC; ++k) a[k] = 0.0;
-    gather_B<G, NC>(B, s, gl, t, LoadVec{x, t}, a);
-#pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      int c = gl + G * k;
-      if (c < t) y[s * t + c] = x[s * t + c] + a[k];
+      for (int i = 0; i < NU * U; ++i) a[i] += xs[i];
     }
+    store_row<G, NU, U>(y, ld, s, gl, t, a);
   }
 };
 
@@ -79,46 +157,26 @@ struct BodyBtx {  // y = B^T x
   BView B;
   const double* x;
   double* y;
-  template <int G, int NC, int NR>
-  VL_D void run(int64_t s, bool valid, int gl, int t, double (&)[NR][NC]) const {
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&)[NR][NU * U]) const {
+    double a[NU * U];
+    zero(a);
+    gather_Bt<G, NU, U>(B, s, valid, gl, t, LoadU<U>{x, ld}, a);
     if (!valid) return;
-    double a[NC];
+    double xs[NU * U];
+    load_row<G, NU, U>(x, ld, s, gl, t, xs);
 #pragma unroll
-    for (int k = 0; k < NC; ++k) a[k] = 0.0;
-    gather_Bt<G, NC>(B, s, gl, t, LoadVec{x, t}, a);
-#pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      int c = gl + G * k;
-      if (c < t) y[s * t + c] = x[s * t + c] + a[k];
-    }
-  }
-};
-
-// dB x with dB sharing B's pattern (no diagonal)
-struct BodyDBx {
-  BView dB;
-  const double* x;
-  double* y;
-  template <int G, int NC, int NR>
-  VL_D void run(int64_t s, bool valid, int gl, int t, double (&)[NR][NC]) const {
-    if (!valid) return;
-    double a[NC];
-#pragma unroll
-    for (int k = 0; k < NC; ++k) a[k] = 0.0;
-    gather_B<G, NC>(dB, s, gl, t, LoadVec{x, t}, a);
-#pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      int c = gl + G * k;
-      if (c < t) y[s * t + c] = a[k];
-    }
+    for (int i = 0; i < NU * U; ++i) a[i] += xs[i];
+    store_row<G, NU, U>(y, ld, s, gl, t, a);
   }
 };
 
 // ---- plain triangular solves -------------------------------------------------
 struct TrsvPlain {
   const double* b;
-  int t;
-  VL_D double rhs(int64_t s, int c, double&) const { return b[s * t + c]; }
+  int ld;
+  VL_D double rhs(int64_t s, int c, double&) const { return b[s * ld + c]; }
   VL_D void out(int64_t, int, double, double&) const {}
 };
 

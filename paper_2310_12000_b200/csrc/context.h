@@ -36,9 +36,12 @@ struct Ctx {
   bool own_stream = false;
   int num_sms = 148;
   std::string last_error;
-  // dependency flags for the triangular solves (epoch-tagged, never reset)
-  DevBuf flags;
-  int flag_epoch = 0;
+  // CTAs per SM for the dependency-driven solves (bounds the spinning warps)
+  int trsv_blocks_per_sm = 2;
+  // max nanosleep backoff while spinning on a dependency (0 = pure polling)
+  int spin_max_ns = 64;
+  // debug: per-row completion timestamps of the next triangular solves (n entries)
+  long long* debug_tstamp = nullptr;
   // deterministic reduction scratch: per-block partials + ticket counters
   DevBuf red_partial;   // doubles
   DevBuf red_counter;   // unsigned ints (ring of slots)
@@ -46,7 +49,6 @@ struct Ctx {
   // small pinned host staging for scalar read-back
   double* host_scalars = nullptr;
   DevBuf dev_scalars;
-  int next_flag_epoch() { return ++flag_epoch; }
 };
 
 // Sparsity pattern of the Vecchia factor + solve schedules (once per dataset).
@@ -69,8 +71,9 @@ struct Pattern {
   DevBuf nbr;       // n*m  int32 storage index of neighbour k (reference in-row order)
   DevBuf cnt;       // n    int32 neighbour count
   DevBuf fidx;      // n    int32 factor index of storage row
-  DevBuf fwd_order; // n    int32 storage rows in (level, position) order
-  DevBuf bwd_order; // n    int32 storage rows in (height, position) order
+  DevBuf fwd_order; // fwd_len int32 storage rows in (level, position) order, levels padded to 32 with -1
+  DevBuf bwd_order; // bwd_len int32 storage rows in (height, position) order, padded likewise
+  int64_t fwd_len = 0, bwd_len = 0;
   DevBuf tptr;      // n+1  int32 children CSR (= CSR of B^T) in storage order
   DevBuf tidx;      // nnz  int32 child storage row
   DevBuf tmap;      // nnz  int32 ELL slot (child*m + k) holding B[child, s]

@@ -239,6 +239,16 @@ __global__ void gather_values_kernel(int64_t nnz, const int32_t* __restrict__ ma
     dst[p] = src[map[p]];
 }
 
+void factor_refresh_transpose(Ctx& C, Factor& F) {
+  const Pattern& P = *F.pat;
+  if (P.nnz_off > 0) {
+    int blocks = C.num_sms * 8;
+    gather_values_kernel<<<blocks, 256, 0, C.stream>>>(P.nnz_off, P.tmap.as<int32_t>(), F.val.as<double>(),
+                                                       F.valT.as<double>());
+    VL_LAUNCH_CHECK();
+  }
+}
+
 template <int Q, int DIM>
 static void launch_build(Ctx& C, const Pattern& P, Factor& F, const Matern& K, int want_grad, double* gscr,
                          int use_smem, size_t per) {
@@ -314,12 +324,7 @@ void factor_build(Ctx& C, const Pattern& P, Factor& F, double sigma2, double rho
   else if (mp <= 128) launch_build_q<4>(C, P, F, K, want_grad, g, use_smem, per);
   else if (mp <= 256) launch_build_q<8>(C, P, F, K, want_grad, g, use_smem, per);
   else fail(kECapacity, "m > 256 neighbours is not supported");
-  if (P.nnz_off > 0) {
-    int blocks = C.num_sms * 8;
-    gather_values_kernel<<<blocks, 256, 0, C.stream>>>(P.nnz_off, P.tmap.as<int32_t>(), F.val.as<double>(),
-                                                       F.valT.as<double>());
-    VL_LAUNCH_CHECK();
-  }
+  factor_refresh_transpose(C, F);
   VL_CUDA(cudaMemcpyAsync(h_err, F.err.p, sizeof(h_err), cudaMemcpyDeviceToHost, C.stream));
   VL_CUDA(cudaStreamSynchronize(C.stream));
   if (h_err[0]) {

@@ -1,6 +1,8 @@
-// Launch helpers: (G, NC) dispatch by column count, rows/trsv launchers.
+// Launch helpers: (G, NU, U) dispatch by column count / leading dimension,
+// rows/trsv launchers.
 #pragma once
 
+#include <algorithm>
 #include <type_traits>
 
 #include "context.h"
@@ -11,29 +13,37 @@ namespace vl {
 template <int V>
 using IC = std::integral_constant<int, V>;
 
-// Lanes-per-row G and columns-per-lane NC for a given t.
+// Column layout of an n x ld block holding t <= ld columns.
+//   U  = 2 (16-byte units) when ld is even and t > 1, else 1
+//   G  = lanes per row = min(32, pow2ceil(#units))
+//   NU = units per lane
 template <class F>
-void dispatch_t(int t, F&& f) {
-  if (t <= 0) fail(kEConfig, "column count must be >= 1");
-  if (t == 1) f(IC<1>{}, IC<1>{});
-  else if (t <= 2) f(IC<2>{}, IC<1>{});
-  else if (t <= 4) f(IC<4>{}, IC<1>{});
-  else if (t <= 8) f(IC<8>{}, IC<1>{});
-  else if (t <= 16) f(IC<16>{}, IC<1>{});
-  else if (t <= 32) f(IC<32>{}, IC<1>{});
-  else if (t <= 64) f(IC<32>{}, IC<2>{});
-  else if (t <= 128) f(IC<32>{}, IC<4>{});
-  else fail(kECapacity, "more than 128 right-hand sides per call are not supported; shard the probes");
+void dispatch_cols(int t, int ld, F&& f) {
+  if (t <= 0 || ld < t) fail(kEConfig, "invalid column count / leading dimension");
+  const bool pair = (t > 1) && (ld % 2 == 0);
+  const int units = pair ? (t + 1) / 2 : t;
+  auto go = [&](auto u) {
+    constexpr int U = decltype(u)::value;
+    if (units == 1) f(IC<1>{}, IC<1>{}, IC<U>{});
+    else if (units <= 2) f(IC<2>{}, IC<1>{}, IC<U>{});
+    else if (units <= 4) f(IC<4>{}, IC<1>{}, IC<U>{});
+    else if (units <= 8) f(IC<8>{}, IC<1>{}, IC<U>{});
+    else if (units <= 16) f(IC<16>{}, IC<1>{}, IC<U>{});
+    else if (units <= 32) f(IC<32>{}, IC<1>{}, IC<U>{});
+    else if (units <= 64) f(IC<32>{}, IC<2>{}, IC<U>{});
+    else fail(kECapacity, "more than 128 right-hand sides per call are not supported; shard the probes");
+  };
+  if (pair) go(IC<2>{});
+  else go(IC<1>{});
 }
 
 unsigned* next_counter(Ctx& C);
-void ensure_flags(Ctx& C, int64_t n);
 int coop_grid(Ctx& C, const void* func, size_t smem);
 
-template <int G, int NC, int NR, int MAXMASK, class Body, class Fin>
+template <int G, int NU, int U, int NR, int MAXMASK, class Body, class Fin>
 void launch_rows(Ctx& C, int64_t n, int t, const Body& body, const Fin& fin, const int* gate = nullptr) {
-  auto kern = rows_kernel<G, NC, NR, MAXMASK, Body, Fin>;
-  const size_t smem = red_smem_bytes<G, NC, NR>(kRowsThreads, t);
+  auto kern = rows_kernel<G, NU, U, NR, MAXMASK, Body, Fin>;
+  const size_t smem = red_smem_bytes<G, NU, U, NR>(kRowsThreads, t);
   int64_t need = (n * G + kRowsThreads - 1) / kRowsThreads;
   int64_t cap = (int64_t)C.num_sms * (2048 / kRowsThreads);
   int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
@@ -41,21 +51,24 @@ void launch_rows(Ctx& C, int64_t n, int t, const Body& body, const Fin& fin, con
   VL_LAUNCH_CHECK();
 }
 
-template <int G, int NC, int NR, class Deps, class Body, class Fin>
-void launch_trsv(Ctx& C, int64_t n, int t, const int32_t* order, const Deps& deps, double* x, const Body& body,
-                 const Fin& fin, const int* gate = nullptr) {
-  auto kern = trsv_kernel<G, NC, NR, Deps, Body, Fin>;
-  const size_t smem = red_smem_bytes<G, NC, NR>(kRowsThreads, t);
-  ensure_flags(C, n);
+// x (n x ld) is overwritten: it is first filled with the "not ready" sentinel.
+template <int G, int NU, int U, int NR, class Deps, class Body, class Fin>
+void launch_trsv(Ctx& C, int64_t n, int64_t npos, int t, int ld, const int32_t* order, const Deps& deps, double* x,
+                 const Body& body, const Fin& fin, const int* gate = nullptr) {
+  auto kern = trsv_kernel<G, NU, U, NR, Deps, Body, Fin>;
+  const size_t smem = red_smem_bytes<G, NU, U, NR>(kRowsThreads, t);
   int grid = coop_grid(C, (const void*)kern, smem);
-  int64_t need = (n * G + kRowsThreads - 1) / kRowsThreads;
+  grid = std::min(grid, C.num_sms * C.trsv_blocks_per_sm);
+  int64_t need = (npos * G + kRowsThreads - 1) / kRowsThreads;
   if (need < grid) grid = (int)std::max<int64_t>(1, need);
-  int epoch = C.next_flag_epoch();
-  int* flags = C.flags.as<int>();
+  VL_CUDA(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)n * ld, C.stream));
   double* partials = C.red_partial.as<double>();
   unsigned* counter = next_counter(C);
-  void* args[] = {(void*)&n, (void*)&t, (void*)&order, (void*)&deps, (void*)&x, (void*)&flags, (void*)&epoch,
-                  (void*)&body, (void*)&fin, (void*)&partials, (void*)&counter, (void*)&gate};
+  unsigned smax = (unsigned)C.spin_max_ns;
+  long long* tstamp = C.debug_tstamp;
+  void* args[] = {(void*)&npos,  (void*)&t,    (void*)&ld,       (void*)&order,   (void*)&deps,
+                  (void*)&x,     (void*)&body, (void*)&fin,      (void*)&partials, (void*)&counter,
+                  (void*)&gate,  (void*)&smax, (void*)&tstamp};
   VL_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kRowsThreads), args, smem, C.stream));
 }
 

@@ -17,15 +17,6 @@ unsigned* next_counter(Ctx& C) {
   return base + slot;
 }
 
-void ensure_flags(Ctx& C, int64_t n) {
-  size_t need = sizeof(int) * (size_t)std::max<int64_t>(n, 1);
-  if (C.flags.bytes < need) {
-    C.flags.alloc(need);
-    VL_CUDA(cudaMemsetAsync(C.flags.p, 0, need, C.stream));
-    C.flag_epoch = 0;
-  }
-}
-
 int coop_grid(Ctx& C, const void* func, size_t smem) {
   static std::mutex mu;
   static std::map<std::pair<const void*, size_t>, int> cache;
@@ -54,29 +45,32 @@ BView bview(const Factor& F, bool grad) {
   return v;
 }
 
-void op_spmm(Ctx& C, const Factor& F, int op, int t, const double* x, double* y) {
+void op_spmm(Ctx& C, const Factor& F, int op, int t, int ld, const double* x, double* y) {
   const Pattern& P = *F.pat;
   if (op == 2 && !F.has_grad) fail(kEConfig, "factor was built without gradient");
-  dispatch_t(t, [&](auto g, auto nc) {
-    constexpr int G = decltype(g)::value, NC = decltype(nc)::value;
-    if (op == 0) launch_rows<G, NC, 0, 0>(C, P.n, t, BodyBx{bview(F, false), x, y}, Fin0<0>{});
-    else if (op == 1) launch_rows<G, NC, 0, 0>(C, P.n, t, BodyBtx{bview(F, false), x, y}, Fin0<0>{});
-    else if (op == 2) launch_rows<G, NC, 0, 0>(C, P.n, t, BodyDBx{bview(F, true), x, y}, Fin0<0>{});
+  BView B = bview(F, false);
+  dispatch_cols(t, ld, [&](auto g, auto nu, auto u) {
+    constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(u)::value;
+    if (op == 0) launch_rows<G, NU, U, 0, 0>(C, P.n, t, BodyBx{B, F.val.as<double>(), x, y, ld, 1}, Fin0<0>{});
+    else if (op == 1) launch_rows<G, NU, U, 0, 0>(C, P.n, t, BodyBtx{B, x, y, ld}, Fin0<0>{});
+    else if (op == 2) launch_rows<G, NU, U, 0, 0>(C, P.n, t, BodyBx{B, F.dval.as<double>(), x, y, ld, 0}, Fin0<0>{});
     else fail(kEConfig, "unknown product op");
   });
 }
 
-void op_trsv(Ctx& C, const Factor& F, bool transpose, int t, const double* b, double* x) {
+void op_trsv(Ctx& C, const Factor& F, bool transpose, int t, int ld, const double* b, double* x) {
   const Pattern& P = *F.pat;
   if (b == x) fail(kEConfig, "triangular solve cannot run in place");
-  dispatch_t(t, [&](auto g, auto nc) {
-    constexpr int G = decltype(g)::value, NC = decltype(nc)::value;
+  dispatch_cols(t, ld, [&](auto g, auto nu, auto u) {
+    constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(u)::value;
     if (!transpose) {
       DepsEll deps{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
-      launch_trsv<G, NC, 0>(C, P.n, t, P.fwd_order.as<int32_t>(), deps, x, TrsvPlain{b, t}, Fin0<0>{});
+      launch_trsv<G, NU, U, 0>(C, P.n, P.fwd_len, t, ld, P.fwd_order.as<int32_t>(), deps, x, TrsvPlain{b, ld},
+                               Fin0<0>{});
     } else {
       DepsCsr deps{P.tptr.as<int32_t>(), P.tidx.as<int32_t>(), F.valT.as<double>()};
-      launch_trsv<G, NC, 0>(C, P.n, t, P.bwd_order.as<int32_t>(), deps, x, TrsvPlain{b, t}, Fin0<0>{});
+      launch_trsv<G, NU, U, 0>(C, P.n, P.bwd_len, t, ld, P.bwd_order.as<int32_t>(), deps, x, TrsvPlain{b, ld},
+                               Fin0<0>{});
     }
   });
 }

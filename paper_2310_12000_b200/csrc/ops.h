@@ -12,12 +12,11 @@ void pattern_build_host(Pattern& P, const double* xy, const int32_t* nbr, std::v
                         std::vector<int32_t>& tptr, std::vector<int32_t>& tidx, std::vector<int32_t>& tmap);
 void pattern_upload(Ctx& C, Pattern& P, const double* xy_factor_order, const int32_t* nbr_factor_order);
 
-void ensure_flags(Ctx& C, int64_t n);
-
 void factor_build(Ctx& C, const Pattern& P, Factor& F, double sigma2, double rho, double nu, bool want_grad);
 
+void factor_refresh_transpose(Ctx& C, Factor& F);
 BView bview(const Factor& F, bool grad);
-void op_spmm(Ctx& C, const Factor& F, int op, int t, const double* x, double* y);
-void op_trsv(Ctx& C, const Factor& F, bool transpose, int t, const double* b, double* x);
+void op_spmm(Ctx& C, const Factor& F, int op, int t, int ld, const double* x, double* y);
+void op_trsv(Ctx& C, const Factor& F, bool transpose, int t, int ld, const double* b, double* x);
 
 }  // namespace vl

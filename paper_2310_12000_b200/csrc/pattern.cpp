@@ -323,11 +323,14 @@ void pattern_build_host(Pattern& P, const double* xy, const int32_t* nbr, std::v
   P.nnz_off = nnz;
   if (nnz >= (int64_t)INT32_MAX) fail(kECapacity, "pattern too large for int32 CSR offsets");
   // schedules: rows ordered by (level, storage position)
+  // each level padded with -1 to a multiple of 32 (rows of one warp-iteration
+  // of the solve kernels are then always independent)
   auto bucket = [&](const std::vector<int32_t>& lv, int nl, std::vector<int32_t>& order, std::vector<int32_t>& ptr) {
+    std::vector<int64_t> size(nl, 0);
+    for (int64_t s = 0; s < n; ++s) size[lv[P.sperm[s]]]++;
     ptr.assign(nl + 1, 0);
-    for (int64_t s = 0; s < n; ++s) ptr[lv[P.sperm[s]] + 1]++;
-    for (int l = 0; l < nl; ++l) ptr[l + 1] += ptr[l];
-    order.assign(n, 0);
+    for (int l = 0; l < nl; ++l) ptr[l + 1] = ptr[l] + (int32_t)((size[l] + 31) / 32 * 32);
+    order.assign(ptr[nl], -1);
     std::vector<int32_t> fill(ptr.begin(), ptr.end() - 1);
     for (int64_t s = 0; s < n; ++s) order[fill[lv[P.sperm[s]]]++] = (int32_t)s;
   };

@@ -1,16 +1,21 @@
-// Row-parallel kernel frameworks over the n x t row-major (storage order)
+// Row-parallel kernel frameworks over the n x ld row-major (storage order)
 // vectors of the Vecchia path.
 //
-//  * rows_kernel   : no dependencies (products with B, B^T, dB, elementwise
-//                    passes).  A group of G lanes owns one row; lane gl of a
-//                    group owns columns c = gl + G*k (k < NC).
-//  * trsv_kernel   : dependency-driven (sync-free) triangular solve.  Rows
-//                    are visited in level order; a row spins on the
-//                    epoch-tagged ready flags of the rows it reads, so there
-//                    is no per-level launch or grid barrier.  The kernel is
-//                    launched cooperatively (all CTAs co-resident) and rows
-//                    are assigned statically in level order, which makes the
-//                    spin deadlock-free.
+// Column mapping.  A row is owned by a group of G lanes.  Columns are moved
+// in units of U doubles (U = 2 -> 16-byte vector loads when ld is even);
+// lane gl of a group owns units u = gl + G*k (k < NU), i.e. columns
+// c = U*u + i (i < U).  Per-lane column arrays have NC = NU*U entries and
+// entry a[U*k + i] is column U*(gl + G*k) + i.
+//
+//  * rows_kernel : no dependencies (products with B, B^T, dB, elementwise
+//                  passes).
+//  * trsv_kernel : dependency-driven (sync-free) triangular solve.  Rows are
+//                  visited in level order; a row polls the VALUES of the rows
+//                  it reads (x is pre-filled with a NaN sentinel), warp-
+//                  converged, so there is no per-row flag, fence or
+//                  per-level barrier.  Launched cooperatively (all CTAs
+//                  co-resident) with a static level-order assignment, which
+//                  makes the spin deadlock-free.
 //
 // Both end with a DETERMINISTIC column reduction (NR quantities per column):
 // fixed-order warp -> block -> grid (last-block) sums, no float atomics.
@@ -24,38 +29,75 @@ namespace vl {
 
 constexpr int kRowsThreads = 256;
 
+// ---- column-unit helpers ---------------------------------------------------
+template <int G, int NU, int U>
+struct Cols {
+  static constexpr int NC = NU * U;
+  VL_D static int col(int gl, int i) { return U * (gl + G * (i / U)) + (i % U); }
+};
+
+template <int U>
+VL_D void load_unit(const double* p, double* out) {
+  if constexpr (U == 2) {
+    double2 v = __ldg(reinterpret_cast<const double2*>(p));
+    out[0] = v.x;
+    out[1] = v.y;
+  } else {
+    out[0] = __ldg(p);
+  }
+}
+
+// L2-coherent polling load of one unit (bypasses L1).
+template <int U>
+VL_D void ld_cg_unit(const double* p, double* out) {
+  if constexpr (U == 2) {
+    double a, b;
+    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
+    out[0] = a;
+    out[1] = b;
+  } else {
+    double a;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(a) : "l"(p));
+    out[0] = a;
+  }
+}
+
 template <int NR>
 struct Fin0 {
   VL_D void operator()(const double* /*sums*/, int /*t*/) const {}
 };
 
-// acc[r][k] for columns c = gl + G*k.  MAXMASK bit r set -> max-reduce (values >= 0).
-template <int G, int NC, int NR, int MAXMASK>
-VL_D void block_reduce_cols(double (&acc)[NR > 0 ? NR : 1][NC], int t, double* out, double* sh) {
-  if (NR == 0) return;
+// acc[r][i] for columns Cols::col(gl, i).  MAXMASK bit r set -> max-reduce.
+template <int G, int NU, int U, int NR, int MAXMASK>
+VL_D void block_reduce_cols(double (&acc)[NR > 0 ? NR : 1][NU * U], int t, double* out, double* sh) {
+  if constexpr (NR == 0) return;
+  constexpr int NC = NU * U;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
 #pragma unroll
   for (int r = 0; r < NR; ++r)
 #pragma unroll
-    for (int k = 0; k < NC; ++k)
+    for (int i = 0; i < NC; ++i)
 #pragma unroll
       for (int o = G; o < 32; o <<= 1) {
-        double other = __shfl_xor_sync(0xffffffffu, acc[r][k], o);
-        acc[r][k] = ((MAXMASK >> r) & 1) ? fmax(acc[r][k], other) : acc[r][k] + other;
+        double other = __shfl_xor_sync(0xffffffffu, acc[r][i], o);
+        acc[r][i] = ((MAXMASK >> r) & 1) ? fmax(acc[r][i], other) : acc[r][i] + other;
       }
+  // lane gl (< G) of warp w writes its NC entries
   if (lane < G) {
 #pragma unroll
     for (int r = 0; r < NR; ++r)
 #pragma unroll
-      for (int k = 0; k < NC; ++k) sh[((warp * NR + r) * NC + k) * G + lane] = acc[r][k];
+      for (int i = 0; i < NC; ++i) sh[((warp * NR + r) * NC + i) * G + lane] = acc[r][i];
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < NR * t; idx += blockDim.x) {
-    int r = idx / t, c = idx - r * t;
-    int k = c / G, gl = c - k * G;
+    const int r = idx / t, c = idx - r * t;
+    const int u = c / U, ii = c % U;
+    const int gl = u % G, k = u / G;
+    const int i = U * k + ii;
     double s = 0.0;
     for (int w = 0; w < nwarps; ++w) {
-      double v = sh[((w * NR + r) * NC + k) * G + gl];
+      double v = sh[((w * NR + r) * NC + i) * G + gl];
       s = ((MAXMASK >> r) & 1) ? fmax(s, v) : s + v;
     }
     out[idx] = s;
@@ -65,7 +107,7 @@ VL_D void block_reduce_cols(double (&acc)[NR > 0 ? NR : 1][NC], int t, double* o
 // Grid-level finalisation by the last CTA to finish (fixed block order).
 template <int NR, int MAXMASK, class Fin>
 VL_D void grid_finalize(const double* partials, unsigned* counter, int t, const Fin& fin, double* sh) {
-  if (NR == 0) return;
+  if constexpr (NR == 0) return;
   __threadfence();
   __syncthreads();
   __shared__ unsigned s_ticket;
@@ -75,7 +117,7 @@ VL_D void grid_finalize(const double* partials, unsigned* counter, int t, const 
   __threadfence();
   const int nb = gridDim.x;
   for (int idx = threadIdx.x; idx < NR * t; idx += blockDim.x) {
-    int r = idx / t;
+    const int r = idx / t;
     double s = 0.0;
     for (int b = 0; b < nb; ++b) {
       double v = __ldcg(partials + (size_t)b * NR * t + idx);
@@ -89,22 +131,21 @@ VL_D void grid_finalize(const double* partials, unsigned* counter, int t, const 
   if (threadIdx.x == 0) *counter = 0u;  // ready for the next launch using this slot
 }
 
-// shared memory needed by the reductions
-template <int G, int NC, int NR>
+template <int G, int NU, int U, int NR>
 constexpr size_t red_smem_bytes(int threads, int t) {
-  size_t a = (size_t)(threads / 32) * (NR > 0 ? NR : 1) * NC * G * sizeof(double);
+  size_t a = (size_t)(threads / 32) * (NR > 0 ? NR : 1) * NU * U * G * sizeof(double);
   size_t b = (size_t)(NR > 0 ? NR : 1) * t * sizeof(double);
   return a > b ? a : b;
 }
 
 // ---------------------------------------------------------------------------
 // Body concept for rows_kernel:
-//   template<int G,int NC,int NR> VL_D void operator()(int64_t s, bool valid, int gl, int t,
-//                                                      double (&acc)[NR][NC]) const;
-// Bodies must keep every lane of the warp participating when they use
-// group shuffles (valid == false rows just skip memory traffic).
+//   template <int G, int NU, int U, int NR>
+//   VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU*U]) const;
+// run() is called by every lane of the warp (valid == false for tail rows)
+// so bodies may use warp shuffles.
 // ---------------------------------------------------------------------------
-template <int G, int NC, int NR, int MAXMASK, class Body, class Fin>
+template <int G, int NU, int U, int NR, int MAXMASK, class Body, class Fin>
 __global__ void __launch_bounds__(kRowsThreads) rows_kernel(int64_t n, int t, Body body, Fin fin,
                                                             double* __restrict__ partials,
                                                             unsigned* __restrict__ counter,
@@ -112,112 +153,185 @@ __global__ void __launch_bounds__(kRowsThreads) rows_kernel(int64_t n, int t, Bo
   if (gate != nullptr && *((volatile const int*)gate) == 0) return;
   extern __shared__ double rsh[];
   constexpr int GPW = 32 / G;
+  constexpr int NRR = NR > 0 ? NR : 1;
   const int lane = threadIdx.x & 31;
   const int gl = lane % G;
   const int gi = lane / G;
-  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  double acc[NR > 0 ? NR : 1][NC];
+  // Block-contiguous row chunks: each CTA sweeps a compact run of storage rows
+  // (a spatial patch in Hilbert order), so neighbour rows gathered by
+  // adjacent rows are reused from L1 instead of re-fetched from L2.
+  const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  chunk = (chunk + GPW - 1) / GPW * GPW;
+  const int64_t r0 = (int64_t)blockIdx.x * chunk;
+  const int64_t r1 = r0 + chunk < n ? r0 + chunk : n;
+  double acc[NRR][NU * U];
 #pragma unroll
-  for (int r = 0; r < (NR > 0 ? NR : 1); ++r)
+  for (int r = 0; r < NRR; ++r)
 #pragma unroll
-    for (int k = 0; k < NC; ++k) acc[r][k] = 0.0;
-  for (int64_t s0 = gwarp * GPW; s0 < n; s0 += nwarps * GPW) {
+    for (int i = 0; i < NU * U; ++i) acc[r][i] = 0.0;
+  for (int64_t s0 = r0 + (int64_t)wib * GPW; s0 < r1; s0 += (int64_t)wpb * GPW) {
     const int64_t s = s0 + gi;
-    body.template run<G, NC, (NR > 0 ? NR : 1)>(s, s < n, gl, t, acc);
+    body.template run<G, NU, U, NRR>(s, s < r1, gl, t, acc);
   }
-  if (NR > 0) {
-    block_reduce_cols<G, NC, NR, MAXMASK>(acc, t, partials + (size_t)blockIdx.x * NR * t, rsh);
+  if constexpr (NR > 0) {
+    block_reduce_cols<G, NU, U, NR, MAXMASK>(acc, t, partials + (size_t)blockIdx.x * NR * t, rsh);
     grid_finalize<NR, MAXMASK>(partials, counter, t, fin, rsh);
   }
 }
 
 // ---------------------------------------------------------------------------
-// Dependency-driven triangular solve.
-//   Solve:  x_s = rhs(s,c) - sum_{e in deps(s)} w_e * x_{dep(e)}
-//   deps are read through the Deps functor (ELL rows of B for the forward
-//   solve, children CSR of B^T for the backward solve).
+// Dependency-driven triangular solve (value-as-flag).
+//   x_s = rhs(s,c) - sum_{e in deps(s)} w_e * x_{dep(e)}
+// `order` lists storage rows in level order, each level padded with -1 to a
+// multiple of 32, so the rows of one warp-iteration are always independent.
 // Body concept:
-//   VL_D double rhs(int64_t s, int c, double& racc) const;      // right-hand side
-//   VL_D void   out(int64_t s, int c, double x, double& racc) const;  // epilogue
+//   VL_D double rhs(int64_t s, int c, double& racc) const;
+//   VL_D void   out(int64_t s, int c, double x, double& racc) const;
 // ---------------------------------------------------------------------------
+constexpr unsigned long long kSentinel = 0xFFFFFFFFFFFFFFFFull;
+
+VL_D bool is_sentinel(double v) { return (unsigned long long)__double_as_longlong(v) == kSentinel; }
+VL_D double sanitize(double v) { return is_sentinel(v) ? __longlong_as_double(0x7ff8000000000000ll) : v; }
+
 struct DepsEll {
   const int32_t* nbr;
   const int32_t* cnt;
   const double* val;
   int m;
-  VL_D int begin(int64_t s) const { return 0; }
-  VL_D int end(int64_t s) const { return cnt[s]; }
-  VL_D int32_t col(int64_t s, int e) const { return nbr[s * m + e]; }
-  VL_D double w(int64_t s, int e) const { return val[s * m + e]; }
+  VL_D int count(int64_t s) const { return cnt[s]; }
+  VL_D int64_t base(int64_t s) const { return s * m; }
+  VL_D int32_t idx(int64_t b) const { return nbr[b]; }
+  VL_D double w(int64_t b) const { return val[b]; }
 };
 struct DepsCsr {
   const int32_t* ptr;
-  const int32_t* idx;
+  const int32_t* ind;
   const double* val;
-  VL_D int begin(int64_t s) const { return ptr[s]; }
-  VL_D int end(int64_t s) const { return ptr[s + 1]; }
-  VL_D int32_t col(int64_t s, int e) const { return idx[e]; }
-  VL_D double w(int64_t s, int e) const { return val[e]; }
+  VL_D int count(int64_t s) const { return ptr[s + 1] - ptr[s]; }
+  VL_D int64_t base(int64_t s) const { return ptr[s]; }
+  VL_D int32_t idx(int64_t b) const { return ind[b]; }
+  VL_D double w(int64_t b) const { return val[b]; }
 };
 
-template <int G, int NC, int NR, class Deps, class Body, class Fin>
-__global__ void __launch_bounds__(kRowsThreads) trsv_kernel(int64_t n, int t, const int32_t* __restrict__ order,
-                                                            Deps deps, double* __restrict__ x, int* __restrict__ flags,
-                                                            int epoch, Body body, Fin fin,
+template <int G, int NU, int U, int NR, class Deps, class Body, class Fin>
+__global__ void __launch_bounds__(kRowsThreads) trsv_kernel(int64_t npos, int t, int ld,
+                                                            const int32_t* __restrict__ order, Deps deps,
+                                                            double* __restrict__ x, Body body, Fin fin,
                                                             double* __restrict__ partials,
                                                             unsigned* __restrict__ counter,
-                                                            const int* __restrict__ gate) {
+                                                            const int* __restrict__ gate, unsigned smax,
+                                                            long long* __restrict__ tstamp) {
   if (gate != nullptr && *((volatile const int*)gate) == 0) return;
   extern __shared__ double rsh[];
   constexpr int GPW = 32 / G;
+  constexpr int NC = NU * U;
+  constexpr int NRR = NR > 0 ? NR : 1;
+  constexpr int BATCH = (NC <= 2) ? 8 : 4;
+  using CL = Cols<G, NU, U>;
   const int lane = threadIdx.x & 31;
   const int gl = lane % G;
   const int gi = lane / G;
-  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gi * G));
-  const int64_t gid = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * GPW + gi;
-  const int64_t ngroups = (((int64_t)gridDim.x * blockDim.x) >> 5) * GPW;
-  double acc[NR > 0 ? NR : 1][NC];
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double acc[NRR][NC];
 #pragma unroll
-  for (int r = 0; r < (NR > 0 ? NR : 1); ++r)
+  for (int r = 0; r < NRR; ++r)
 #pragma unroll
-    for (int k = 0; k < NC; ++k) acc[r][k] = 0.0;
+    for (int i = 0; i < NC; ++i) acc[r][i] = 0.0;
 
-  for (int64_t p = gid; p < n; p += ngroups) {
-    const int64_t s = order[p];
+  for (int64_t pbase = gwarp * GPW; pbase < npos; pbase += nwarps * GPW) {
+    const int64_t p = pbase + gi;
+    const int32_t so = (p < npos) ? order[p] : -1;
+    const bool valid = so >= 0;
+    const int64_t s = valid ? so : 0;
     double xs[NC];
 #pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      int c = gl + G * k;
-      xs[k] = (c < t) ? body.rhs(s, c, acc[0][k]) : 0.0;
+    for (int i = 0; i < NC; ++i) {
+      const int c = CL::col(gl, i);
+      xs[i] = (valid && c < t) ? body.rhs(s, c, acc[0][i]) : 0.0;
     }
-    const int e0 = deps.begin(s), e1 = deps.end(s);
-    for (int e = e0; e < e1; ++e) {
-      const int32_t j = deps.col(s, e);
-      const double w = deps.w(s, e);
-      while (ld_acquire(flags + j) != epoch) {
-      }
-      const double* xj = x + (int64_t)j * t;
+    const int cs = valid ? deps.count(s) : 0;
+    const int64_t b0 = valid ? deps.base(s) : 0;
+    // Warp-converged dependency loop: all lanes issue a batch of loads, then
+    // the whole warp re-polls the still-pending ones together.
+    const int cmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)cs);
+    for (int e0 = 0; e0 < cmax; e0 += BATCH) {
+      int32_t j[BATCH];
+      double w[BATCH];
+      double v[BATCH][NC];
 #pragma unroll
-      for (int k = 0; k < NC; ++k) {
-        int c = gl + G * k;
-        if (c < t) xs[k] -= w * ld_cg(xj + c);
+      for (int q = 0; q < BATCH; ++q) {
+        const bool on = e0 + q < cs;
+        j[q] = on ? deps.idx(b0 + e0 + q) : 0;
+        w[q] = on ? deps.w(b0 + e0 + q) : 0.0;
       }
-    }
 #pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      int c = gl + G * k;
-      if (c < t) {
-        x[s * t + c] = xs[k];
-        body.out(s, c, xs[k], acc[0][k]);
+      for (int q = 0; q < BATCH; ++q)
+#pragma unroll
+        for (int k = 0; k < NU; ++k) {
+          const int c = U * (gl + G * k);
+          if (e0 + q < cs && c < t) {
+            ld_cg_unit<U>(x + (int64_t)j[q] * ld + c, &v[q][U * k]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < U; ++i) v[q][U * k + i] = 0.0;
+          }
+        }
+      unsigned ns = 8;
+      for (;;) {
+        bool pend = false;
+#pragma unroll
+        for (int q = 0; q < BATCH; ++q)
+#pragma unroll
+          for (int i = 0; i < NC; ++i) pend |= is_sentinel(v[q][i]);
+        if (!__any_sync(0xffffffffu, pend)) break;
+        if (smax) {
+          __nanosleep(ns);
+          ns = ns < smax ? ns * 2 : smax;
+        }
+#pragma unroll
+        for (int q = 0; q < BATCH; ++q)
+#pragma unroll
+          for (int k = 0; k < NU; ++k) {
+            bool pk = false;
+#pragma unroll
+            for (int i = 0; i < U; ++i) pk |= is_sentinel(v[q][U * k + i]);
+            if (pk) ld_cg_unit<U>(x + (int64_t)j[q] * ld + U * (gl + G * k), &v[q][U * k]);
+          }
+      }
+#pragma unroll
+      for (int q = 0; q < BATCH; ++q)
+#pragma unroll
+        for (int i = 0; i < NC; ++i) xs[i] -= w[q] * v[q][i];
+    }
+    if (valid) {
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        const int c = CL::col(gl, i);
+        if (c < t) body.out(s, c, xs[i], acc[0][i]);
+      }
+#pragma unroll
+      for (int k = 0; k < NU; ++k) {
+        const int c = U * (gl + G * k);
+        if (c < t) {
+          double* dst = x + s * ld + c;
+          if constexpr (U == 2) {
+            *reinterpret_cast<double2*>(dst) = make_double2(sanitize(xs[2 * k]), sanitize(xs[2 * k + 1]));
+          } else {
+            *dst = sanitize(xs[k]);
+          }
+        }
+      }
+      if (tstamp != nullptr && gl == 0) {
+        long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        tstamp[s] = g;
       }
     }
-    __threadfence();
-    __syncwarp(gmask);
-    if (gl == 0) st_release(flags + s, epoch);
   }
-  if (NR > 0) {
-    block_reduce_cols<G, NC, NR, 0>(acc, t, partials + (size_t)blockIdx.x * NR * t, rsh);
+  if constexpr (NR > 0) {
+    block_reduce_cols<G, NU, U, NR, 0>(acc, t, partials + (size_t)blockIdx.x * NR * t, rsh);
     grid_finalize<NR, 0>(partials, counter, t, fin, rsh);
   }
 }

@@ -200,6 +200,26 @@ class VecchiaFactor:
         out[self.pattern.sperm] = a
         return out
 
+    def set_values(self, B=None, D=None):
+        """Replay externally computed factor values (factor-order CSR with the
+        reference layout, diagonal last) into the device factor."""
+        P = self.pattern
+        if D is not None:
+            Ds = np.ascontiguousarray(np.asarray(D, dtype=float)[P.sperm])
+            _lib.call("vl_factor_set", self.ctx.h, self.h, 0, _lib.ptr(Ds))
+            self._D = np.asarray(D, dtype=float).copy()
+        if B is not None and P.m:
+            B = B.tocsr()
+            n, m = self.n, P.m
+            ell = np.zeros((n, m))
+            cnt = np.diff(B.indptr) - 1
+            for i in range(n):
+                lo = B.indptr[i]
+                ell[i, :cnt[i]] = B.data[lo:lo + cnt[i]]
+            ell = np.ascontiguousarray(ell[P.sperm])
+            _lib.call("vl_factor_set", self.ctx.h, self.h, 3, _lib.ptr(ell))
+            self._B = None
+
     @property
     def D(self):
         if self._D is None:
@@ -248,11 +268,15 @@ class VecchiaFactor:
         v = np.asarray(v, dtype=float)
         vec = v.ndim == 1
         V = v[:, None] if vec else v
-        t = V.shape[1]
-        x = self.pattern.to_dev(np.ascontiguousarray(V))
-        y = dev.empty(self.ctx, self.n, t)
-        _lib.call(name, self.ctx.h, self.h, *args, t, _lib.ptr(x), _lib.ptr(y))
-        out = self.pattern.from_dev(y)
+        outs = []
+        for c0 in range(0, V.shape[1], 128):  # the kernels take <= 128 columns per call
+            blk = np.ascontiguousarray(V[:, c0:c0 + 128])
+            t = blk.shape[1]
+            x = self.pattern.to_dev(blk)
+            y = dev.empty(self.ctx, self.n, t)
+            _lib.call(name, self.ctx.h, self.h, *args, t, _lib.ptr(x), _lib.ptr(y))
+            outs.append(self.pattern.from_dev(y))
+        out = np.concatenate(outs, axis=1) if outs else np.zeros_like(V)
         return out[:, 0] if vec else out
 
     def B_matvec(self, v):

@@ -4,8 +4,13 @@ import argparse
 import json
 import time
 
+import os
+import sys
+
 import numpy as np
 import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import paper_2310_12000_b200 as vg
 from paper_2310_12000_b200 import _lib
