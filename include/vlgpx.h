@@ -97,6 +97,77 @@ int vl_spmm(vl_ctx* ctx, const vl_factor* f, int op, int64_t t, const double* x_
 /* y = B^-1 x (transpose=0) or B^-T x (transpose=1)  (vecchia.py:172-174) */
 int vl_sptrsv(vl_ctx* ctx, const vl_factor* f, int transpose, int64_t t, const double* x_dev, double* y_dev);
 
+/* ---- Laplace objective (iterative backend, VADU preconditioner) ---------- */
+
+/* likelihood family: 0 bernoulli-logit, 1 bernoulli-probit, 2 gamma
+ * (likelihoods.py:62-181); shape = gamma shape xi */
+typedef struct {
+  int family;
+  double shape;
+} vl_lik;
+
+/* subset of BackendConfig (laplace.py:51-84) driving find_mode */
+typedef struct {
+  double mode_cg_tol; /* min(cg_tol, 1e-4), laplace.py:80-84 */
+  int cg_max_iter;
+  int newton_max_iter;
+  double newton_grad_tol;
+  double newton_obj_tol;
+} vl_newton_cfg;
+
+/* Damped-Newton mode b* (replaces laplace.py:204-287 find_mode).  Device
+ * vectors of length n (storage order): y, F in; b, W, d1, d3 out.
+ * out[0..6] = logp, quad, objective, grad_norm, newton_iters, converged,
+ * n_cg_solves; cg_iters (host, optional) = CG iterations per Newton step.
+ * Returns VL_ECONVERGENCE when not converged (outputs still written). */
+int vl_find_mode(vl_ctx* ctx, const vl_factor* f, const vl_lik* lik, const vl_newton_cfg* cfg, const double* y_dev,
+                 const double* F_dev, double* b_dev, double* W_dev, double* d1_dev, double* d3_dev, double* out_host,
+                 int32_t* cg_iters_host, int cg_iters_cap);
+
+/* Probes for VADU (replaces preconditioners.py:121-122 sample_block with the
+ * reference's Gaussian base draws G, and iterative.py:268-271 psolves):
+ * Z = B^T (sqrt(d) o G), V = P^-1 Z = B^-1 (G / sqrt(d)), w_host[c] = z_c . v_c.
+ * G, Z, V: n x t device (storage order). */
+int vl_probes_vadu(vl_ctx* ctx, const vl_factor* f, const double* W_dev, int64_t t, const double* G_dev, double* Z_dev,
+                   double* V_dev, double* w_host);
+
+/* PCG on (W + B^T D^-1 B) U = Bm with the VADU preconditioner, t columns
+ * (replaces iterative.py:104-178 pcg_solve per column, laplace.py:290-309).
+ * Host outputs per column: iterations, converged flag, residual norm; with
+ * capture, alpha/beta histories [hist_cap x t] (row l = CG iteration l). */
+int vl_pcg_vadu(vl_ctx* ctx, const vl_factor* f, const double* W_dev, int64_t t, const double* B_dev, double* U_dev,
+                double tol, int max_iter, int capture, int32_t* iters_host, int32_t* conv_host, double* res_host,
+                double* alpha_host, double* beta_host, int hist_cap);
+
+/* out6 = [sum log D, sum log(W + 1/D), sum dD_s2/D, sum dD_rho/D,
+ *         -sum dD_s2/(D(DW+1)), -sum dD_rho/(D(DW+1))]
+ * (laplace.py:331-336, 502, 511-513) */
+int vl_factor_sums(vl_ctx* ctx, const vl_factor* f, const double* W_dev, double* out6_host);
+
+/* Fused gradient pass over the probe solves U and psolves V (n x t):
+ * s_out = 0.5 dlogdet/dmu (laplace.py:389-436, VADU control variates) and the
+ * per-probe STE terms cols4 = [h_s2 | r_s2 | h_rho | r_rho] (4 x t, host)
+ * (laplace.py:493-541, iterative.py:280-304).  With md3x (gamma), xicols2 =
+ * [h_xi | r_xi] (laplace.py:543-576). */
+int vl_grad_probe_pass(vl_ctx* ctx, const vl_factor* f, const double* W_dev, const double* d3_dev, const double* U_dev,
+                       const double* V_dev, int64_t t, double* s_dev, double* cols4_host, const double* md3x_dev,
+                       double* xicols2_host);
+
+/* out4 = [b^T dQ_s2 b, tvec^T dQ_s2 b, b^T dQ_rho b, tvec^T dQ_rho b]
+ * (vecchia.py:357-361 quad_dprecision; laplace.py:537-541) */
+int vl_grad_scalar_terms(vl_ctx* ctx, const vl_factor* f, const double* b_dev, const double* tvec_dev,
+                         double* out4_host);
+
+/* dbeta = X^T (-d1 + s - W o tvec)  (laplace.py:578-580); X: n x p device */
+int vl_grad_dbeta(vl_ctx* ctx, int64_t n, const double* d1_dev, const double* s_dev, const double* W_dev,
+                  const double* tvec_dev, const double* X_dev, int64_t p, double* dbeta_host);
+
+/* gamma shape terms (likelihoods.py:164-170 at mu = F + b):
+ * md3x = y e^{-mu} (device), out3 = [sum(log y - mu - y e^{-mu}),
+ * sum(tvec (-1 + y e^{-mu})), sum(md3x / (W + 1/D))] */
+int vl_gamma_xi_terms(vl_ctx* ctx, const vl_factor* f, const double* y_dev, const double* F_dev, const double* b_dev,
+                      const double* W_dev, const double* tvec_dev, double* md3x_dev, double* out3_host);
+
 #ifdef __cplusplus
 }
 #endif

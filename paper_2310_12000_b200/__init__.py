@@ -28,3 +28,6 @@ from .vecchia import (
 )
 
 __version__ = "0.1.0"
+from .laplace import BackendConfig, LaplaceState, find_mode, gradient, make_probes, neg_marginal_loglik
+from .likelihoods import get_likelihood
+from .iterative import ProbeSet, Tridiag

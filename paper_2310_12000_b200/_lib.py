@@ -43,6 +43,26 @@ _SIGS = {
     "vl_spmm": [c_void_p, c_void_p, c_int, c_int64, c_void_p, c_void_p],
     "vl_sptrsv": [c_void_p, c_void_p, c_int, c_int64, c_void_p, c_void_p],
 }
+class VlLik(C.Structure):
+    _fields_ = [("family", C.c_int), ("shape", C.c_double)]
+
+
+class VlNewtonCfg(C.Structure):
+    _fields_ = [("mode_cg_tol", C.c_double), ("cg_max_iter", C.c_int), ("newton_max_iter", C.c_int),
+                ("newton_grad_tol", C.c_double), ("newton_obj_tol", C.c_double)]
+
+
+_V = c_void_p
+_SIGS.update({
+    "vl_find_mode": [_V, _V, C.POINTER(VlLik), C.POINTER(VlNewtonCfg), _V, _V, _V, _V, _V, _V, _V, _V, c_int],
+    "vl_probes_vadu": [_V, _V, _V, c_int64, _V, _V, _V, _V],
+    "vl_pcg_vadu": [_V, _V, _V, c_int64, _V, _V, c_double, c_int, c_int, _V, _V, _V, _V, _V, c_int],
+    "vl_factor_sums": [_V, _V, _V, _V],
+    "vl_grad_probe_pass": [_V, _V, _V, _V, _V, _V, c_int64, _V, _V, _V, _V],
+    "vl_grad_scalar_terms": [_V, _V, _V, _V, _V],
+    "vl_grad_dbeta": [_V, c_int64, _V, _V, _V, _V, _V, c_int64, _V],
+    "vl_gamma_xi_terms": [_V, _V, _V, _V, _V, _V, _V, _V, _V],
+})
 _RET = {"vl_last_error": C.c_char_p}
 
 # functions declared in include/vlgpx.h (tests check the export table)

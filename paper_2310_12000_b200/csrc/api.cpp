@@ -10,7 +10,9 @@
 #include <vector>
 
 #include "../../include/vlgpx.h"
+#include "laplace.h"
 #include "ops.h"
+#include "pcg.h"
 
 struct vl_ctx {
   vl::Ctx c;
@@ -179,7 +181,7 @@ int vl_ctx_create(int device, void* stream, vl_ctx** out) {
       C.red_partial.alloc(16u << 20);
       C.red_counter.alloc(64 * sizeof(unsigned));
       VL_CUDA(cudaMemsetAsync(C.red_counter.p, 0, 64 * sizeof(unsigned), C.stream));
-      C.dev_scalars.alloc(4096);
+      C.dev_scalars.alloc(1 << 16);
       VL_CUDA(cudaMallocHost(&C.host_scalars, 4096));
       VL_CUDA(cudaStreamSynchronize(C.stream));
     } catch (...) {
@@ -334,6 +336,100 @@ int vl_factor_set(vl_ctx* h, vl_factor* f, int which, const double* in) {
 // subsequent triangular solves into a device buffer of n int64 (NULL disables)
 int vl_debug_set_tstamp(vl_ctx* h, void* dev_buf) {
   return guard([&] { h->c.debug_tstamp = (long long*)dev_buf; });
+}
+
+// ---- Laplace path -----------------------------------------------------------
+
+int vl_find_mode(vl_ctx* h, const vl_factor* f, const vl_lik* lik, const vl_newton_cfg* cfg, const double* y,
+                 const double* Fv, double* b, double* W, double* d1, double* d3, double* out, int32_t* cg_iters,
+                 int cg_iters_cap) {
+  return guard([&] {
+    if (!h || !f || !lik || !cfg || !out) fail(kEConfig, "null argument");
+    LikSpec L{lik->family, lik->shape};
+    NewtonCfg nc{cfg->mode_cg_tol, cfg->cg_max_iter, cfg->newton_max_iter, cfg->newton_grad_tol, cfg->newton_obj_tol};
+    NewtonOut no;
+    auto fill = [&] {
+      out[0] = no.logp;
+      out[1] = no.quad;
+      out[2] = no.objective;
+      out[3] = no.grad_norm;
+      out[4] = no.iters;
+      out[5] = no.converged;
+      out[6] = (double)no.cg_iters.size();
+      if (cg_iters)
+        for (int i = 0; i < (int)no.cg_iters.size() && i < cg_iters_cap; ++i) cg_iters[i] = no.cg_iters[i];
+    };
+    try {
+      newton_mode(h->c, f->f, L, nc, y, Fv, b, W, d1, d3, &no);
+    } catch (...) {
+      fill();
+      throw;
+    }
+    fill();
+  });
+}
+
+int vl_probes_vadu(vl_ctx* h, const vl_factor* f, const double* W, int64_t t, const double* G, double* Z, double* V,
+                   double* w_host) {
+  return guard([&] {
+    if (t < 1 || t > 128) fail(kECapacity, "probe count per call must be in [1, 128]");
+    probes_vadu(h->c, f->f, W, (int)t, (int)t, G, Z, V, w_host);
+  });
+}
+
+int vl_pcg_vadu(vl_ctx* h, const vl_factor* f, const double* W, int64_t t, const double* bm, double* u, double tol,
+                int max_iter, int capture, int32_t* iters, int32_t* conv, double* res, double* alpha, double* beta,
+                int hist_cap) {
+  return guard([&] {
+    if (t < 1 || t > 128) fail(kECapacity, "right-hand sides per call must be in [1, 128]");
+    const Factor& F = f->f;
+    const int64_t n = F.pat->n;
+    DevBuf Dinv, dinv;
+    Dinv.alloc(sizeof(double) * n);
+    dinv.alloc(sizeof(double) * n);
+    vadu_diags(h->c, F, W, Dinv.as<double>(), dinv.as<double>());
+    SysVadu S{&F, W, Dinv.as<double>(), dinv.as<double>()};
+    PcgResult pr;
+    pcg_vadu(h->c, S, (int)t, (int)t, bm, u, tol, max_iter, capture != 0, &pr);
+    for (int c = 0; c < t; ++c) {
+      if (iters) iters[c] = pr.iters[c];
+      if (conv) conv[c] = pr.converged[c];
+      if (res) res[c] = pr.res[c];
+    }
+    if (capture && alpha && beta) {
+      for (int l = 0; l < std::min(pr.max_iters, hist_cap); ++l)
+        for (int c = 0; c < t; ++c) {
+          alpha[(size_t)l * t + c] = pr.alpha[(size_t)l * t + c];
+          beta[(size_t)l * t + c] = pr.beta[(size_t)l * t + c];
+        }
+    }
+  });
+}
+
+int vl_factor_sums(vl_ctx* h, const vl_factor* f, const double* W, double* out6) {
+  return guard([&] { factor_sums(h->c, f->f, W, out6); });
+}
+
+int vl_grad_probe_pass(vl_ctx* h, const vl_factor* f, const double* W, const double* d3, const double* U,
+                       const double* V, int64_t t, double* s_out, double* cols4, const double* md3x, double* xicols2) {
+  return guard([&] {
+    if (t < 1 || t > 128) fail(kECapacity, "probe count per call must be in [1, 128]");
+    grad_probe_pass(h->c, f->f, W, d3, U, V, (int)t, (int)t, s_out, cols4, md3x, xicols2);
+  });
+}
+
+int vl_grad_scalar_terms(vl_ctx* h, const vl_factor* f, const double* b, const double* tvec, double* out4) {
+  return guard([&] { grad_scalar_terms(h->c, f->f, b, tvec, out4); });
+}
+
+int vl_grad_dbeta(vl_ctx* h, int64_t n, const double* d1, const double* s, const double* W, const double* tvec,
+                  const double* X, int64_t p, double* dbeta) {
+  return guard([&] { grad_dF(h->c, n, d1, s, W, tvec, X, (int)p, dbeta); });
+}
+
+int vl_gamma_xi_terms(vl_ctx* h, const vl_factor* f, const double* y, const double* Fv, const double* b,
+                      const double* W, const double* tvec, double* md3x, double* out3) {
+  return guard([&] { gamma_xi_terms(h->c, f->f, y, Fv, b, W, tvec, md3x, out3); });
 }
 
 int vl_spmm(vl_ctx* h, const vl_factor* f, int op, int64_t t, const double* x, double* y) {

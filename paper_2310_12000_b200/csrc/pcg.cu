@@ -1,0 +1,360 @@
+// Multi-RHS preconditioned CG for the VADU-preconditioned Laplace system
+// (laplace.py:156-182 eq6 operator, preconditioners.py:101-132 VADU solve,
+// iterative.py:104-178 pcg_solve).  Each column runs the reference's scalar
+// recurrence independently; converged columns are frozen by a device-side
+// mask so results equal a per-column stop at the reference's iteration.
+//
+// One iteration = 4 kernels:
+//   K1  h = z + beta h_prev (fused into the gather),  tmp = D^-1 (B h)
+//   K2  v = W h + B^T tmp,  h.v -> alpha            (last-CTA finalize)
+//   K3  r -= alpha v, u += alpha h (fused rhs),  w = B^-T r,  ||r|| -> converged?
+//   K4  z = B^-1 (w / d),  r.z -> beta
+#include <cmath>
+#include <cstring>
+
+#include "bodies.cuh"
+#include "launch.cuh"
+#include "ops.h"
+#include "pcg.h"
+
+namespace vl {
+
+namespace {
+
+struct CgCols {
+  double* nb;
+  double* rz;
+  double* alpha;
+  double* beta;
+  double* res;
+  double* tolnb;
+  int* active;
+  int* iters;
+  int* conv;
+  int* status;   // [0] n_active, [1] error code, [2] error column
+  double* errval;
+  double* ah;    // [cap x t]
+  double* bh;
+};
+
+VL_D void recount(const CgCols& K, int t) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int na = 0;
+    for (int c = 0; c < t; ++c) na += K.active[c];
+    if (K.status[1] != 0) na = 0;
+    K.status[0] = na;
+  }
+}
+
+VL_D void set_error(const CgCols& K, int code, int c, double v) {
+  if (atomicCAS(K.status + 1, 0, code) == 0) {
+    K.status[2] = c;
+    *K.errval = v;
+  }
+}
+
+// ---- init: r = b, u = 0, hprev = 0, ||b||^2 --------------------------------
+struct InitBody {
+  const double* b;
+  double* r;
+  double* u;
+  double* hprev;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    if (!valid) return;
+    double a[NU * U], z[NU * U];
+    load_row<G, NU, U>(b, ld, s, gl, t, a);
+    zero(z);
+    store_row<G, NU, U>(r, ld, s, gl, t, a);
+    store_row<G, NU, U>(u, ld, s, gl, t, z);
+    store_row<G, NU, U>(hprev, ld, s, gl, t, z);
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) acc[0][i] += a[i] * a[i];
+  }
+};
+struct InitFin {
+  CgCols K;
+  double tol;
+  VL_D void operator()(const double* sums, int t) const {
+    for (int c = threadIdx.x; c < t; c += blockDim.x) {
+      const double nb = sqrt(sums[c]);
+      K.nb[c] = nb;
+      K.tolnb[c] = tol * nb;
+      const bool act = nb != 0.0;
+      K.active[c] = act ? 1 : 0;
+      K.conv[c] = act ? 0 : 1;
+      K.iters[c] = 0;
+      K.beta[c] = 0.0;
+      K.rz[c] = 0.0;
+      K.res[c] = nb;
+    }
+    if (threadIdx.x == 0) K.status[1] = 0;
+    recount(K, t);
+  }
+};
+
+// ---- preconditioner solve pieces ------------------------------------------
+struct RhsPlainActive {  // w = B^-T r  (init)
+  const double* r;
+  int ld;
+  VL_D double rhs(int64_t s, int c, double&) const { return r[s * ld + c]; }
+  VL_D void out(int64_t, int, double, double&) const {}
+};
+struct RhsScaleDot {  // z = B^-1 (w * dinv) ; acc += r . z
+  const double* w;
+  const double* dinv;
+  const double* r;
+  int ld;
+  VL_D double rhs(int64_t s, int c, double&) const { return w[s * ld + c] * dinv[s]; }
+  VL_D void out(int64_t s, int c, double x, double& acc) const { acc += r[s * ld + c] * x; }
+};
+struct RzInitFin {
+  CgCols K;
+  VL_D void operator()(const double* sums, int t) const {
+    for (int c = threadIdx.x; c < t; c += blockDim.x) K.rz[c] = sums[c];
+  }
+};
+
+// ---- K1: h = z + beta hprev; tmp = Dinv (B h) ------------------------------
+struct K1Body {
+  BView B;
+  const double* z;
+  const double* hprev;
+  double* h;
+  double* tmp;
+  const double* Dinv;
+  const double* beta;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&)[NR][NU * U]) const {
+    double bt[NU * U];
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) {
+      const int c = vl::Cols<G, NU, U>::col(gl, i);
+      bt[i] = c < t ? beta[c] : 0.0;
+    }
+    auto load = [&](int64_t j, int c, double* out) {
+      double zz[U], hh[U];
+      load_unit<U>(z + j * ld + c, zz);
+      load_unit<U>(hprev + j * ld + c, hh);
+      const int i0 = U * ((c / U - gl) / G);
+#pragma unroll
+      for (int i = 0; i < U; ++i) out[i] = zz[i] + bt[i0 + i] * hh[i];
+    };
+    double a[NU * U];
+    zero(a);
+    gather_B<G, NU, U>(B, B.val, s, valid, gl, t, load, a);
+    if (!valid) return;
+    double hs[NU * U];
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+      const int c = U * (gl + G * k);
+      if (c < t) load(s, c, &hs[U * k]);
+      else
+#pragma unroll
+        for (int i = 0; i < U; ++i) hs[U * k + i] = 0.0;
+    }
+    store_row<G, NU, U>(h, ld, s, gl, t, hs);
+    const double di = Dinv[s];
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) a[i] = di * (hs[i] + a[i]);
+    store_row<G, NU, U>(tmp, ld, s, gl, t, a);
+  }
+};
+
+// ---- K2: v = W h + B^T tmp; h.v -> alpha -----------------------------------
+struct K2Body {
+  BView B;
+  const double* h;
+  const double* tmp;
+  double* v;
+  const double* W;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    double a[NU * U];
+    zero(a);
+    gather_Bt<G, NU, U>(B, s, valid, gl, t, LoadU<U>{tmp, ld}, a);
+    if (!valid) return;
+    double ts[NU * U], hs[NU * U];
+    load_row<G, NU, U>(tmp, ld, s, gl, t, ts);
+    load_row<G, NU, U>(h, ld, s, gl, t, hs);
+    const double ws = W[s];
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) {
+      a[i] = ws * hs[i] + (ts[i] + a[i]);
+      acc[0][i] += hs[i] * a[i];
+    }
+    store_row<G, NU, U>(v, ld, s, gl, t, a);
+  }
+};
+struct K2Fin {
+  CgCols K;
+  int l;
+  int cap;
+  VL_D void operator()(const double* sums, int t) const {
+    for (int c = threadIdx.x; c < t; c += blockDim.x) {
+      if (!K.active[c]) continue;
+      const double hv = sums[c];
+      if (hv <= 0.0) set_error(K, kEBreakdown, c, hv);
+      const double al = K.rz[c] / hv;
+      K.alpha[c] = al;
+      if (l < cap) K.ah[(size_t)l * t + c] = al;
+    }
+    recount(K, t);
+  }
+};
+
+// ---- K3: r -= alpha v, u += alpha h (rhs of w = B^-T r); ||r|| -------------
+struct K3Rhs {
+  double* r;
+  double* u;
+  const double* v;
+  const double* h;
+  const double* alpha;
+  const int* active;
+  int ld;
+  VL_D double rhs(int64_t s, int c, double& acc) const {
+    const int64_t o = s * ld + c;
+    if (!active[c]) return r[o];
+    const double al = alpha[c];
+    const double rn = r[o] - al * v[o];
+    r[o] = rn;
+    u[o] = u[o] + al * h[o];
+    acc += rn * rn;
+    return rn;
+  }
+  VL_D void out(int64_t, int, double, double&) const {}
+};
+struct K3Fin {
+  CgCols K;
+  int l;
+  VL_D void operator()(const double* sums, int t) const {
+    for (int c = threadIdx.x; c < t; c += blockDim.x) {
+      if (!K.active[c]) continue;
+      const double res = sqrt(sums[c]);
+      K.res[c] = res;
+      K.iters[c] = l + 1;
+      if (res < K.tolnb[c]) {
+        K.active[c] = 0;
+        K.conv[c] = 1;
+      }
+    }
+    recount(K, t);
+  }
+};
+
+// ---- K4: z = B^-1 (w / d); r.z -> beta -------------------------------------
+struct K4Fin {
+  CgCols K;
+  int l;
+  int cap;
+  VL_D void operator()(const double* sums, int t) const {
+    for (int c = threadIdx.x; c < t; c += blockDim.x) {
+      if (!K.active[c]) continue;
+      const double rzn = sums[c];
+      if (rzn <= 0.0) set_error(K, kEBreakdown, c, rzn);
+      const double be = rzn / K.rz[c];
+      K.beta[c] = be;
+      K.rz[c] = rzn;
+      if (l < cap) K.bh[(size_t)l * t + c] = be;
+    }
+    recount(K, t);
+  }
+};
+
+}  // namespace
+
+void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* u, double tol, int max_iter,
+              bool capture, PcgResult* out) {
+  const Factor& F = *S.F;
+  const Pattern& P = *F.pat;
+  const int64_t n = P.n;
+  if (!(tol > 0)) fail(kEConfig, "tol must be > 0");
+  if (max_iter < 0) fail(kEConfig, "max_iter must be >= 0");
+  const size_t vb = sizeof(double) * (size_t)n * ld;
+  DevBuf r, z, w, v, tmp, h0, h1;
+  r.alloc(vb); z.alloc(vb); w.alloc(vb); v.alloc(vb); tmp.alloc(vb); h0.alloc(vb); h1.alloc(vb);
+  const int cap = capture ? std::max(max_iter, 1) : 1;
+  DevBuf colsd, colsi, hist;
+  colsd.alloc(sizeof(double) * (7 * (size_t)t + 1));
+  colsi.alloc(sizeof(int) * (3 * (size_t)t + 4));
+  hist.alloc(sizeof(double) * 2 * (size_t)cap * t);
+  CgCols K;
+  double* cd = colsd.as<double>();
+  K.nb = cd; K.rz = cd + t; K.alpha = cd + 2 * t; K.beta = cd + 3 * t; K.res = cd + 4 * t; K.tolnb = cd + 5 * t;
+  K.errval = cd + 7 * t;
+  int* ci = colsi.as<int>();
+  K.active = ci; K.iters = ci + t; K.conv = ci + 2 * t; K.status = ci + 3 * t;
+  K.ah = hist.as<double>();
+  K.bh = K.ah + (size_t)cap * t;
+  const int* gate = K.status;
+  BView B = bview(F, false);
+  DepsEll dfw{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
+  DepsCsr dbw{P.tptr.as<int32_t>(), P.tidx.as<int32_t>(), F.valT.as<double>()};
+  double* hb[2] = {h0.as<double>(), h1.as<double>()};
+
+  dispatch_cols(t, ld, [&](auto g, auto nu, auto uu) {
+    constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
+    // init
+    launch_rows<G, NU, U, 1, 0>(C, n, t, InitBody{b, r.as<double>(), u, hb[0], ld}, InitFin{K, tol});
+    launch_trsv<G, NU, U, 0>(C, n, P.bwd_len, t, ld, P.bwd_order.as<int32_t>(), dbw, w.as<double>(),
+                             RhsPlainActive{r.as<double>(), ld}, Fin0<0>{}, gate);
+    launch_trsv<G, NU, U, 1>(C, n, P.fwd_len, t, ld, P.fwd_order.as<int32_t>(), dfw, z.as<double>(),
+                             RhsScaleDot{w.as<double>(), S.dinv, r.as<double>(), ld}, RzInitFin{K}, gate);
+    int status[3] = {0, 0, 0};
+    int l = 0;
+    int chunk = 4;
+    while (l < max_iter) {
+      const int lim = std::min(max_iter, l + chunk);
+      for (; l < lim; ++l) {
+        double* hp = hb[l & 1];
+        double* hn = hb[(l + 1) & 1];
+        launch_rows<G, NU, U, 0, 0>(C, n, t, K1Body{B, z.as<double>(), hp, hn, tmp.as<double>(), S.Dinv, K.beta, ld},
+                                    Fin0<0>{}, gate);
+        launch_rows<G, NU, U, 1, 0>(C, n, t, K2Body{B, hn, tmp.as<double>(), v.as<double>(), S.W, ld},
+                                    K2Fin{K, l, cap}, gate);
+        launch_trsv<G, NU, U, 1>(C, n, P.bwd_len, t, ld, P.bwd_order.as<int32_t>(), dbw, w.as<double>(),
+                                 K3Rhs{r.as<double>(), u, v.as<double>(), hn, K.alpha, K.active, ld}, K3Fin{K, l},
+                                 gate);
+        launch_trsv<G, NU, U, 1>(C, n, P.fwd_len, t, ld, P.fwd_order.as<int32_t>(), dfw, z.as<double>(),
+                                 RhsScaleDot{w.as<double>(), S.dinv, r.as<double>(), ld}, K4Fin{K, l, cap}, gate);
+      }
+      VL_CUDA(cudaMemcpyAsync(status, K.status, sizeof(status), cudaMemcpyDeviceToHost, C.stream));
+      VL_CUDA(cudaStreamSynchronize(C.stream));
+      if (status[1] != 0 || status[0] == 0) break;
+      chunk = std::min(chunk * 2, 16);
+    }
+    if (status[1] != 0) {
+      double ev = 0;
+      VL_CUDA(cudaMemcpy(&ev, K.errval, sizeof(double), cudaMemcpyDeviceToHost));
+      char buf[256];
+      snprintf(buf, sizeof(buf), "CG breakdown in column %d: curvature %.3e <= 0 (operator or preconditioner not PD)",
+               status[2], ev);
+      fail(kEBreakdown, buf);
+    }
+  });
+  if (out) {
+    out->iters.assign(t, 0);
+    out->converged.assign(t, 0);
+    out->res.assign(t, 0.0);
+    VL_CUDA(cudaMemcpyAsync(out->iters.data(), K.iters, sizeof(int) * t, cudaMemcpyDeviceToHost, C.stream));
+    VL_CUDA(cudaMemcpyAsync(out->converged.data(), K.conv, sizeof(int) * t, cudaMemcpyDeviceToHost, C.stream));
+    VL_CUDA(cudaMemcpyAsync(out->res.data(), K.res, sizeof(double) * t, cudaMemcpyDeviceToHost, C.stream));
+    VL_CUDA(cudaStreamSynchronize(C.stream));
+    int mx = 0;
+    for (int c = 0; c < t; ++c) mx = std::max(mx, out->iters[c]);
+    out->max_iters = mx;
+    if (capture && mx > 0) {
+      out->alpha.assign((size_t)mx * t, 0.0);
+      out->beta.assign((size_t)mx * t, 0.0);
+      VL_CUDA(cudaMemcpyAsync(out->alpha.data(), K.ah, sizeof(double) * mx * t, cudaMemcpyDeviceToHost, C.stream));
+      VL_CUDA(cudaMemcpyAsync(out->beta.data(), K.bh, sizeof(double) * mx * t, cudaMemcpyDeviceToHost, C.stream));
+      VL_CUDA(cudaStreamSynchronize(C.stream));
+    }
+  }
+}
+
+}  // namespace vl

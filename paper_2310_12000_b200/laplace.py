@@ -1,0 +1,371 @@
+"""Mode finding, marginal likelihood and its gradient -- device backend.
+
+Drop-in for the iterative backend of vlgp/laplace.py: same names, arguments,
+return types and errors (BackendConfig 51-84, LaplaceState 87-102, find_mode
+204-287, make_probes 312-315, neg_marginal_loglik 340-348, gradient
+439-580).  Everything n-sized stays in HBM (storage order); the host sees
+only scalars, t per-probe tridiagonals and the gradient.
+
+Objective:  L = -log p(y | mu*) + 0.5 b*^T SigmaTilde^-1 b* + 0.5 log det(SigmaTilde W + I)
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, replace
+
+import numpy as np
+from scipy.special import digamma
+
+from . import _lib
+from . import device as dev
+from .errors import CapabilityError, ConfigError, ConvergenceError
+from .iterative import (CG_MAX_ITER_DEFAULT, CG_TOL_DEFAULT, ProbeSet, slq_from_parts, ste_combine,
+                        tridiag_from_cg)
+
+MODE_CG_TOL_CAP = 1e-4
+EQ5_VARIANTS = ("lrac", "l2")
+SUPPORTED_PRECONDITIONERS = ("vadu", "l1")
+
+
+@dataclass(frozen=True)
+class BackendConfig:
+    """How linear algebra is performed during likelihood evaluations."""
+
+    backend: str = "iterative"
+    preconditioner: str = "vadu"
+    t: int = 50
+    cg_tol: float = CG_TOL_DEFAULT
+    cg_max_iter: int = CG_MAX_ITER_DEFAULT
+    probe_seed: int = 0
+    logdet_split: str = "auto"
+    rank: int | None = None
+    newton_max_iter: int = 100
+    newton_grad_tol: float = 1e-6
+    newton_obj_tol: float = 1e-8
+
+    def __post_init__(self):
+        if self.backend not in ("cholesky", "iterative"):
+            raise ConfigError(f"unknown backend {self.backend!r}")
+        if self.t < 1:
+            raise ConfigError("t must be >= 1")
+        if self.logdet_split not in ("auto", "eq6", "eq7"):
+            raise ConfigError(f"unknown logdet split {self.logdet_split!r}")
+
+    def resolved_split(self):
+        if self.logdet_split != "auto":
+            return self.logdet_split
+        return "eq7" if self.preconditioner in EQ5_VARIANTS else "eq6"
+
+    @property
+    def mode_cg_tol(self):
+        return min(self.cg_tol, MODE_CG_TOL_CAP)
+
+
+def _check_supported(cfg):
+    if cfg.backend != "iterative":
+        raise CapabilityError("the device backend implements the iterative path; the dense 'cholesky' "
+                              "backend is the reference's CPU oracle")
+    if cfg.preconditioner not in SUPPORTED_PRECONDITIONERS:
+        raise CapabilityError(f"preconditioner {cfg.preconditioner!r} is not available on the device backend "
+                              f"(supported: {', '.join(SUPPORTED_PRECONDITIONERS)})")
+    if cfg.resolved_split() != "eq6":
+        raise CapabilityError("the VADU device path uses the eq6 log-determinant split")
+
+
+class LaplaceState:
+    """Converged mode and everything the likelihood/gradient needs at it.
+
+    Vectors live on the device (storage order); attribute access returns
+    numpy arrays in factor order like the reference's dataclass.
+    """
+
+    def __init__(self, pattern, dev_vecs, y, F, logp, quad, objective, newton_iters, converged, cg_iters=()):
+        self._pattern = pattern
+        self._dev = dev_vecs          # b, W, d1, d3, y, F (device, storage order)
+        self._y = y
+        self._F = F
+        self.logp = float(logp)
+        self.quad = float(quad)
+        self.objective = float(objective)
+        self.newton_iters = int(newton_iters)
+        self.converged = bool(converged)
+        self.cg_iters = list(cg_iters)
+        self._cache = {}
+
+    def _host(self, key):
+        v = self._cache.get(key)
+        if v is None:
+            v = self._pattern.from_dev(self._dev[key])[:, 0]
+            self._cache[key] = v
+        return v
+
+    @property
+    def b(self):
+        return self._host("b")
+
+    @property
+    def W(self):
+        return self._host("W")
+
+    @property
+    def d1(self):
+        return self._host("d1")
+
+    @property
+    def d3(self):
+        return self._host("d3")
+
+    @property
+    def y(self):
+        return self._y
+
+    @property
+    def F(self):
+        return self._F
+
+    @property
+    def mu(self):
+        return self._F + self.b
+
+    def with_converged(self, flag):
+        s = LaplaceState(self._pattern, self._dev, self._y, self._F, self.logp, self.quad, self.objective,
+                         self.newton_iters, flag, self.cg_iters)
+        return s
+
+
+def _col(pattern, v):
+    return pattern.to_dev(np.asarray(v, dtype=float)[:, None])
+
+
+def find_mode(factor, lik, y, F, cfg, trace=None):
+    """Damped Newton iteration for the penalised-likelihood mode b*."""
+    _check_supported(cfg)
+    y = lik.validate(y)
+    F = np.asarray(F, dtype=float)
+    pat = factor.pattern
+    ctx = factor.ctx
+    n = factor.n
+    y_d, F_d = _col(pat, y), _col(pat, F)
+    b, W, d1, d3 = (dev.empty(ctx, n, 1) for _ in range(4))
+    lk = _lib.VlLik(lik.family_id, float(lik.shape_param))
+    nc = _lib.VlNewtonCfg(float(cfg.mode_cg_tol), int(cfg.cg_max_iter), int(cfg.newton_max_iter),
+                          float(cfg.newton_grad_tol), float(cfg.newton_obj_tol))
+    out = (C.c_double * 8)()
+    cg_its = np.zeros(max(cfg.newton_max_iter, 1), dtype=np.int32)
+    st = _lib.lib().vl_find_mode(ctx.h, factor.h, C.byref(lk), C.byref(nc), _lib.ptr(y_d), _lib.ptr(F_d),
+                                 _lib.ptr(b), _lib.ptr(W), _lib.ptr(d1), _lib.ptr(d3), out,
+                                 _lib.ptr(cg_its), int(cg_its.size))
+    state = LaplaceState(pat, {"b": b, "W": W, "d1": d1, "d3": d3, "y": y_d, "F": F_d}, y, F,
+                         out[0], out[1], out[2], int(out[4]), bool(out[5]), cg_its[: int(out[6])].tolist())
+    if trace is not None:
+        trace.append(state.objective)
+    if st == 42:
+        msg = _lib.lib().vl_last_error().decode()
+        raise ConvergenceError(msg, last_state=state.with_converged(False))
+    _lib.check(st)
+    return state
+
+
+class VaduPreconditioner:
+    """P = B^T diag(W + 1/D) B on the device (preconditioners.py:101-132)."""
+
+    name = "vadu"
+
+    def __init__(self, factor, W_dev, name="vadu"):
+        self.factor = factor
+        self.W_dev = W_dev
+        self.name = name
+        self._sums = None
+
+    def sums(self):
+        if self._sums is None:
+            out = np.zeros(6)
+            _lib.call("vl_factor_sums", self.factor.ctx.h, self.factor.h, _lib.ptr(self.W_dev), _lib.ptr(out))
+            self._sums = out
+        return self._sums
+
+    def logdet(self):
+        return float(self.sums()[1])
+
+
+def build_preconditioner(factor, W_dev, cfg):
+    _check_supported(cfg)
+    return VaduPreconditioner(factor, W_dev, cfg.preconditioner)
+
+
+_G_CACHE = []  # (pattern, seed, t, cols, tensor) -- SAA: same probes every evaluation
+
+
+def base_normals(factor, seed, t, cols=None):
+    """G = default_rng(seed).standard_normal((n, t)) in factor order (the
+    reference's VADU sample_block draw, preconditioners.py:121-122), uploaded
+    once and cached on the device (storage order).  ``cols`` selects a
+    contiguous column shard (multi-GPU)."""
+    pat = factor.pattern
+    key = (seed, t, cols)
+    for ent in _G_CACHE:
+        if ent[0] is pat and ent[1] == key:
+            return ent[2]
+    G = np.random.default_rng(seed).standard_normal((factor.n, t))
+    if cols is not None:
+        G = G[:, cols[0]:cols[1]]
+    Gd = pat.to_dev(np.ascontiguousarray(G))
+    _G_CACHE.append((pat, key, Gd))
+    del _G_CACHE[:-2]
+    return Gd
+
+
+def make_probes(factor, state, cfg, cols=None):
+    """Fresh N(0, P) probes for the current mode, deterministic in the seed."""
+    P = build_preconditioner(factor, state._dev["W"], cfg)
+    G = base_normals(factor, cfg.probe_seed, cfg.t, cols)
+    t = int(G.shape[1])
+    Z = dev.empty(factor.ctx, factor.n, t)
+    V = dev.empty(factor.ctx, factor.n, t)
+    w = np.zeros(t)
+    _lib.call("vl_probes_vadu", factor.ctx.h, factor.h, _lib.ptr(state._dev["W"]), t, _lib.ptr(G), _lib.ptr(Z),
+              _lib.ptr(V), _lib.ptr(w))
+    ps = ProbeSet(Z, cfg.probe_seed, P.name, pattern=factor.pattern, psolves_dev=V, weights=w,
+                  shard=(0 if cols is None else cols[0], cfg.t))
+    return ps, P
+
+
+def probes_from_Z(factor, state, cfg, Z):
+    """Inject caller-supplied probes (e.g. Rademacher): psolves are
+    computed with the full VADU solve P^-1 Z = B^-1 d^-1 B^-T Z."""
+    P = build_preconditioner(factor, state._dev["W"], cfg)
+    Z = np.asarray(Z, dtype=float)
+    Zd = factor.pattern.to_dev(Z)
+    n, t = Z.shape
+    # P^-1 Z = B^-1 (B^-T Z / d) ; d = W + 1/D
+    x = factor.solve_B(Z, transpose=True)
+    d = state.W + 1.0 / factor.D
+    V = factor.solve_B(x / d[:, None])
+    Vd = factor.pattern.to_dev(V)
+    w = np.einsum("it,it->t", Z, V)
+    return ProbeSet(Zd, cfg.probe_seed, P.name, pattern=factor.pattern, psolves_dev=Vd, weights=w), P
+
+
+def _run_probe_solves(factor, state, P, cfg, probes):
+    """CG-solve every probe at mode_cg_tol, capturing tridiagonals (laplace.py:290-309)."""
+    if probes.solves_dev is not None and len(probes.tridiags) == probes.t:
+        return
+    t = probes.t
+    U = dev.empty(factor.ctx, factor.n, t)
+    cap = int(cfg.cg_max_iter)
+    its = np.zeros(t, dtype=np.int32)
+    conv = np.zeros(t, dtype=np.int32)
+    res = np.zeros(t)
+    al = np.zeros((max(cap, 1), t))
+    be = np.zeros((max(cap, 1), t))
+    _lib.call("vl_pcg_vadu", factor.ctx.h, factor.h, _lib.ptr(state._dev["W"]), t, _lib.ptr(probes.Z_dev),
+              _lib.ptr(U), float(cfg.mode_cg_tol), int(cfg.cg_max_iter), 1, _lib.ptr(its), _lib.ptr(conv),
+              _lib.ptr(res), _lib.ptr(al), _lib.ptr(be), max(cap, 1))
+    probes.solves_dev = U
+    probes.iters = its
+    probes.tridiags = [tridiag_from_cg(al[:, c], be[:, c], int(its[c])) for c in range(t)]
+
+
+def solve_system(factor, state, rhs_dev, cfg, tol=None):
+    """u = (W + SigmaTilde^-1)^-1 rhs (eq6, VADU) for device rhs (n x k)."""
+    tol = cfg.cg_tol if tol is None else tol
+    k = int(rhs_dev.shape[1])
+    u = dev.empty(factor.ctx, factor.n, k)
+    its = np.zeros(k, dtype=np.int32)
+    conv = np.zeros(k, dtype=np.int32)
+    res = np.zeros(k)
+    _lib.call("vl_pcg_vadu", factor.ctx.h, factor.h, _lib.ptr(state._dev["W"]), k, _lib.ptr(rhs_dev), _lib.ptr(u),
+              float(tol), int(cfg.cg_max_iter), 0, _lib.ptr(its), _lib.ptr(conv), _lib.ptr(res), None, None, 1)
+    return u, its
+
+
+def slq_parts(probes):
+    """Per-probe SLQ terms w_i e1^T log(T_i) e1 (summed by the caller)."""
+    out = np.zeros(probes.t)
+    for i, tri in enumerate(probes.tridiags):
+        if tri.order:
+            out[i] = float(probes.weights[i]) * tri.quadrature_logdet()
+    return out
+
+
+def logdet_system(factor, state, cfg, probes=None, P=None, comm=None):
+    """log det(SigmaTilde W + I) = sum log D + log det P + SLQ (laplace.py:318-337)."""
+    _check_supported(cfg)
+    if P is None or probes is None:
+        probes, P = make_probes(factor, state, cfg)
+    if probes.precond_tag != P.name:
+        raise ConfigError("probes were drawn against a different preconditioner")
+    _run_probe_solves(factor, state, P, cfg, probes)
+    parts = slq_parts(probes)
+    if comm is not None:
+        parts = comm.allgather_cols(parts, probes.shard)
+    slq = float(sum(parts[i] for i in range(len(parts)))) / len(parts)
+    sums = P.sums()
+    return float(sums[0]) + float(sums[1]) + slq
+
+
+def neg_marginal_loglik(state, factor, cfg, probes=None, P=None, comm=None):
+    """Approximate negative log-marginal likelihood at the converged mode."""
+    if not state.converged:
+        raise ConvergenceError("state is not converged", last_state=state)
+    return -state.logp + 0.5 * state.quad + 0.5 * logdet_system(factor, state, cfg, probes=probes, P=P, comm=comm)
+
+
+def gradient(state, factor, lik, X, cfg, probes=None, P=None, comm=None):
+    """Full gradient: d theta (2,), d beta (p,), d xi (r,) (laplace.py:439-580)."""
+    if not state.converged:
+        raise ConvergenceError("state is not converged", last_state=state)
+    _check_supported(cfg)
+    X = np.asarray(X, dtype=float)
+    if X.ndim == 1:
+        X = X[:, None]
+    pat, ctx, n = factor.pattern, factor.ctx, factor.n
+    if P is None or probes is None:
+        probes, P = make_probes(factor, state, cfg)
+    _run_probe_solves(factor, state, P, cfg, probes)
+    dv = state._dev
+    t = probes.t
+    gamma = lik.n_xi > 0
+    md3x = None
+    if gamma:
+        md3x = dev.empty(ctx, n, 1)
+        junk = np.zeros(3)
+        _lib.call("vl_gamma_xi_terms", ctx.h, factor.h, _lib.ptr(dv["y"]), _lib.ptr(dv["F"]), _lib.ptr(dv["b"]),
+                  _lib.ptr(dv["W"]), _lib.ptr(dv["b"]), _lib.ptr(md3x), _lib.ptr(junk))
+    s = dev.empty(ctx, n, 1)
+    cols = np.zeros((4, t))
+    xicols = np.zeros((2, t))
+    if comm is not None and comm.world > 1:
+        s, cols, xicols = comm.grad_probe_pass(factor, state, probes, md3x)
+    else:
+        _lib.call("vl_grad_probe_pass", ctx.h, factor.h, _lib.ptr(dv["W"]), _lib.ptr(dv["d3"]),
+                  _lib.ptr(probes.solves_dev), _lib.ptr(probes.psolves_dev), t, _lib.ptr(s), _lib.ptr(cols),
+                  _lib.ptr(md3x) if gamma else None, _lib.ptr(xicols) if gamma else None)
+    tvec, _ = solve_system(factor, state, s, cfg, tol=cfg.mode_cg_tol)
+    terms = np.zeros(4)
+    _lib.call("vl_grad_scalar_terms", ctx.h, factor.h, _lib.ptr(dv["b"]), _lib.ptr(tvec), _lib.ptr(terms))
+    sums = P.sums()
+    dtheta = np.empty(2)
+    for k in (0, 1):
+        ex = float(sums[2 + k])
+        dPt = float(sums[4 + k])
+        h, r = cols[2 * k], cols[2 * k + 1]
+        ste = ste_combine(h, r, dPt)
+        dtheta[k] = 0.5 * terms[2 * k] + 0.5 * (ex + ste) - terms[2 * k + 1]
+    dxi = np.empty(lik.n_xi)
+    if gamma:
+        g3 = np.zeros(3)
+        _lib.call("vl_gamma_xi_terms", ctx.h, factor.h, _lib.ptr(dv["y"]), _lib.ptr(dv["F"]), _lib.ptr(dv["b"]),
+                  _lib.ptr(dv["W"]), _lib.ptr(tvec), _lib.ptr(md3x), _lib.ptr(g3))
+        a = lik.shape
+        dlogp = n * (np.log(a) + 1.0 - digamma(a)) + g3[0]
+        ste = ste_combine(xicols[0], xicols[1], float(g3[2]))
+        dxi[0] = -dlogp + 0.5 * (0.0 + ste) + g3[1]
+    p = X.shape[1]
+    dbeta = np.zeros(p)
+    if p:
+        Xd = pat.to_dev(np.ascontiguousarray(X))
+        _lib.call("vl_grad_dbeta", ctx.h, n, _lib.ptr(dv["d1"]), _lib.ptr(s), _lib.ptr(dv["W"]), _lib.ptr(tvec),
+                  _lib.ptr(Xd), p, _lib.ptr(dbeta))
+    return {"dtheta": dtheta, "dbeta": dbeta, "dxi": dxi}
