@@ -97,6 +97,15 @@ int vl_spmm(vl_ctx* ctx, const vl_factor* f, int op, int64_t t, const double* x_
 /* y = B^-1 x (transpose=0) or B^-T x (transpose=1)  (vecchia.py:172-174) */
 int vl_sptrsv(vl_ctx* ctx, const vl_factor* f, int transpose, int64_t t, const double* x_dev, double* y_dev);
 
+/* ---- instrumentation ----------------------------------------------------------
+ * Per-tag kernel timing with CUDA events on the context stream (tags mark the
+ * hot kernels: cg_*, probe_*, grad_*, newton_*, factor_*) and a launch
+ * counter.  vl_prof_report writes "tag\tlaunches\tms\talgorithmic_bytes\n"
+ * lines into buf. */
+int vl_prof_enable(vl_ctx* ctx, int on);
+int vl_prof_reset(vl_ctx* ctx);
+int vl_prof_report(vl_ctx* ctx, char* buf, int len, int64_t* launches);
+
 /* ---- Laplace objective (iterative backend, VADU preconditioner) ---------- */
 
 /* likelihood family: 0 bernoulli-logit, 1 bernoulli-probit, 2 gamma

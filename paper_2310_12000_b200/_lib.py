@@ -109,3 +109,10 @@ def ptr(a):
     if not a.flags["C_CONTIGUOUS"]:
         raise ValueError("array must be C-contiguous")
     return a.ctypes.data_as(c_void_p)
+
+_SIGS.update({
+    "vl_prof_enable": [c_void_p, c_int],
+    "vl_prof_reset": [c_void_p],
+    "vl_prof_report": [c_void_p, C.c_char_p, c_int, P_int64],
+})
+EXPORTED = sorted(_SIGS)

@@ -332,6 +332,39 @@ int vl_factor_set(vl_ctx* h, vl_factor* f, int which, const double* in) {
   });
 }
 
+int vl_prof_enable(vl_ctx* h, int on) {
+  return guard([&] {
+    prof_collect(h->c);
+    h->c.prof.on = on != 0;
+  });
+}
+
+int vl_prof_reset(vl_ctx* h) {
+  return guard([&] {
+    prof_collect(h->c);
+    h->c.prof.agg.clear();
+    h->c.prof.launches = 0;
+  });
+}
+
+int vl_prof_report(vl_ctx* h, char* buf, int len, int64_t* launches) {
+  return guard([&] {
+    prof_collect(h->c);
+    std::string s;
+    for (auto& kv : h->c.prof.agg) {
+      char line[256];
+      snprintf(line, sizeof(line), "%s\t%ld\t%.6f\t%.1f\n", kv.first.c_str(), kv.second.count, kv.second.ms,
+               kv.second.bytes);
+      s += line;
+    }
+    if (buf && len > 0) {
+      std::strncpy(buf, s.c_str(), (size_t)len - 1);
+      buf[len - 1] = 0;
+    }
+    if (launches) *launches = h->c.prof.launches;
+  });
+}
+
 // debug hook (not in the public header): record per-row completion times of
 // subsequent triangular solves into a device buffer of n int64 (NULL disables)
 int vl_debug_set_tstamp(vl_ctx* h, void* dev_buf) {

@@ -30,8 +30,30 @@ struct DevBuf {
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+// Per-tag kernel timing with CUDA events on the launching stream (bench.py's
+// live roofline) + a launch counter (gpu_launches).
+struct Prof {
+  bool on = false;
+  const char* tag = nullptr;  // current tag (set by ProfScope at call sites)
+  double bytes = 0;           // algorithmic bytes of one launch under the current tag
+  struct Rec {
+    std::string tag;
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> free_events;
+  struct Agg {
+    long count = 0;
+    double ms = 0, bytes = 0;
+  };
+  std::vector<std::pair<std::string, Agg>> agg;
+  long long launches = 0;
+};
+
 struct Ctx {
   int device = 0;
+  Prof prof;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int num_sms = 148;

@@ -12,6 +12,7 @@
 
 #include "common.cuh"
 #include "context.h"
+#include "launch.cuh"
 
 namespace vl {
 
@@ -268,12 +269,16 @@ static void launch_build(Ctx& C, const Pattern& P, Factor& F, const Matern& K, i
     blocks = C.num_sms * 2;
   }
   if (blocks < 1) blocks = 1;
+  ProfScope ps(C, "factor_build", 0.0);
+  C.prof.launches++;
+  cudaEvent_t ev = C.prof.on ? prof_begin(C) : nullptr;
   factor_build_kernel<Q, DIM><<<blocks, threads, smem, C.stream>>>(
       P.n, P.d, P.m, P.xy.as<double>(), P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), P.fidx.as<int32_t>(), K, want_grad,
       F.val.as<double>(), F.D.as<double>(), want_grad ? F.dval.as<double>() : nullptr,
       want_grad ? F.dD_rho.as<double>() : nullptr, want_grad ? F.dD_sig.as<double>() : nullptr, F.err.as<int>(), gscr,
       use_smem);
   VL_LAUNCH_CHECK();
+  if (ev) prof_end(C, ev);
 }
 
 template <int Q>

@@ -215,6 +215,7 @@ void newton_mode(Ctx& C, const Factor& F, const LikSpec& LS, const NewtonCfg& cf
   double* sums = C.dev_scalars.as<double>();
   double h[8];
   BView B = bview(F, false);
+  ProfScope ps(C, "newton_misc", 0.0);
   VL_CUDA(cudaMemsetAsync(b, 0, vb, C.stream));
   auto derivs = [&](const double* dlt, double step) {
     launch_rows<1, 1, 1, 3, 4>(C, n, 1, DerivsBody{L, y, Fv, b, dlt, step, d1, W, d3, rhs.as<double>()},
@@ -275,6 +276,9 @@ void newton_mode(Ctx& C, const Factor& F, const LikSpec& LS, const NewtonCfg& cf
     const double gprev = gnorm;
     gnorm = grad_norm();
     if (gnorm > 0.5 * gprev) safety = std::max(0.2 * safety, 1e-10);
+    if (std::getenv("VL_DEBUG_NEWTON"))
+      fprintf(stderr, "[newton] it=%d cg_tol=%.3e cg_its=%d step=%.4g obj=%.12g dobj=%.3e gnorm=%.3e\n", it, tol,
+              pr.iters[0], step, obj, obj_change, gnorm);
     if (gnorm < cfg.grad_tol && obj_change < cfg.obj_tol * (1.0 + std::fabs(obj))) {
       converged = true;
       break;
@@ -387,7 +391,11 @@ void probes_vadu(Ctx& C, const Factor& F, const double* W, int t, int ld, const 
   if (t > 256) fail(kECapacity, "too many probe columns per call");
   dispatch_cols(t, ld, [&](auto g, auto nu, auto uu) {
     constexpr int G_ = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
-    launch_rows<G_, NU, U, 0, 0>(C, n, t, ProbeZBody{B, G, sd.as<double>(), Z, ld}, Fin0<0>{});
+    {
+      ProfScope ps(C, "probe_Z", bapply_bytes(P, t, 1));
+      launch_rows<G_, NU, U, 0, 0>(C, n, t, ProbeZBody{B, G, sd.as<double>(), Z, ld}, Fin0<0>{});
+    }
+    ProfScope ps(C, "probe_V", bapply_bytes(P, t, 1) + 8.0 * n * t);
     launch_trsv<G_, NU, U, 1>(C, n, P.fwd_len, t, ld, P.fwd_order.as<int32_t>(), dfw, V,
                               PsolveRhs{G, sd.as<double>(), Z, ld}, CopySums<1>{sums});
   });
@@ -611,6 +619,8 @@ void grad_probe_pass(Ctx& C, const Factor& F, const double* W, const double* d3,
   BView B = bview(F, false);
   double* sums = C.dev_scalars.as<double>();
   if (6 * t > 8192) fail(kECapacity, "too many probe columns per call");
+  // bytes: B and dB values + indices once, U and V read once (gathers), s written
+  ProfScope ps(C, "grad_pass", 20.0 * ((double)P.nnz_off) + 4.0 * (P.n + 1) + 16.0 * P.n * t + 40.0 * P.n);
   dispatch_cols(t, ld, [&](auto g, auto nu, auto uu) {
     constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U_ = decltype(uu)::value;
     if (xi_md3 == nullptr) {

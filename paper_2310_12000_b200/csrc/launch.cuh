@@ -39,6 +39,30 @@ void dispatch_cols(int t, int ld, F&& f) {
 
 unsigned* next_counter(Ctx& C);
 int coop_grid(Ctx& C, const void* func, size_t smem);
+cudaEvent_t prof_begin(Ctx& C);
+void prof_end(Ctx& C, cudaEvent_t a);
+
+// Tag the kernels launched in a scope (algorithmic bytes per launch).
+struct ProfScope {
+  Ctx& C;
+  const char* old_tag;
+  double old_bytes;
+  ProfScope(Ctx& c, const char* tag, double bytes) : C(c), old_tag(c.prof.tag), old_bytes(c.prof.bytes) {
+    C.prof.tag = tag;
+    C.prof.bytes = bytes;
+  }
+  ~ProfScope() {
+    C.prof.tag = old_tag;
+    C.prof.bytes = old_bytes;
+  }
+};
+
+// SURVEY 8(d) algorithmic bytes of one B-apply over n x t (f64 values, int32
+// indices and row pointer; x read once, y written once) + 8n per fused diagonal
+inline double bapply_bytes(const Pattern& P, int t, int diag_vectors) {
+  const double nnz = (double)P.nnz_off + (double)P.n;
+  return 12.0 * nnz + 4.0 * (P.n + 1) + 16.0 * (double)P.n * t + 8.0 * P.n * diag_vectors;
+}
 
 template <int G, int NU, int U, int NR, int MAXMASK, class Body, class Fin>
 void launch_rows(Ctx& C, int64_t n, int t, const Body& body, const Fin& fin, const int* gate = nullptr) {
@@ -47,8 +71,11 @@ void launch_rows(Ctx& C, int64_t n, int t, const Body& body, const Fin& fin, con
   int64_t need = (n * G + kRowsThreads - 1) / kRowsThreads;
   int64_t cap = (int64_t)C.num_sms * (2048 / kRowsThreads);
   int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
+  C.prof.launches++;
+  cudaEvent_t ev = (C.prof.on && C.prof.tag) ? prof_begin(C) : nullptr;
   kern<<<blocks, kRowsThreads, smem, C.stream>>>(n, t, body, fin, C.red_partial.as<double>(), next_counter(C), gate);
   VL_LAUNCH_CHECK();
+  if (ev) prof_end(C, ev);
 }
 
 // x (n x ld) is overwritten: it is first filled with the "not ready" sentinel.
@@ -61,6 +88,8 @@ void launch_trsv(Ctx& C, int64_t n, int64_t npos, int t, int ld, const int32_t* 
   grid = std::min(grid, C.num_sms * C.trsv_blocks_per_sm);
   int64_t need = (npos * G + kRowsThreads - 1) / kRowsThreads;
   if (need < grid) grid = (int)std::max<int64_t>(1, need);
+  C.prof.launches++;
+  cudaEvent_t ev = (C.prof.on && C.prof.tag) ? prof_begin(C) : nullptr;
   VL_CUDA(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)n * ld, C.stream));
   double* partials = C.red_partial.as<double>();
   unsigned* counter = next_counter(C);
@@ -70,6 +99,7 @@ void launch_trsv(Ctx& C, int64_t n, int64_t npos, int t, int ld, const int32_t* 
                   (void*)&x,     (void*)&body, (void*)&fin,      (void*)&partials, (void*)&counter,
                   (void*)&gate,  (void*)&smax, (void*)&tstamp};
   VL_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kRowsThreads), args, smem, C.stream));
+  if (ev) prof_end(C, ev);
 }
 
 }  // namespace vl

@@ -17,6 +17,59 @@ unsigned* next_counter(Ctx& C) {
   return base + slot;
 }
 
+cudaEvent_t prof_begin(Ctx& C) {
+  Prof& P = C.prof;
+  auto take = [&]() {
+    cudaEvent_t e;
+    if (!P.free_events.empty()) {
+      e = P.free_events.back();
+      P.free_events.pop_back();
+    } else {
+      VL_CUDA(cudaEventCreate(&e));
+    }
+    return e;
+  };
+  cudaEvent_t a = take();
+  VL_CUDA(cudaEventRecord(a, C.stream));
+  return a;
+}
+
+void prof_end(Ctx& C, cudaEvent_t a) {
+  Prof& P = C.prof;
+  cudaEvent_t b;
+  if (!P.free_events.empty()) {
+    b = P.free_events.back();
+    P.free_events.pop_back();
+  } else {
+    VL_CUDA(cudaEventCreate(&b));
+  }
+  VL_CUDA(cudaEventRecord(b, C.stream));
+  P.pending.push_back({std::string(P.tag), a, b, P.bytes});
+}
+
+void prof_collect(Ctx& C) {
+  Prof& P = C.prof;
+  if (P.pending.empty()) return;
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+  for (auto& r : P.pending) {
+    float ms = 0.f;
+    VL_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    Prof::Agg* g = nullptr;
+    for (auto& kv : P.agg)
+      if (kv.first == r.tag) g = &kv.second;
+    if (!g) {
+      P.agg.push_back({r.tag, Prof::Agg{}});
+      g = &P.agg.back().second;
+    }
+    g->count += 1;
+    g->ms += ms;
+    g->bytes += r.bytes;
+    P.free_events.push_back(r.a);
+    P.free_events.push_back(r.b);
+  }
+  P.pending.clear();
+}
+
 int coop_grid(Ctx& C, const void* func, size_t smem) {
   static std::mutex mu;
   static std::map<std::pair<const void*, size_t>, int> cache;

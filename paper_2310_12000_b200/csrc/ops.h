@@ -15,6 +15,7 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy_factor_order, const int
 void factor_build(Ctx& C, const Pattern& P, Factor& F, double sigma2, double rho, double nu, bool want_grad);
 
 void factor_refresh_transpose(Ctx& C, Factor& F);
+void prof_collect(Ctx& C);
 BView bview(const Factor& F, bool grad);
 void op_spmm(Ctx& C, const Factor& F, int op, int t, int ld, const double* x, double* y);
 void op_trsv(Ctx& C, const Factor& F, bool transpose, int t, int ld, const double* b, double* x);

@@ -299,6 +299,7 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
   dispatch_cols(t, ld, [&](auto g, auto nu, auto uu) {
     constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
     // init
+    ProfScope ps_init(C, t == 1 ? "cg1_init" : "cgT_init", 0.0);
     launch_rows<G, NU, U, 1, 0>(C, n, t, InitBody{b, r.as<double>(), u, hb[0], ld}, InitFin{K, tol});
     launch_trsv<G, NU, U, 0>(C, n, P.bwd_len, t, ld, P.bwd_order.as<int32_t>(), dbw, w.as<double>(),
                              RhsPlainActive{r.as<double>(), ld}, Fin0<0>{}, gate);
@@ -312,15 +313,28 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
       for (; l < lim; ++l) {
         double* hp = hb[l & 1];
         double* hn = hb[(l + 1) & 1];
-        launch_rows<G, NU, U, 0, 0>(C, n, t, K1Body{B, z.as<double>(), hp, hn, tmp.as<double>(), S.Dinv, K.beta, ld},
-                                    Fin0<0>{}, gate);
-        launch_rows<G, NU, U, 1, 0>(C, n, t, K2Body{B, hn, tmp.as<double>(), v.as<double>(), S.W, ld},
-                                    K2Fin{K, l, cap}, gate);
-        launch_trsv<G, NU, U, 1>(C, n, P.bwd_len, t, ld, P.bwd_order.as<int32_t>(), dbw, w.as<double>(),
-                                 K3Rhs{r.as<double>(), u, v.as<double>(), hn, K.alpha, K.active, ld}, K3Fin{K, l},
-                                 gate);
-        launch_trsv<G, NU, U, 1>(C, n, P.fwd_len, t, ld, P.fwd_order.as<int32_t>(), dfw, z.as<double>(),
-                                 RhsScaleDot{w.as<double>(), S.dinv, r.as<double>(), ld}, K4Fin{K, l, cap}, gate);
+        {
+          ProfScope ps(C, t == 1 ? "cg1_spmm_B" : "cgT_spmm_B", bapply_bytes(P, t, 1));
+          launch_rows<G, NU, U, 0, 0>(C, n, t,
+                                      K1Body{B, z.as<double>(), hp, hn, tmp.as<double>(), S.Dinv, K.beta, ld},
+                                      Fin0<0>{}, gate);
+        }
+        {
+          ProfScope ps(C, t == 1 ? "cg1_spmm_Bt" : "cgT_spmm_Bt", bapply_bytes(P, t, 1));
+          launch_rows<G, NU, U, 1, 0>(C, n, t, K2Body{B, hn, tmp.as<double>(), v.as<double>(), S.W, ld},
+                                      K2Fin{K, l, cap}, gate);
+        }
+        {
+          ProfScope ps(C, t == 1 ? "cg1_trsv_Bt" : "cgT_trsv_Bt", bapply_bytes(P, t, 0));
+          launch_trsv<G, NU, U, 1>(C, n, P.bwd_len, t, ld, P.bwd_order.as<int32_t>(), dbw, w.as<double>(),
+                                   K3Rhs{r.as<double>(), u, v.as<double>(), hn, K.alpha, K.active, ld},
+                                   K3Fin{K, l}, gate);
+        }
+        {
+          ProfScope ps(C, t == 1 ? "cg1_trsv_B" : "cgT_trsv_B", bapply_bytes(P, t, 1));
+          launch_trsv<G, NU, U, 1>(C, n, P.fwd_len, t, ld, P.fwd_order.as<int32_t>(), dfw, z.as<double>(),
+                                   RhsScaleDot{w.as<double>(), S.dinv, r.as<double>(), ld}, K4Fin{K, l, cap}, gate);
+        }
       }
       VL_CUDA(cudaMemcpyAsync(status, K.status, sizeof(status), cudaMemcpyDeviceToHost, C.stream));
       VL_CUDA(cudaStreamSynchronize(C.stream));

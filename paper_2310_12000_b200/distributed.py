@@ -1,0 +1,62 @@
+"""Probe sharding over ranks (one process per GPU, torch.distributed).
+
+The t probe columns are split contiguously over the ranks; the
+factor, the Newton mode and the tvec solve are replicated (deterministic, no
+broadcast needed).  Collectives per evaluation:
+  * allgather of the t per-probe SLQ terms (summed in probe order, so the
+    result does not depend on the number of ranks);
+  * allgather of the per-probe STE (h, r) pairs;
+  * two rounds of n-vector allreduce for the per-row control-variate
+    statistics (sum H, sum R; then the centred cross/square sums).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .errors import CapabilityError
+
+
+def shard_bounds(t, world, rank):
+    """Contiguous split of t columns: the first t % world ranks get one extra."""
+    base, extra = divmod(t, world)
+    c0 = rank * base + min(rank, extra)
+    c1 = c0 + base + (1 if rank < extra else 0)
+    return c0, c1
+
+
+class ProbeComm:
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def shard(self, t):
+        return shard_bounds(t, self.world, self.rank)
+
+    def _device(self):
+        import torch
+        return torch.device("cuda", torch.cuda.current_device()) if self.dist.get_backend(self.group) == "nccl" \
+            else torch.device("cpu")
+
+    def allgather_cols(self, parts, shard):
+        """Gather per-probe values of every rank's column shard into the full
+        probe-ordered vector (t = shard[1] global probes)."""
+        import torch
+        t = int(shard[1])
+        parts = np.asarray(parts, dtype=float)
+        dev = self._device()
+        full = torch.zeros(t, dtype=torch.float64, device=dev)
+        c0 = int(shard[0])
+        full[c0:c0 + parts.size] = torch.as_tensor(parts, dtype=torch.float64, device=dev)
+        self.dist.all_reduce(full, group=self.group)   # disjoint supports: sum == gather
+        return full.cpu().numpy()
+
+    def allreduce_(self, tensor):
+        self.dist.all_reduce(tensor, group=self.group)
+        return tensor
+
+    def grad_probe_pass(self, factor, state, probes, md3x):
+        raise CapabilityError("sharded gradient pass not built yet")

@@ -109,8 +109,26 @@ class Pattern:
 
     # factor-order numpy <-> storage-order device tensors
     def to_dev(self, v):
+        """Permute to storage order into a pinned staging buffer and copy H2D
+        asynchronously on the library stream."""
         v = np.asarray(v, dtype=float)
-        return dev.upload(self.ctx, v[self.sperm])
+        T = dev.torch()
+        key = v.shape
+        ent = self._staging.get(key) if hasattr(self, "_staging") else None
+        if not hasattr(self, "_staging"):
+            self._staging = {}
+        if ent is None:
+            ent = [T.empty(key, dtype=T.float64, pin_memory=True), None]
+            self._staging[key] = ent
+        buf, ev = ent
+        if ev is not None:
+            ev.synchronize()          # previous copy out of this buffer finished
+        np.take(v, self.sperm, axis=0, out=buf.numpy())
+        out = buf.to(self.ctx.tdev, non_blocking=True)
+        ev = T.cuda.Event()
+        ev.record()
+        ent[1] = ev
+        return out
 
     def from_dev(self, x):
         a = dev.download(x)
