@@ -146,6 +146,42 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
   upload(C, P.tmap, tmap);
   P.fwd_len = (int64_t)fwd.size();
   P.bwd_len = (int64_t)bwd.size();
+  upload(C, P.fwd_lptr, P.fwd_level_ptr);
+  upload(C, P.bwd_lptr, P.bwd_level_ptr);
+  // single-RHS work items: 32-row chunks, expanded to per-row (warp-per-row)
+  // items on thin levels and for chunks holding a row with many dependencies
+  int heavy_rows = 64, heavy_deps = 40;
+  if (const char* e = std::getenv("VL_HEAVY_LEVEL_ROWS")) heavy_rows = std::atoi(e);
+  if (const char* e = std::getenv("VL_HEAVY_DEPS")) heavy_deps = std::atoi(e);
+  auto items = [&](const std::vector<int32_t>& order, const std::vector<int32_t>& lptr, bool fwd_dir) {
+    std::vector<uint32_t> it;
+    for (size_t L = 0; L + 1 < lptr.size(); ++L) {
+      const int32_t q0 = lptr[L], q1 = lptr[L + 1];
+      const bool thin = (q1 - q0) <= heavy_rows;
+      for (int32_t c = q0; c < q1; c += 32) {
+        bool heavy = thin;
+        for (int32_t p = c; p < c + 32 && !heavy; ++p) {
+          const int32_t s = order[p];
+          if (s < 0) continue;
+          const int deg = fwd_dir ? cnt[s] : (tptr[s + 1] - tptr[s]);
+          if (deg > heavy_deps) heavy = true;
+        }
+        if (!heavy) {
+          it.push_back((uint32_t)c);
+        } else {
+          for (int32_t p = c; p < c + 32; ++p)
+            if (order[p] >= 0) it.push_back((uint32_t)p | 0x80000000u);
+        }
+      }
+    }
+    return it;
+  };
+  auto fi = items(fwd, P.fwd_level_ptr, true);
+  auto bi = items(bwd, P.bwd_level_ptr, false);
+  P.fwd_nitems = (int64_t)fi.size();
+  P.bwd_nitems = (int64_t)bi.size();
+  upload(C, P.fwd_items, fi);
+  upload(C, P.bwd_items, bi);
   VL_CUDA(cudaStreamSynchronize(C.stream));
 }
 
@@ -174,6 +210,8 @@ int vl_ctx_create(int device, void* stream, vl_ctx** out) {
     C.num_sms = prop.multiProcessorCount;
     if (const char* e = std::getenv("VL_TRSV_BPS")) C.trsv_blocks_per_sm = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("VL_SPIN_MAX_NS")) C.spin_max_ns = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("VL_THIN_PASSES")) C.thin_passes = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("VL_MIN_THICK")) C.min_thick_levels = std::max(0, std::atoi(e));
     try {
       // NULL selects the legacy default stream (same as torch's default stream)
       C.stream = (cudaStream_t)stream;

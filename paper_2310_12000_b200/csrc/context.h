@@ -62,6 +62,9 @@ struct Ctx {
   int trsv_blocks_per_sm = 2;
   // max nanosleep backoff while spinning on a dependency (0 = pure polling)
   int spin_max_ns = 64;
+  // thin solve levels: <= thin_passes * (1024 / G) rows run on a single CTA
+  int thin_passes = 0;
+  int min_thick_levels = 4;
   // debug: per-row completion timestamps of the next triangular solves (n entries)
   long long* debug_tstamp = nullptr;
   // deterministic reduction scratch: per-block partials + ticket counters
@@ -96,6 +99,9 @@ struct Pattern {
   DevBuf fwd_order; // fwd_len int32 storage rows in (level, position) order, levels padded to 32 with -1
   DevBuf bwd_order; // bwd_len int32 storage rows in (height, position) order, padded likewise
   int64_t fwd_len = 0, bwd_len = 0;
+  DevBuf fwd_lptr, bwd_lptr;  // device copies of the padded level pointers
+  DevBuf fwd_items, bwd_items;  // single-RHS work items (light 32-row chunks / heavy rows)
+  int64_t fwd_nitems = 0, bwd_nitems = 0;
   DevBuf tptr;      // n+1  int32 children CSR (= CSR of B^T) in storage order
   DevBuf tidx;      // nnz  int32 child storage row
   DevBuf tmap;      // nnz  int32 ELL slot (child*m + k) holding B[child, s]

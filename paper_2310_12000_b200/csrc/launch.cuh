@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <type_traits>
+#include <vector>
 
 #include "context.h"
 #include "rows.cuh"
@@ -78,27 +79,100 @@ void launch_rows(Ctx& C, int64_t n, int t, const Body& body, const Fin& fin, con
   if (ev) prof_end(C, ev);
 }
 
-// x (n x ld) is overwritten: it is first filled with the "not ready" sentinel.
+// Split a level sequence (padded position pointer, nlev levels) into
+// alternating thin / thick segments: a level is thin when it has at most
+// `thin_rows` (padded) rows.  Returns {L0, L1, thin}.
+struct Seg {
+  int L0, L1;
+  bool thin;
+};
+std::vector<Seg> solve_segments(const std::vector<int32_t>& lptr, int thin_rows, int min_thick_levels);
+
+// Triangular solve over the fwd (B) or bwd (B^T) schedule.  x (n x ld) is
+// overwritten: it is first filled with the "not ready" sentinel; thin
+// segments run on one CTA, thick segments grid-wide (sync-free).  Fused
+// column reductions finalise once over all segments' partial slots.
 template <int G, int NU, int U, int NR, class Deps, class Body, class Fin>
-void launch_trsv(Ctx& C, int64_t n, int64_t npos, int t, int ld, const int32_t* order, const Deps& deps, double* x,
-                 const Body& body, const Fin& fin, const int* gate = nullptr) {
+void launch_trsv(Ctx& C, const Pattern& P, bool fwd, int t, int ld, const Deps& deps, double* x, const Body& body,
+                 const Fin& fin, const int* gate = nullptr) {
+  const int64_t n = P.n;
+  const int32_t* order = fwd ? P.fwd_order.as<int32_t>() : P.bwd_order.as<int32_t>();
+  if constexpr (G == 1 && NU == 1 && U == 1) {
+    if (C.thin_passes == 0) {
+      // single right-hand side: light/heavy work items, one sync-free launch
+      auto k1 = trsv1_kernel<NR, Deps, Body, Fin>;
+      const size_t smem1 = red_smem_bytes<1, 1, 1, NR>(kRowsThreads, 1);
+      int grid = coop_grid(C, (const void*)k1, smem1);
+      grid = std::min(grid, C.num_sms * C.trsv_blocks_per_sm);
+      const int64_t nitems = fwd ? P.fwd_nitems : P.bwd_nitems;
+      const int64_t npos = fwd ? P.fwd_len : P.bwd_len;
+      const uint32_t* items = fwd ? P.fwd_items.as<uint32_t>() : P.bwd_items.as<uint32_t>();
+      C.prof.launches += 2;
+      cudaEvent_t ev = (C.prof.on && C.prof.tag) ? prof_begin(C) : nullptr;
+      VL_CUDA(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)n * ld, C.stream));
+      double* partials = C.red_partial.as<double>();
+      unsigned* counter = next_counter(C);
+      unsigned smax = (unsigned)C.spin_max_ns;
+      long long* tstamp = C.debug_tstamp;
+      void* args[] = {(void*)&nitems, (void*)&npos,     (void*)&items,   (void*)&order, (void*)&deps,
+                      (void*)&x,      (void*)&body,     (void*)&fin,     (void*)&partials, (void*)&counter,
+                      (void*)&gate,   (void*)&smax,     (void*)&tstamp};
+      VL_CUDA(cudaLaunchCooperativeKernel((const void*)k1, dim3(grid), dim3(kRowsThreads), args, smem1, C.stream));
+      if (ev) prof_end(C, ev);
+      return;
+    }
+  }
+  const int32_t* lptr_d = fwd ? P.fwd_lptr.as<int32_t>() : P.bwd_lptr.as<int32_t>();
+  const std::vector<int32_t>& lptr = fwd ? P.fwd_level_ptr : P.bwd_level_ptr;
   auto kern = trsv_kernel<G, NU, U, NR, Deps, Body, Fin>;
+  auto tkern = trsv_thin_kernel<G, NU, U, NR, Deps, Body, Fin>;
   const size_t smem = red_smem_bytes<G, NU, U, NR>(kRowsThreads, t);
-  int grid = coop_grid(C, (const void*)kern, smem);
-  grid = std::min(grid, C.num_sms * C.trsv_blocks_per_sm);
-  int64_t need = (npos * G + kRowsThreads - 1) / kRowsThreads;
-  if (need < grid) grid = (int)std::max<int64_t>(1, need);
-  C.prof.launches++;
+  const size_t tsmem = red_smem_bytes<G, NU, U, NR>(kThinThreads, t);
+  const int thin_rows = C.thin_passes * (kThinThreads / G);
+  std::vector<Seg> segs = solve_segments(lptr, thin_rows, C.min_thick_levels);
+  int gcap = coop_grid(C, (const void*)kern, smem);
+  gcap = std::min(gcap, C.num_sms * C.trsv_blocks_per_sm);
+  std::vector<int> grids(segs.size(), 1);
+  int total = 0;
+  for (size_t i = 0; i < segs.size(); ++i) {
+    if (!segs[i].thin) {
+      const int64_t npos = (int64_t)lptr[segs[i].L1] - lptr[segs[i].L0];
+      const int64_t need = (npos * G + kRowsThreads - 1) / kRowsThreads;
+      grids[i] = (int)std::max<int64_t>(1, std::min<int64_t>(need, gcap));
+    }
+    total += grids[i];
+  }
+  C.prof.launches += 1 + (long long)segs.size();
   cudaEvent_t ev = (C.prof.on && C.prof.tag) ? prof_begin(C) : nullptr;
   VL_CUDA(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)n * ld, C.stream));
   double* partials = C.red_partial.as<double>();
   unsigned* counter = next_counter(C);
   unsigned smax = (unsigned)C.spin_max_ns;
   long long* tstamp = C.debug_tstamp;
-  void* args[] = {(void*)&npos,  (void*)&t,    (void*)&ld,       (void*)&order,   (void*)&deps,
-                  (void*)&x,     (void*)&body, (void*)&fin,      (void*)&partials, (void*)&counter,
-                  (void*)&gate,  (void*)&smax, (void*)&tstamp};
-  VL_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kRowsThreads), args, smem, C.stream));
+  int slot = 0;
+  for (size_t i = 0; i < segs.size(); ++i) {
+    TrsvLaunch L;
+    L.L0 = segs[i].L0;
+    L.L1 = segs[i].L1;
+    L.p0 = lptr[segs[i].L0];
+    L.p1 = lptr[segs[i].L1];
+    L.lptr = lptr_d;
+    L.slot_base = slot;
+    L.total_slots = total;
+    slot += grids[i];
+    if (segs[i].thin) {
+      if (tsmem > 48 * 1024) VL_CUDA(cudaFuncSetAttribute(tkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
+      tkern<<<1, kThinThreads, tsmem, C.stream>>>(L, t, ld, order, deps, x, body, fin, partials, counter, gate,
+                                                  tstamp);
+      VL_LAUNCH_CHECK();
+    } else {
+      void* args[] = {(void*)&L,     (void*)&t,       (void*)&ld,       (void*)&order,   (void*)&deps,
+                      (void*)&x,     (void*)&body,    (void*)&fin,      (void*)&partials, (void*)&counter,
+                      (void*)&gate,  (void*)&smax,    (void*)&tstamp};
+      VL_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grids[i]), dim3(kRowsThreads), args, smem,
+                                          C.stream));
+    }
+  }
   if (ev) prof_end(C, ev);
 }
 

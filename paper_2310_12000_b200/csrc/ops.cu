@@ -70,6 +70,28 @@ void prof_collect(Ctx& C) {
   P.pending.clear();
 }
 
+std::vector<Seg> solve_segments(const std::vector<int32_t>& lptr, int thin_rows, int min_thick_levels) {
+  std::vector<Seg> segs;
+  const int nl = (int)lptr.size() - 1;
+  int L = 0;
+  while (L < nl) {
+    const bool thin = (lptr[L + 1] - lptr[L]) <= thin_rows;
+    int E = L + 1;
+    while (E < nl && ((lptr[E + 1] - lptr[E]) <= thin_rows) == thin) ++E;
+    segs.push_back({L, E, thin});
+    L = E;
+  }
+  // short thick runs are cheaper on the single CTA than a grid launch
+  for (auto& s : segs)
+    if (!s.thin && s.L1 - s.L0 < min_thick_levels) s.thin = true;
+  std::vector<Seg> merged;
+  for (auto& s : segs) {
+    if (!merged.empty() && merged.back().thin == s.thin) merged.back().L1 = s.L1;
+    else merged.push_back(s);
+  }
+  return merged;
+}
+
 int coop_grid(Ctx& C, const void* func, size_t smem) {
   static std::mutex mu;
   static std::map<std::pair<const void*, size_t>, int> cache;
@@ -118,11 +140,11 @@ void op_trsv(Ctx& C, const Factor& F, bool transpose, int t, int ld, const doubl
     constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(u)::value;
     if (!transpose) {
       DepsEll deps{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
-      launch_trsv<G, NU, U, 0>(C, P.n, P.fwd_len, t, ld, P.fwd_order.as<int32_t>(), deps, x, TrsvPlain{b, ld},
+      launch_trsv<G, NU, U, 0>(C, P, true, t, ld, deps, x, TrsvPlain{b, ld},
                                Fin0<0>{});
     } else {
       DepsCsr deps{P.tptr.as<int32_t>(), P.tidx.as<int32_t>(), F.valT.as<double>()};
-      launch_trsv<G, NU, U, 0>(C, P.n, P.bwd_len, t, ld, P.bwd_order.as<int32_t>(), deps, x, TrsvPlain{b, ld},
+      launch_trsv<G, NU, U, 0>(C, P, false, t, ld, deps, x, TrsvPlain{b, ld},
                                Fin0<0>{});
     }
   });

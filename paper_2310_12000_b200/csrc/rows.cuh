@@ -105,17 +105,20 @@ VL_D void block_reduce_cols(double (&acc)[NR > 0 ? NR : 1][NU * U], int t, doubl
 }
 
 // Grid-level finalisation by the last CTA to finish (fixed block order).
+// `total_slots` partial slots may be filled by several stream-ordered
+// launches (the solve segments); the CTA drawing the last ticket reduces all.
 template <int NR, int MAXMASK, class Fin>
-VL_D void grid_finalize(const double* partials, unsigned* counter, int t, const Fin& fin, double* sh) {
+VL_D void grid_finalize(const double* partials, unsigned* counter, int t, const Fin& fin, double* sh,
+                        int total_slots = -1) {
   if constexpr (NR == 0) return;
+  const int nb = total_slots > 0 ? total_slots : (int)gridDim.x;
   __threadfence();
   __syncthreads();
   __shared__ unsigned s_ticket;
   if (threadIdx.x == 0) s_ticket = atomicAdd(counter, 1u);
   __syncthreads();
-  if (s_ticket != gridDim.x - 1) return;
+  if (s_ticket != (unsigned)nb - 1) return;
   __threadfence();
-  const int nb = gridDim.x;
   for (int idx = threadIdx.x; idx < NR * t; idx += blockDim.x) {
     const int r = idx / t;
     double s = 0.0;
@@ -214,70 +217,51 @@ struct DepsCsr {
   VL_D double w(int64_t b) const { return val[b]; }
 };
 
-template <int G, int NU, int U, int NR, class Deps, class Body, class Fin>
-__global__ void __launch_bounds__(kRowsThreads) trsv_kernel(int64_t npos, int t, int ld,
-                                                            const int32_t* __restrict__ order, Deps deps,
-                                                            double* __restrict__ x, Body body, Fin fin,
-                                                            double* __restrict__ partials,
-                                                            unsigned* __restrict__ counter,
-                                                            const int* __restrict__ gate, unsigned smax,
-                                                            long long* __restrict__ tstamp) {
-  if (gate != nullptr && *((volatile const int*)gate) == 0) return;
-  extern __shared__ double rsh[];
-  constexpr int GPW = 32 / G;
+// One solve row per group: rhs, dependency gather (optionally polling the
+// sentinel), epilogue and store.  Called by every lane of the warp.
+template <int G, int NU, int U, bool POLL, class Deps, class Body>
+VL_D void trsv_row(int64_t p, int64_t pend_, int t, int ld, const int32_t* __restrict__ order, const Deps& deps,
+                   double* __restrict__ x, const Body& body, unsigned smax, long long* __restrict__ tstamp, int gl,
+                   double (&acc0)[NU * U]) {
   constexpr int NC = NU * U;
-  constexpr int NRR = NR > 0 ? NR : 1;
-  constexpr int BATCH = (NC <= 2) ? 8 : 4;
+  constexpr int BATCH = (NC == 1) ? 32 : (NC == 2 ? 16 : 8);
   using CL = Cols<G, NU, U>;
-  const int lane = threadIdx.x & 31;
-  const int gl = lane % G;
-  const int gi = lane / G;
-  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  double acc[NRR][NC];
+  const int32_t so = (p < pend_) ? order[p] : -1;
+  const bool valid = so >= 0;
+  const int64_t s = valid ? so : 0;
+  double xs[NC];
 #pragma unroll
-  for (int r = 0; r < NRR; ++r)
+  for (int i = 0; i < NC; ++i) {
+    const int c = CL::col(gl, i);
+    xs[i] = (valid && c < t) ? body.rhs(s, c, acc0[i]) : 0.0;
+  }
+  const int cs = valid ? deps.count(s) : 0;
+  const int64_t b0 = valid ? deps.base(s) : 0;
+  const int cmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)cs);
+  for (int e0 = 0; e0 < cmax; e0 += BATCH) {
+    int32_t j[BATCH];
+    double w[BATCH];
+    double v[BATCH][NC];
 #pragma unroll
-    for (int i = 0; i < NC; ++i) acc[r][i] = 0.0;
-
-  for (int64_t pbase = gwarp * GPW; pbase < npos; pbase += nwarps * GPW) {
-    const int64_t p = pbase + gi;
-    const int32_t so = (p < npos) ? order[p] : -1;
-    const bool valid = so >= 0;
-    const int64_t s = valid ? so : 0;
-    double xs[NC];
-#pragma unroll
-    for (int i = 0; i < NC; ++i) {
-      const int c = CL::col(gl, i);
-      xs[i] = (valid && c < t) ? body.rhs(s, c, acc[0][i]) : 0.0;
+    for (int q = 0; q < BATCH; ++q) {
+      const bool on = e0 + q < cs;
+      j[q] = on ? deps.idx(b0 + e0 + q) : 0;
+      w[q] = on ? deps.w(b0 + e0 + q) : 0.0;
     }
-    const int cs = valid ? deps.count(s) : 0;
-    const int64_t b0 = valid ? deps.base(s) : 0;
-    // Warp-converged dependency loop: all lanes issue a batch of loads, then
-    // the whole warp re-polls the still-pending ones together.
-    const int cmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)cs);
-    for (int e0 = 0; e0 < cmax; e0 += BATCH) {
-      int32_t j[BATCH];
-      double w[BATCH];
-      double v[BATCH][NC];
 #pragma unroll
-      for (int q = 0; q < BATCH; ++q) {
-        const bool on = e0 + q < cs;
-        j[q] = on ? deps.idx(b0 + e0 + q) : 0;
-        w[q] = on ? deps.w(b0 + e0 + q) : 0.0;
-      }
+    for (int q = 0; q < BATCH; ++q)
 #pragma unroll
-      for (int q = 0; q < BATCH; ++q)
+      for (int k = 0; k < NU; ++k) {
+        const int c = U * (gl + G * k);
+        if (e0 + q < cs && c < t) {
+          ld_cg_unit<U>(x + (int64_t)j[q] * ld + c, &v[q][U * k]);
+        } else {
 #pragma unroll
-        for (int k = 0; k < NU; ++k) {
-          const int c = U * (gl + G * k);
-          if (e0 + q < cs && c < t) {
-            ld_cg_unit<U>(x + (int64_t)j[q] * ld + c, &v[q][U * k]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < U; ++i) v[q][U * k + i] = 0.0;
-          }
+          for (int i = 0; i < U; ++i) v[q][U * k + i] = 0.0;
         }
+      }
+    if constexpr (POLL) {
+      // warp-converged polling: the whole warp re-polls its pending entries together
       unsigned ns = 8;
       for (;;) {
         bool pend = false;
@@ -300,30 +284,149 @@ __global__ void __launch_bounds__(kRowsThreads) trsv_kernel(int64_t npos, int t,
             if (pk) ld_cg_unit<U>(x + (int64_t)j[q] * ld + U * (gl + G * k), &v[q][U * k]);
           }
       }
-#pragma unroll
-      for (int q = 0; q < BATCH; ++q)
-#pragma unroll
-        for (int i = 0; i < NC; ++i) xs[i] -= w[q] * v[q][i];
     }
-    if (valid) {
 #pragma unroll
-      for (int i = 0; i < NC; ++i) {
-        const int c = CL::col(gl, i);
-        if (c < t) body.out(s, c, xs[i], acc[0][i]);
-      }
+    for (int q = 0; q < BATCH; ++q)
 #pragma unroll
-      for (int k = 0; k < NU; ++k) {
-        const int c = U * (gl + G * k);
-        if (c < t) {
-          double* dst = x + s * ld + c;
-          if constexpr (U == 2) {
-            *reinterpret_cast<double2*>(dst) = make_double2(sanitize(xs[2 * k]), sanitize(xs[2 * k + 1]));
-          } else {
-            *dst = sanitize(xs[k]);
-          }
+      for (int i = 0; i < NC; ++i) xs[i] -= w[q] * v[q][i];
+  }
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int c = CL::col(gl, i);
+      if (c < t) body.out(s, c, xs[i], acc0[i]);
+    }
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+      const int c = U * (gl + G * k);
+      if (c < t) {
+        double* dst = x + s * ld + c;
+        if constexpr (U == 2) {
+          __stcg(reinterpret_cast<double2*>(dst), make_double2(sanitize(xs[2 * k]), sanitize(xs[2 * k + 1])));
+        } else {
+          __stcg(dst, sanitize(xs[k]));
         }
       }
-      if (tstamp != nullptr && gl == 0) {
+    }
+    if (tstamp != nullptr && gl == 0) {
+      long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      tstamp[s] = g;
+    }
+  }
+}
+
+struct TrsvLaunch {
+  int64_t p0, p1;          // position range (thick) ; unused by thin
+  int L0, L1;              // level range (thin)
+  const int32_t* lptr;     // device level pointer (thin)
+  int slot_base, total_slots;
+};
+
+// Thick segment: grid-wide sync-free over positions [p0, p1).
+template <int G, int NU, int U, int NR, class Deps, class Body, class Fin>
+__global__ void __launch_bounds__(kRowsThreads) trsv_kernel(TrsvLaunch L, int t, int ld,
+                                                            const int32_t* __restrict__ order, Deps deps,
+                                                            double* __restrict__ x, Body body, Fin fin,
+                                                            double* __restrict__ partials,
+                                                            unsigned* __restrict__ counter,
+                                                            const int* __restrict__ gate, unsigned smax,
+                                                            long long* __restrict__ tstamp) {
+  if (gate != nullptr && *((volatile const int*)gate) == 0) return;
+  extern __shared__ double rsh[];
+  constexpr int GPW = 32 / G;
+  constexpr int NC = NU * U;
+  constexpr int NRR = NR > 0 ? NR : 1;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % G;
+  const int gi = lane / G;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double acc[NRR][NC];
+#pragma unroll
+  for (int r = 0; r < NRR; ++r)
+#pragma unroll
+    for (int i = 0; i < NC; ++i) acc[r][i] = 0.0;
+  for (int64_t pbase = L.p0 + gwarp * GPW; pbase < L.p1; pbase += nwarps * GPW)
+    trsv_row<G, NU, U, true>(pbase + gi, L.p1, t, ld, order, deps, x, body, smax, tstamp, gl, acc[0]);
+  if constexpr (NR > 0) {
+    block_reduce_cols<G, NU, U, NR, 0>(acc, t, partials + (size_t)(L.slot_base + blockIdx.x) * NR * t, rsh);
+    grid_finalize<NR, 0>(partials, counter, t, fin, rsh, L.total_slots);
+  }
+}
+
+// Single right-hand side: work items in level order.  A light item is a
+// 32-row chunk of one level (thread per row); a heavy item (bit 31 set) is
+// one row solved warp-per-row with the lanes over its dependencies (rows of
+// thin levels / rows with many children), then a shuffle reduction.
+constexpr uint32_t kHeavyBit = 0x80000000u;
+
+template <int NR, class Deps, class Body, class Fin>
+__global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int64_t npos,
+                                                             const uint32_t* __restrict__ items,
+                                                             const int32_t* __restrict__ order, Deps deps,
+                                                             double* __restrict__ x, Body body, Fin fin,
+                                                             double* __restrict__ partials,
+                                                             unsigned* __restrict__ counter,
+                                                             const int* __restrict__ gate, unsigned smax,
+                                                             long long* __restrict__ tstamp) {
+  if (gate != nullptr && *((volatile const int*)gate) == 0) return;
+  extern __shared__ double rsh[];
+  constexpr int NRR = NR > 0 ? NR : 1;
+  constexpr int HB = 8;  // deps per lane per heavy round (256 per warp)
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double acc[NRR][1];
+#pragma unroll
+  for (int r = 0; r < NRR; ++r) acc[r][0] = 0.0;
+  for (int64_t it = gwarp; it < nitems; it += nwarps) {
+    const uint32_t item = items[it];
+    if (!(item & kHeavyBit)) {
+      trsv_row<1, 1, 1, true>((int64_t)item + lane, npos, 1, 1, order, deps, x, body, smax, tstamp, 0, acc[0]);
+      continue;
+    }
+    const int32_t so = order[item & ~kHeavyBit];
+    const int64_t s = so;
+    const int cs = deps.count(s);
+    const int64_t b0 = deps.base(s);
+    double part = 0.0;
+    for (int e0 = 0; e0 < cs; e0 += 32 * HB) {
+      int32_t j[HB];
+      double w[HB], v[HB];
+#pragma unroll
+      for (int q = 0; q < HB; ++q) {
+        const int e = e0 + q * 32 + lane;
+        const bool on = e < cs;
+        j[q] = on ? deps.idx(b0 + e) : 0;
+        w[q] = on ? deps.w(b0 + e) : 0.0;
+        if (on) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
+        else v[q] = 0.0;
+      }
+      unsigned ns = 8;
+      for (;;) {
+        bool pend = false;
+#pragma unroll
+        for (int q = 0; q < HB; ++q) pend |= is_sentinel(v[q]);
+        if (!__any_sync(0xffffffffu, pend)) break;
+        if (smax) {
+          __nanosleep(ns);
+          ns = ns < smax ? ns * 2 : smax;
+        }
+#pragma unroll
+        for (int q = 0; q < HB; ++q)
+          if (is_sentinel(v[q])) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < HB; ++q) part += w[q] * v[q];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) {
+      const double xs = body.rhs(s, 0, acc[0][0]) - part;
+      body.out(s, 0, xs, acc[0][0]);
+      __stcg(x + s, sanitize(xs));
+      if (tstamp != nullptr) {
         long long g;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
         tstamp[s] = g;
@@ -331,8 +434,47 @@ __global__ void __launch_bounds__(kRowsThreads) trsv_kernel(int64_t npos, int t,
     }
   }
   if constexpr (NR > 0) {
-    block_reduce_cols<G, NU, U, NR, 0>(acc, t, partials + (size_t)blockIdx.x * NR * t, rsh);
-    grid_finalize<NR, 0>(partials, counter, t, fin, rsh);
+    block_reduce_cols<1, 1, 1, NR, 0>(acc, 1, partials + (size_t)blockIdx.x * NR, rsh);
+    grid_finalize<NR, 0>(partials, counter, 1, fin, rsh);
+  }
+}
+
+constexpr int kThinThreads = 1024;
+
+// Thin segment: ONE CTA walks levels [L0, L1) with a barrier per level (no
+// polling: every dependency is in an earlier level or an earlier segment).
+template <int G, int NU, int U, int NR, class Deps, class Body, class Fin>
+__global__ void __launch_bounds__(kThinThreads) trsv_thin_kernel(TrsvLaunch L, int t, int ld,
+                                                                 const int32_t* __restrict__ order, Deps deps,
+                                                                 double* __restrict__ x, Body body, Fin fin,
+                                                                 double* __restrict__ partials,
+                                                                 unsigned* __restrict__ counter,
+                                                                 const int* __restrict__ gate,
+                                                                 long long* __restrict__ tstamp) {
+  if (gate != nullptr && *((volatile const int*)gate) == 0) return;
+  extern __shared__ double rsh[];
+  constexpr int GPW = 32 / G;
+  constexpr int NC = NU * U;
+  constexpr int NRR = NR > 0 ? NR : 1;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % G;
+  const int gi = lane / G;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  double acc[NRR][NC];
+#pragma unroll
+  for (int r = 0; r < NRR; ++r)
+#pragma unroll
+    for (int i = 0; i < NC; ++i) acc[r][i] = 0.0;
+  for (int lv = L.L0; lv < L.L1; ++lv) {
+    const int64_t q0 = L.lptr[lv], q1 = L.lptr[lv + 1];
+    for (int64_t pbase = q0 + (int64_t)warp * GPW; pbase < q1; pbase += (int64_t)nwarps * GPW)
+      trsv_row<G, NU, U, false>(pbase + gi, q1, t, ld, order, deps, x, body, 0u, tstamp, gl, acc[0]);
+    __syncthreads();
+  }
+  if constexpr (NR > 0) {
+    block_reduce_cols<G, NU, U, NR, 0>(acc, t, partials + (size_t)L.slot_base * NR * t, rsh);
+    grid_finalize<NR, 0>(partials, counter, t, fin, rsh, L.total_slots);
   }
 }
 

@@ -24,18 +24,25 @@ L.vl_debug_set_tstamp.argtypes = [C.c_void_p, C.c_void_p]
 ts = torch.zeros(n, dtype=torch.int64, device="cuda")
 # levels in factor order
 nb = nbr
+TR = int(os.environ.get("KP_TR", "0"))
 lev = np.zeros(n, dtype=np.int64)
-for i in range(n):
-    row = nb[i][nb[i] >= 0]
-    if row.size:
-        lev[i] = lev[row].max() + 1
+if not TR:
+    for i in range(n):
+        row = nb[i][nb[i] >= 0]
+        if row.size:
+            lev[i] = lev[row].max() + 1
+else:  # heights (levels of the B^T solve)
+    for i in range(n - 1, -1, -1):
+        row = nb[i][nb[i] >= 0]
+        if row.size:
+            lev[row] = np.maximum(lev[row], lev[i] + 1)
 for t in [int(x) for x in os.environ.get("KP_TS", "1,50").split(",")]:
     X = torch.randn(n, t, dtype=torch.float64, device="cuda") / 20
     Y = torch.empty_like(X)
-    _lib.call("vl_sptrsv", f.ctx.h, f.h, 0, t, _lib.ptr(X), _lib.ptr(Y))
+    _lib.call("vl_sptrsv", f.ctx.h, f.h, TR, t, _lib.ptr(X), _lib.ptr(Y))
     torch.cuda.synchronize()
     L.vl_debug_set_tstamp(f.ctx.h, C.c_void_p(ts.data_ptr()))
-    _lib.call("vl_sptrsv", f.ctx.h, f.h, 0, t, _lib.ptr(X), _lib.ptr(Y))
+    _lib.call("vl_sptrsv", f.ctx.h, f.h, TR, t, _lib.ptr(X), _lib.ptr(Y))
     torch.cuda.synchronize()
     L.vl_debug_set_tstamp(f.ctx.h, None)
     tsf = np.empty(n, dtype=np.int64)
@@ -51,7 +58,10 @@ for t in [int(x) for x in os.environ.get("KP_TS", "1,50").split(",")]:
     for k in range(m):
         col = nb[:, k]
         ok = col >= 0
-        depmax[ok] = np.maximum(depmax[ok], tsf[col[ok]])
+        if not TR:
+            depmax[ok] = np.maximum(depmax[ok], tsf[col[ok]])
+        else:
+            np.maximum.at(depmax, col[ok], tsf[np.flatnonzero(ok)])
     hop = tsf - depmax
     print(f"t={t} total={tsf.max()/1e3:.1f}us levels={nl}")
     print("  hop latency us: p50 %.2f p90 %.2f p99 %.2f max %.2f" % tuple(np.percentile(hop[lev > 0], [50, 90, 99, 100]) / 1e3))
