@@ -162,6 +162,19 @@ int vl_grad_probe_pass(vl_ctx* ctx, const vl_factor* f, const double* W_dev, con
                        const double* V_dev, int64_t t, double* s_dev, double* cols4_host, const double* md3x_dev,
                        double* xicols2_host);
 
+/* Probe-sharded split of vl_grad_probe_pass for multi-GPU runs (the per-row
+ * control-variate weights need all t_glob probes):
+ *   mode 1: rowA = [sum_c U*V, sum_c (BV)^2] over the local t columns (n x 2,
+ *           device) + local STE partials cols4 (and xicols2);
+ *   -- caller allreduces rowA --
+ *   mode 2: rowB = [sum_c (H - hbar)(R - rbar), sum_c (R - rbar)^2];
+ *   -- caller allreduces rowB --
+ *   mode 3: s_out from rowA, rowB (elementwise). */
+int vl_grad_probe_pass_split(vl_ctx* ctx, const vl_factor* f, int mode, const double* W_dev, const double* d3_dev,
+                             const double* U_dev, const double* V_dev, int64_t t, int64_t t_glob, double* rowA_dev,
+                             double* rowB_dev, double* s_dev, double* cols4_host, const double* md3x_dev,
+                             double* xicols2_host);
+
 /* out4 = [b^T dQ_s2 b, tvec^T dQ_s2 b, b^T dQ_rho b, tvec^T dQ_rho b]
  * (vecchia.py:357-361 quad_dprecision; laplace.py:537-541) */
 int vl_grad_scalar_terms(vl_ctx* ctx, const vl_factor* f, const double* b_dev, const double* tvec_dev,

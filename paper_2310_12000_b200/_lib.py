@@ -116,3 +116,9 @@ _SIGS.update({
     "vl_prof_report": [c_void_p, C.c_char_p, c_int, P_int64],
 })
 EXPORTED = sorted(_SIGS)
+
+_SIGS.update({
+    "vl_grad_probe_pass_split": [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
+                                 c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+})
+EXPORTED = sorted(_SIGS)

@@ -489,6 +489,16 @@ int vl_grad_probe_pass(vl_ctx* h, const vl_factor* f, const double* W, const dou
   });
 }
 
+int vl_grad_probe_pass_split(vl_ctx* h, const vl_factor* f, int mode, const double* W, const double* d3,
+                             const double* U, const double* V, int64_t t, int64_t t_glob, double* rowA, double* rowB,
+                             double* s_out, double* cols4, const double* md3x, double* xicols2) {
+  return guard([&] {
+    if (mode != 3 && (t < 1 || t > 128)) fail(kECapacity, "probe shard width must be in [1, 128]");
+    grad_probe_pass_split(h->c, f->f, mode, W, d3, U, V, (int)t, (int)t, (int)t_glob, rowA, rowB, s_out, cols4, md3x,
+                          xicols2);
+  });
+}
+
 int vl_grad_scalar_terms(vl_ctx* h, const vl_factor* f, const double* b, const double* tvec, double* out4) {
   return guard([&] { grad_scalar_terms(h->c, f->f, b, tvec, out4); });
 }

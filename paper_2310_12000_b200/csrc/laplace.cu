@@ -540,6 +540,132 @@ struct GradProbeBody {
   }
 };
 
+// Probe-sharded variant (multi-GPU): the per-row control-variate statistics
+// need all t probes, so they are split into allreduce-able row sums.
+//   MODE 1: rowA = [sum_c H, sum_c R] (local columns) + STE column partials
+//   MODE 2: rowB = [sum_c (H - hbar)(R - rbar), sum_c (R - rbar)^2] with the
+//           global means hbar = rowA/t_glob (rowA already allreduced)
+template <int MODE, bool XI>
+struct GradSplitBody {
+  BView B;
+  const double* dval;
+  const double* U_;
+  const double* V_;
+  const double* D;
+  const double* dDs;
+  const double* dDr;
+  const double* W;
+  const double* md3x;
+  double* rowA;
+  double* rowB;
+  int tg;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    constexpr int NC = NU * U;
+    double BU[NC], BV[NC], dBU[NC], dBV[NC];
+    zero(BU); zero(BV); zero(dBU); zero(dBV);
+    const int cs = valid ? B.cnt[s] : 0;
+    const int64_t base = (valid ? s : 0) * B.m;
+    for (int e = 0; e < cs; ++e) {
+      const int32_t j = B.nbr[base + e];
+      const double w = B.val[base + e];
+      const double dw = (MODE == 1) ? dval[base + e] : 0.0;
+#pragma unroll
+      for (int k = 0; k < NU; ++k) {
+        const int c = U * (gl + G * k);
+        if (c < t) {
+          double uu[U], vv[U];
+          load_unit<U>(V_ + (int64_t)j * ld + c, vv);
+          if (MODE == 1) load_unit<U>(U_ + (int64_t)j * ld + c, uu);
+#pragma unroll
+          for (int i = 0; i < U; ++i) {
+            BV[U * k + i] += w * vv[i];
+            if (MODE == 1) {
+              BU[U * k + i] += w * uu[i];
+              dBU[U * k + i] += dw * uu[i];
+              dBV[U * k + i] += dw * vv[i];
+            }
+          }
+        }
+      }
+    }
+    double us[NC], vs[NC];
+    load_row<G, NU, U>(U_, ld, valid ? s : 0, gl, valid ? t : 0, us);
+    load_row<G, NU, U>(V_, ld, valid ? s : 0, gl, valid ? t : 0, vs);
+    double a = 0.0, b = 0.0;
+    double hm = 0.0, rm = 0.0;
+    if (MODE == 2 && valid) {
+      hm = rowA[2 * s] / tg;
+      rm = rowA[2 * s + 1] / tg;
+    }
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int c = vl::Cols<G, NU, U>::col(gl, i);
+      BU[i] += us[i];
+      BV[i] += vs[i];
+      if (valid && c < t) {
+        const double H = us[i] * vs[i], R = BV[i] * BV[i];
+        if (MODE == 1) {
+          a += H;
+          b += R;
+        } else {
+          a += (H - hm) * (R - rm);
+          b += (R - rm) * (R - rm);
+        }
+      }
+    }
+    a = gsum<G>(a);
+    b = gsum<G>(b);
+    if (!valid) return;
+    if (gl == 0) {
+      double* dst = (MODE == 1) ? rowA : rowB;
+      dst[2 * s] = a;
+      dst[2 * s + 1] = b;
+    }
+    if (MODE != 1) return;
+    const double Dinv = 1.0 / D[s], ws = W[s];
+    const double qs = dDs[s] * Dinv * Dinv;
+    const double qr = dDr[s] * Dinv * Dinv;
+    const double mx = XI ? md3x[s] : 0.0;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int c = vl::Cols<G, NU, U>::col(gl, i);
+      if (c >= t) continue;
+      acc[0][i] += -(BU[i] * qs * BV[i]);
+      acc[1][i] += -(qs * BV[i] * BV[i]);
+      acc[2][i] += (dBU[i] * BV[i] + BU[i] * dBV[i]) * Dinv - BU[i] * qr * BV[i];
+      acc[3][i] += 2.0 * dBV[i] * BV[i] * Dinv - qr * BV[i] * BV[i] + 2.0 * ws * dBV[i] * BV[i];
+      if constexpr (XI) {
+        acc[4][i] += mx * us[i] * vs[i];
+        acc[5][i] += mx * BV[i] * BV[i];
+      }
+    }
+  }
+};
+
+// MODE 3: s = 0.5 md3 (c/(W + 1/D) + (sumH - c sumR)/t), c = cov/var (ddof 1)
+struct GradSplitFinishBody {
+  const double* rowA;
+  const double* rowB;
+  const double* D;
+  const double* W;
+  const double* d3;
+  double* s_out;
+  int tg;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int, int, double (&)[NR][NU * U]) const {
+    if (!valid) return;
+    double cw = 0.0;
+    if (tg >= 2) {
+      const double vr = rowB[2 * s + 1] / (tg - 1), cv = rowB[2 * s] / (tg - 1);
+      cw = (vr >= 1e-300) ? cv / vr : 0.0;
+    }
+    const double exact = cw / (W[s] + 1.0 / D[s]);
+    s_out[s] = 0.5 * ((-d3[s]) * (exact + (rowA[2 * s] - cw * rowA[2 * s + 1]) / tg));
+  }
+};
+
 struct ScalarTermsBody {
   BView B;
   const double* dval;
@@ -639,6 +765,54 @@ void grad_probe_pass(Ctx& C, const Factor& F, const double* W, const double* d3,
   });
   read_sums(C, sums, cols_host, 4 * t);
   if (xi_md3 != nullptr) read_sums(C, sums + 4 * t, xi_cols_host, 2 * t);
+}
+
+void grad_probe_pass_split(Ctx& C, const Factor& F, int mode, const double* W, const double* d3, const double* U,
+                           const double* V, int t, int ld, int t_glob, double* rowA, double* rowB, double* s_out,
+                           double* cols_host, const double* xi_md3, double* xi_cols_host) {
+  if (!F.has_grad) fail(kEConfig, "factor was built without gradient");
+  const Pattern& P = *F.pat;
+  BView B = bview(F, false);
+  double* sums = C.dev_scalars.as<double>();
+  ProfScope ps(C, "grad_pass_split", 0.0);
+  if (mode == 3) {
+    launch_rows<1, 1, 1, 0, 0>(C, P.n, 1,
+                               GradSplitFinishBody{rowA, rowB, F.D.as<double>(), W, d3, s_out, t_glob}, Fin0<0>{});
+    return;
+  }
+  if (t < 1 || 6 * t > 8192) fail(kECapacity, "invalid probe shard width");
+  dispatch_cols(t, ld, [&](auto g, auto nu, auto uu) {
+    constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U_ = decltype(uu)::value;
+    auto common = [&](auto body_tag) {};
+    (void)common;
+    if (mode == 1) {
+      if (xi_md3 == nullptr) {
+        launch_rows<G, NU, U_, 4, 0>(C, P.n, t,
+                                     GradSplitBody<1, false>{B, F.dval.as<double>(), U, V, F.D.as<double>(),
+                                                             F.dD_sig.as<double>(), F.dD_rho.as<double>(), W,
+                                                             nullptr, rowA, rowB, t_glob, ld},
+                                     CopySums<4>{sums});
+      } else {
+        launch_rows<G, NU, U_, 6, 0>(C, P.n, t,
+                                     GradSplitBody<1, true>{B, F.dval.as<double>(), U, V, F.D.as<double>(),
+                                                            F.dD_sig.as<double>(), F.dD_rho.as<double>(), W, xi_md3,
+                                                            rowA, rowB, t_glob, ld},
+                                     CopySums<6>{sums});
+      }
+    } else if (mode == 2) {
+      launch_rows<G, NU, U_, 0, 0>(C, P.n, t,
+                                   GradSplitBody<2, false>{B, F.dval.as<double>(), U, V, F.D.as<double>(),
+                                                           F.dD_sig.as<double>(), F.dD_rho.as<double>(), W, nullptr,
+                                                           rowA, rowB, t_glob, ld},
+                                   Fin0<0>{});
+    } else {
+      fail(kEConfig, "unknown split mode");
+    }
+  });
+  if (mode == 1) {
+    read_sums(C, sums, cols_host, 4 * t);
+    if (xi_md3 != nullptr) read_sums(C, sums + 4 * t, xi_cols_host, 2 * t);
+  }
 }
 
 void grad_scalar_terms(Ctx& C, const Factor& F, const double* b, const double* tvec, double* out_host) {

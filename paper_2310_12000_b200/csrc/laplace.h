@@ -54,6 +54,12 @@ void factor_sums(Ctx& C, const Factor& F, const double* W, double* out_host);
 void grad_probe_pass(Ctx& C, const Factor& F, const double* W, const double* d3, const double* U, const double* V,
                      int t, int ld, double* s_out, double* cols_host, const double* xi_md3, double* xi_cols_host);
 
+// Probe-sharded split of grad_probe_pass (modes 1, 2, 3; see laplace.cu).
+// rowA/rowB: n x 2 device; between modes the caller allreduces them.
+void grad_probe_pass_split(Ctx& C, const Factor& F, int mode, const double* W, const double* d3, const double* U,
+                           const double* V, int t, int ld, int t_glob, double* rowA, double* rowB, double* s_out,
+                           double* cols_host, const double* xi_md3, double* xi_cols_host);
+
 // Scalar gradient terms with b and tvec (host out, 4 values):
 // [quad_sigma2(b), tvec.dQ_sigma2 b, quad_rho(b), tvec.dQ_rho b]
 void grad_scalar_terms(Ctx& C, const Factor& F, const double* b, const double* tvec, double* out_host);

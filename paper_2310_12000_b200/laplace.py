@@ -336,7 +336,7 @@ def gradient(state, factor, lik, X, cfg, probes=None, P=None, comm=None):
     s = dev.empty(ctx, n, 1)
     cols = np.zeros((4, t))
     xicols = np.zeros((2, t))
-    if comm is not None and comm.world > 1:
+    if comm is not None and (comm.world > 1 or getattr(comm, "force_split", False)):
         s, cols, xicols = comm.grad_probe_pass(factor, state, probes, md3x)
     else:
         _lib.call("vl_grad_probe_pass", ctx.h, factor.h, _lib.ptr(dv["W"]), _lib.ptr(dv["d3"]),

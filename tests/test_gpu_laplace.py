@@ -85,3 +85,34 @@ def test_probe_solves_match_oracle_replay(vg):
             continue  # stopping-rule flip under rounding: compared elsewhere
         assert _rel(U[:, i], res.u) <= 1e-10
         assert _rel(probes.tridiags[i].diag, res.diag) <= 1e-10
+
+
+def test_sharded_gradient_path_matches_fused(vg):
+    """The multi-GPU split of the gradient pass (row-stat allreduce rounds,
+    probe-ordered gathers) run as a 1-rank NCCL group equals the fused pass."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_2310_12000_b200.distributed import ProbeComm
+    g = load("logit_vadu_n1500")
+    f, lik, cfg, y, F, X = _setup(vg, g)
+    st = vg.find_mode(f, lik, y, F, cfg)
+    probes, P = vg.make_probes(f, st, cfg)
+    vg.neg_marginal_loglik(st, f, cfg, probes=probes, P=P)
+    ref = vg.gradient(st, f, lik, X, cfg, probes=probes, P=P)
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        comm = ProbeComm(force_split=True)
+        got = vg.gradient(st, f, lik, X, cfg, probes=probes, P=P, comm=comm)
+    finally:
+        dist.destroy_process_group()
+    np.testing.assert_allclose(got["dtheta"], ref["dtheta"], rtol=1e-10, atol=1e-12)
