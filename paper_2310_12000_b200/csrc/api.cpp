@@ -150,7 +150,7 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
   upload(C, P.bwd_lptr, P.bwd_level_ptr);
   // single-RHS work items: 32-row chunks, expanded to per-row (warp-per-row)
   // items on thin levels and for chunks holding a row with many dependencies
-  int heavy_rows = 64, heavy_deps = 40;
+  int heavy_rows = 64, heavy_deps = 64;
   if (const char* e = std::getenv("VL_HEAVY_LEVEL_ROWS")) heavy_rows = std::atoi(e);
   if (const char* e = std::getenv("VL_HEAVY_DEPS")) heavy_deps = std::atoi(e);
   auto items = [&](const std::vector<int32_t>& order, const std::vector<int32_t>& lptr, bool fwd_dir) {
@@ -182,6 +182,20 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
   P.bwd_nitems = (int64_t)bi.size();
   upload(C, P.fwd_items, fi);
   upload(C, P.bwd_items, bi);
+  // dense head block + backward schedule without it
+  upload(C, P.head_rows, P.head_rows_h);
+  upload(C, P.head_pos, P.head_pos_h);
+  upload(C, P.head_nbr, P.head_nbr_h);
+  upload(C, P.bwdnh_order, P.bwdnh_order_h);
+  upload(C, P.bwdnh_lptr, P.bwdnh_level_ptr);
+  P.bwdnh_len = (int64_t)P.bwdnh_order_h.size();
+  P.fwd_items_head_end = 0;
+  if (P.head_L > 0)
+    for (uint32_t it : fi)
+      if ((int64_t)(it & 0x7fffffffu) < P.fwd_level_ptr[P.head_L]) ++P.fwd_items_head_end;
+  auto bni = items(P.bwdnh_order_h, P.bwdnh_level_ptr, false);
+  P.bwdnh_nitems = (int64_t)bni.size();
+  upload(C, P.bwdnh_items, bni);
   VL_CUDA(cudaStreamSynchronize(C.stream));
 }
 
@@ -212,6 +226,7 @@ int vl_ctx_create(int device, void* stream, vl_ctx** out) {
     if (const char* e = std::getenv("VL_SPIN_MAX_NS")) C.spin_max_ns = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("VL_THIN_PASSES")) C.thin_passes = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("VL_MIN_THICK")) C.min_thick_levels = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("VL_USE_HEAD")) C.use_head = std::atoi(e) != 0;
     try {
       // NULL selects the legacy default stream (same as torch's default stream)
       C.stream = (cudaStream_t)stream;
@@ -272,6 +287,7 @@ int vl_pattern_create(vl_ctx* h, int64_t n, int d, int m, const double* xy, cons
     p->p.d = d;
     p->p.m = m;
     p->p.order_kind = order_kind;
+    if (const char* e = std::getenv("VL_HEAD_MAX")) p->p.head_max = std::max(0, std::atoi(e));
     try {
       std::vector<int32_t> empty;
       const int32_t* nb = nbr;

@@ -65,6 +65,9 @@ struct Ctx {
   // thin solve levels: <= thin_passes * (1024 / G) rows run on a single CTA
   int thin_passes = 0;
   int min_thick_levels = 4;
+  // dense head block of the solves (see head.cuh) and its scratch
+  bool use_head = true;
+  DevBuf head_Y, head_Xh;
   // debug: per-row completion timestamps of the next triangular solves (n entries)
   long long* debug_tstamp = nullptr;
   // deterministic reduction scratch: per-block partials + ticket counters
@@ -102,6 +105,18 @@ struct Pattern {
   DevBuf fwd_lptr, bwd_lptr;  // device copies of the padded level pointers
   DevBuf fwd_items, bwd_items;  // single-RHS work items (light 32-row chunks / heavy rows)
   int64_t fwd_nitems = 0, bwd_nitems = 0;
+  // dense head block (see pattern.cpp): rows of forward levels < head_L
+  int64_t head_max = 3072;
+  int head_L = 0;
+  int64_t head_H = 0;
+  std::vector<int32_t> head_rows_h, head_pos_h, head_nbr_h;
+  std::vector<int32_t> bwdnh_order_h, bwdnh_level_ptr;
+  DevBuf head_rows;   // H      storage row of head position h (level order)
+  DevBuf head_pos;    // n      head position of a storage row or -1
+  DevBuf head_nbr;    // H*m    head positions of the row's neighbours
+  DevBuf bwdnh_order, bwdnh_lptr, bwdnh_items;  // backward schedule without the head rows
+  int64_t bwdnh_len = 0, bwdnh_nitems = 0;
+  int64_t fwd_items_head_end = 0;  // forward items covering the head levels
   DevBuf tptr;      // n+1  int32 children CSR (= CSR of B^T) in storage order
   DevBuf tidx;      // nnz  int32 child storage row
   DevBuf tmap;      // nnz  int32 ELL slot (child*m + k) holding B[child, s]
@@ -119,6 +134,8 @@ struct Factor {
   DevBuf dD_rho;  // n
   DevBuf dD_sig;  // n    d D / d sigma2 = D / sigma2
   DevBuf err;     // 4 ints: [code, row(factor idx) ...]
+  DevBuf headX;   // H*H  dense B_HH^-1, column-major (head order), lower triangular
+  DevBuf headXr;  // H*H  the same, row-major
 };
 
 }  // namespace vl

@@ -240,6 +240,74 @@ __global__ void gather_values_kernel(int64_t nnz, const int32_t* __restrict__ ma
     dst[p] = src[map[p]];
 }
 
+// X = B_HH^-1, one warp per column (see head.cuh).  Column c is zero above
+// row c (head order is topological), so substitution starts at row c.
+__global__ void __launch_bounds__(128) head_inverse_kernel(int H, int m, const int32_t* __restrict__ head_rows,
+                                                           const int32_t* __restrict__ head_nbr,
+                                                           const int32_t* __restrict__ cnt,
+                                                           const double* __restrict__ val, double* __restrict__ X) {
+  extern __shared__ double xc[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* xcol = xc + (size_t)w * H;
+  for (int c = blockIdx.x * 4 + w; c < H; c += gridDim.x * 4) {
+    for (int r = c; r < H; ++r) {
+      const int64_t s = head_rows[r];
+      const int cs = cnt[s];
+      double part = 0.0;
+      if (lane < cs) {
+        const int q = head_nbr[(int64_t)r * m + lane];
+        if (q >= c) part = val[s * m + lane] * xcol[q];
+      }
+      part = warp_sum(part);
+      const double xr = (r == c ? 1.0 : 0.0) - part;
+      if (lane == 0) {
+        xcol[r] = xr;
+        X[(size_t)c * H + r] = xr;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void transpose_kernel(int H, const double* __restrict__ A, double* __restrict__ B) {
+  __shared__ double tile[32][33];
+  const int x = blockIdx.x * 32 + threadIdx.x;
+  for (int k = 0; k < 32; k += blockDim.y) {
+    const int y = blockIdx.y * 32 + threadIdx.y + k;
+    tile[threadIdx.y + k][threadIdx.x] = (x < H && y < H) ? A[(size_t)y * H + x] : 0.0;
+  }
+  __syncthreads();
+  const int x2 = blockIdx.y * 32 + threadIdx.x;
+  for (int k = 0; k < 32; k += blockDim.y) {
+    const int y2 = blockIdx.x * 32 + threadIdx.y + k;
+    if (x2 < H && y2 < H) B[(size_t)y2 * H + x2] = tile[threadIdx.x][threadIdx.y + k];
+  }
+}
+
+void factor_head_inverse(Ctx& C, Factor& F) {
+  const Pattern& P = *F.pat;
+  if (P.head_H <= 0 || P.m > 32) return;
+  const int H = (int)P.head_H;
+  F.headX.alloc(sizeof(double) * (size_t)H * H);
+  const size_t smem = sizeof(double) * 4 * (size_t)H;
+  VL_CUDA(cudaFuncSetAttribute(head_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  VL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, head_inverse_kernel, 128, smem));
+  const int blocks = std::max(1, std::min((H + 3) / 4, std::max(occ, 1) * C.num_sms));
+  ProfScope ps(C, "factor_head_inverse", 0.0);
+  C.prof.launches++;
+  cudaEvent_t ev = C.prof.on ? prof_begin(C) : nullptr;
+  head_inverse_kernel<<<blocks, 128, smem, C.stream>>>(H, P.m, P.head_rows.as<int32_t>(), P.head_nbr.as<int32_t>(),
+                                                       P.cnt.as<int32_t>(), F.val.as<double>(), F.headX.as<double>());
+  VL_LAUNCH_CHECK();
+  // row-major copy for the forward single-column GEMV (headX is column-major)
+  F.headXr.alloc(sizeof(double) * (size_t)H * H);
+  transpose_kernel<<<dim3((H + 31) / 32, (H + 31) / 32), dim3(32, 8), 0, C.stream>>>(H, F.headX.as<double>(),
+                                                                                     F.headXr.as<double>());
+  VL_LAUNCH_CHECK();
+  if (ev) prof_end(C, ev);
+}
+
 void factor_refresh_transpose(Ctx& C, Factor& F) {
   const Pattern& P = *F.pat;
   if (P.nnz_off > 0) {
@@ -248,6 +316,7 @@ void factor_refresh_transpose(Ctx& C, Factor& F) {
                                                        F.valT.as<double>());
     VL_LAUNCH_CHECK();
   }
+  factor_head_inverse(C, F);  // dense B_HH^-1 for the solves' head block
 }
 
 template <int Q, int DIM>

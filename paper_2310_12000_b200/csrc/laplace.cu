@@ -396,7 +396,7 @@ void probes_vadu(Ctx& C, const Factor& F, const double* W, int t, int ld, const 
       launch_rows<G_, NU, U, 0, 0>(C, n, t, ProbeZBody{B, G, sd.as<double>(), Z, ld}, Fin0<0>{});
     }
     ProfScope ps(C, "probe_V", bapply_bytes(P, t, 1) + 8.0 * n * t);
-    launch_trsv<G_, NU, U, 1>(C, P, true, t, ld, dfw, V,
+    launch_trsv<G_, NU, U, 1>(C, F, true, t, ld, dfw, V,
                               PsolveRhs{G, sd.as<double>(), Z, ld}, CopySums<1>{sums});
   });
   read_sums(C, sums, w_host, t);

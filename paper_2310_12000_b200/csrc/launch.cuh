@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "context.h"
+#include "head.cuh"
 #include "rows.cuh"
 
 namespace vl {
@@ -88,90 +89,172 @@ struct Seg {
 };
 std::vector<Seg> solve_segments(const std::vector<int32_t>& lptr, int thin_rows, int min_thick_levels);
 
-// Triangular solve over the fwd (B) or bwd (B^T) schedule.  x (n x ld) is
-// overwritten: it is first filled with the "not ready" sentinel; thin
-// segments run on one CTA, thick segments grid-wide (sync-free).  Fused
-// column reductions finalise once over all segments' partial slots.
+// Triangular solve over the fwd (B) or bwd (B^T) schedule of factor F.
+// x (n x ld) is overwritten: it is first filled with the "not ready"
+// sentinel.  Phases (one stream, one partial-slot space, one finalisation):
+//   forward : [head rhs] [X . rhs_H] [head out] [sync-free rest]
+//   backward: [sync-free rest] [head rhs - B_RH^T x_R] [X^T . ] [head out]
+// The sync-free part runs as light/heavy work items (t == 1) or as
+// thin (single-CTA) / thick (grid) level segments (t > 1).
 template <int G, int NU, int U, int NR, class Deps, class Body, class Fin>
-void launch_trsv(Ctx& C, const Pattern& P, bool fwd, int t, int ld, const Deps& deps, double* x, const Body& body,
+void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& deps, double* x, const Body& body,
                  const Fin& fin, const int* gate = nullptr) {
+  const Pattern& P = *F.pat;
   const int64_t n = P.n;
-  const int32_t* order = fwd ? P.fwd_order.as<int32_t>() : P.bwd_order.as<int32_t>();
-  if constexpr (G == 1 && NU == 1 && U == 1) {
-    if (C.thin_passes == 0) {
-      // single right-hand side: light/heavy work items, one sync-free launch
-      auto k1 = trsv1_kernel<NR, Deps, Body, Fin>;
-      const size_t smem1 = red_smem_bytes<1, 1, 1, NR>(kRowsThreads, 1);
-      int grid = coop_grid(C, (const void*)k1, smem1);
-      grid = std::min(grid, C.num_sms * C.trsv_blocks_per_sm);
-      const int64_t nitems = fwd ? P.fwd_nitems : P.bwd_nitems;
-      const int64_t npos = fwd ? P.fwd_len : P.bwd_len;
-      const uint32_t* items = fwd ? P.fwd_items.as<uint32_t>() : P.bwd_items.as<uint32_t>();
-      C.prof.launches += 2;
-      cudaEvent_t ev = (C.prof.on && C.prof.tag) ? prof_begin(C) : nullptr;
-      VL_CUDA(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)n * ld, C.stream));
-      double* partials = C.red_partial.as<double>();
-      unsigned* counter = next_counter(C);
-      unsigned smax = (unsigned)C.spin_max_ns;
-      long long* tstamp = C.debug_tstamp;
-      void* args[] = {(void*)&nitems, (void*)&npos,     (void*)&items,   (void*)&order, (void*)&deps,
-                      (void*)&x,      (void*)&body,     (void*)&fin,     (void*)&partials, (void*)&counter,
-                      (void*)&gate,   (void*)&smax,     (void*)&tstamp};
-      VL_CUDA(cudaLaunchCooperativeKernel((const void*)k1, dim3(grid), dim3(kRowsThreads), args, smem1, C.stream));
-      if (ev) prof_end(C, ev);
-      return;
-    }
+  const bool head = C.use_head && P.head_H > 0 && F.headX.p != nullptr;
+  const int H = head ? (int)P.head_H : 0;
+  // ---- main (non-head) schedule ----
+  const int32_t* order;
+  const int32_t* lptr_d;
+  const std::vector<int32_t>* lptr;
+  int L0;
+  const uint32_t* items;
+  int64_t nitems, npos;
+  if (fwd) {
+    order = P.fwd_order.as<int32_t>();
+    lptr_d = P.fwd_lptr.as<int32_t>();
+    lptr = &P.fwd_level_ptr;
+    L0 = head ? P.head_L : 0;
+    items = P.fwd_items.as<uint32_t>() + (head ? P.fwd_items_head_end : 0);
+    nitems = P.fwd_nitems - (head ? P.fwd_items_head_end : 0);
+    npos = P.fwd_len;
+  } else if (head) {
+    order = P.bwdnh_order.as<int32_t>();
+    lptr_d = P.bwdnh_lptr.as<int32_t>();
+    lptr = &P.bwdnh_level_ptr;
+    L0 = 0;
+    items = P.bwdnh_items.as<uint32_t>();
+    nitems = P.bwdnh_nitems;
+    npos = P.bwdnh_len;
+  } else {
+    order = P.bwd_order.as<int32_t>();
+    lptr_d = P.bwd_lptr.as<int32_t>();
+    lptr = &P.bwd_level_ptr;
+    L0 = 0;
+    items = P.bwd_items.as<uint32_t>();
+    nitems = P.bwd_nitems;
+    npos = P.bwd_len;
   }
-  const int32_t* lptr_d = fwd ? P.fwd_lptr.as<int32_t>() : P.bwd_lptr.as<int32_t>();
-  const std::vector<int32_t>& lptr = fwd ? P.fwd_level_ptr : P.bwd_level_ptr;
+  const bool single = (G == 1 && NU == 1 && U == 1) && C.thin_passes == 0;
+  // launch geometry and slot counts
+  auto k1 = trsv1_kernel<NR, Deps, Body, Fin>;
   auto kern = trsv_kernel<G, NU, U, NR, Deps, Body, Fin>;
   auto tkern = trsv_thin_kernel<G, NU, U, NR, Deps, Body, Fin>;
+  const size_t smem1 = red_smem_bytes<1, 1, 1, NR>(kRowsThreads, 1);
   const size_t smem = red_smem_bytes<G, NU, U, NR>(kRowsThreads, t);
   const size_t tsmem = red_smem_bytes<G, NU, U, NR>(kThinThreads, t);
-  const int thin_rows = C.thin_passes * (kThinThreads / G);
-  std::vector<Seg> segs = solve_segments(lptr, thin_rows, C.min_thick_levels);
-  int gcap = coop_grid(C, (const void*)kern, smem);
-  gcap = std::min(gcap, C.num_sms * C.trsv_blocks_per_sm);
-  std::vector<int> grids(segs.size(), 1);
-  int total = 0;
-  for (size_t i = 0; i < segs.size(); ++i) {
-    if (!segs[i].thin) {
-      const int64_t npos = (int64_t)lptr[segs[i].L1] - lptr[segs[i].L0];
-      const int64_t need = (npos * G + kRowsThreads - 1) / kRowsThreads;
-      grids[i] = (int)std::max<int64_t>(1, std::min<int64_t>(need, gcap));
+  std::vector<Seg> segs;
+  std::vector<int> grids;
+  int main_slots = 0;
+  int grid1 = 0;
+  if (single) {
+    grid1 = std::min(coop_grid(C, (const void*)k1, smem1), C.num_sms * C.trsv_blocks_per_sm);
+    main_slots = grid1;
+  } else {
+    std::vector<int32_t> sub(lptr->begin() + L0, lptr->end());
+    segs = solve_segments(sub, C.thin_passes * (kThinThreads / G), C.min_thick_levels);
+    int gcap = std::min(coop_grid(C, (const void*)kern, smem), C.num_sms * C.trsv_blocks_per_sm);
+    for (auto& sg : segs) {
+      sg.L0 += L0;
+      sg.L1 += L0;
+      int gsz = 1;
+      if (!sg.thin) {
+        const int64_t np = (int64_t)(*lptr)[sg.L1] - (*lptr)[sg.L0];
+        gsz = (int)std::max<int64_t>(1, std::min<int64_t>((np * G + kRowsThreads - 1) / kRowsThreads, gcap));
+      }
+      grids.push_back(gsz);
+      main_slots += gsz;
     }
-    total += grids[i];
   }
-  C.prof.launches += 1 + (long long)segs.size();
+  // head kernels: rows per group (warp per row for the single-column backward gather)
+  const int hlanes = (t == 1 && !fwd) ? 32 : G;
+  const int hgrid = head ? std::max(1, std::min(4 * C.num_sms, (int)((H * hlanes + kRowsThreads - 1) / kRowsThreads))) : 0;
+  const int total = main_slots + 2 * hgrid;
+  C.prof.launches += 1 + (single ? 1 : (long long)segs.size()) + (head ? 3 : 0);
   cudaEvent_t ev = (C.prof.on && C.prof.tag) ? prof_begin(C) : nullptr;
   VL_CUDA(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)n * ld, C.stream));
   double* partials = C.red_partial.as<double>();
   unsigned* counter = next_counter(C);
   unsigned smax = (unsigned)C.spin_max_ns;
   long long* tstamp = C.debug_tstamp;
-  int slot = 0;
-  for (size_t i = 0; i < segs.size(); ++i) {
-    TrsvLaunch L;
-    L.L0 = segs[i].L0;
-    L.L1 = segs[i].L1;
-    L.p0 = lptr[segs[i].L0];
-    L.p1 = lptr[segs[i].L1];
-    L.lptr = lptr_d;
-    L.slot_base = slot;
-    L.total_slots = total;
-    slot += grids[i];
-    if (segs[i].thin) {
-      if (tsmem > 48 * 1024) VL_CUDA(cudaFuncSetAttribute(tkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
-      tkern<<<1, kThinThreads, tsmem, C.stream>>>(L, t, ld, order, deps, x, body, fin, partials, counter, gate,
-                                                  tstamp);
-      VL_LAUNCH_CHECK();
+  double *Y = nullptr, *Xh = nullptr;
+  const int ksplit = (t == 1) ? 1 : std::max(1, std::min(16, H / 256));
+  if (head) {
+    C.head_Y.alloc(sizeof(double) * (size_t)H * t);
+    C.head_Xh.alloc(sizeof(double) * (size_t)H * t * ksplit);
+    Y = C.head_Y.as<double>();
+    Xh = C.head_Xh.as<double>();
+  }
+  const int32_t* hrows = P.head_rows.as<int32_t>();
+  auto run_head = [&](int slot_rhs, int slot_out) {
+    const size_t hsm = red_smem_bytes<G, NU, U, NR>(kRowsThreads, t);
+    if (fwd)
+      head_rhs_kernel<G, NU, U, NR, false, Body, Fin><<<hgrid, kRowsThreads, hsm, C.stream>>>(
+          H, t, ld, hrows, P.head_pos.as<int32_t>(), P.tptr.as<int32_t>(), P.tidx.as<int32_t>(),
+          F.valT.as<double>(), x, Y, body, fin, partials, counter, slot_rhs, total, gate);
+    else
+      head_rhs_kernel<G, NU, U, NR, true, Body, Fin><<<hgrid, kRowsThreads, hsm, C.stream>>>(
+          H, t, ld, hrows, P.head_pos.as<int32_t>(), P.tptr.as<int32_t>(), P.tidx.as<int32_t>(),
+          F.valT.as<double>(), x, Y, body, fin, partials, counter, slot_rhs, total, gate);
+    VL_LAUNCH_CHECK();
+    if (t == 1) {
+      const int gb = (H * 32 + 255) / 256;
+      if (fwd) head_gemv_kernel<false><<<gb, 256, 0, C.stream>>>(H, F.headXr.as<double>(), Y, Xh, gate);
+      else head_gemv_kernel<true><<<gb, 256, 0, C.stream>>>(H, F.headX.as<double>(), Y, Xh, gate);
     } else {
-      void* args[] = {(void*)&L,     (void*)&t,       (void*)&ld,       (void*)&order,   (void*)&deps,
-                      (void*)&x,     (void*)&body,    (void*)&fin,      (void*)&partials, (void*)&counter,
-                      (void*)&gate,  (void*)&smax,    (void*)&tstamp};
-      VL_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grids[i]), dim3(kRowsThreads), args, smem,
-                                          C.stream));
+      const size_t asm_ = sizeof(double) * 32 * (size_t)t;
+      const dim3 ga((H + 31) / 32, ksplit);
+      if (fwd) head_apply_kernel<false><<<ga, 256, asm_, C.stream>>>(H, t, F.headX.as<double>(), Y, Xh, gate);
+      else head_apply_kernel<true><<<ga, 256, asm_, C.stream>>>(H, t, F.headX.as<double>(), Y, Xh, gate);
     }
+    VL_LAUNCH_CHECK();
+    head_out_kernel<G, NU, U, NR, Body, Fin><<<hgrid, kRowsThreads, hsm, C.stream>>>(
+        H, t, ld, hrows, Xh, ksplit, x, body, fin, partials, counter, slot_out, total, gate);
+    VL_LAUNCH_CHECK();
+  };
+  auto run_main = [&](int slot0) {
+    if (single) {
+      int sb = slot0;
+      void* args[] = {(void*)&nitems, (void*)&npos,  (void*)&items,    (void*)&order,  (void*)&deps,
+                      (void*)&x,      (void*)&body,  (void*)&fin,      (void*)&partials, (void*)&counter,
+                      (void*)&gate,   (void*)&smax,  (void*)&tstamp,   (void*)&sb,     (void*)&total};
+      if (nitems > 0)
+        VL_CUDA(cudaLaunchCooperativeKernel((const void*)k1, dim3(grid1), dim3(kRowsThreads), args, smem1,
+                                            C.stream));
+      return;
+    }
+    int slot = slot0;
+    for (size_t i = 0; i < segs.size(); ++i) {
+      TrsvLaunch Lc;
+      Lc.L0 = segs[i].L0;
+      Lc.L1 = segs[i].L1;
+      Lc.p0 = (*lptr)[segs[i].L0];
+      Lc.p1 = (*lptr)[segs[i].L1];
+      Lc.lptr = lptr_d;
+      Lc.slot_base = slot;
+      Lc.total_slots = total;
+      slot += grids[i];
+      if (segs[i].thin) {
+        if (tsmem > 48 * 1024)
+          VL_CUDA(cudaFuncSetAttribute(tkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
+        tkern<<<1, kThinThreads, tsmem, C.stream>>>(Lc, t, ld, order, deps, x, body, fin, partials, counter, gate,
+                                                    tstamp);
+        VL_LAUNCH_CHECK();
+      } else {
+        void* args[] = {(void*)&Lc,   (void*)&t,    (void*)&ld,       (void*)&order,   (void*)&deps,
+                        (void*)&x,    (void*)&body, (void*)&fin,      (void*)&partials, (void*)&counter,
+                        (void*)&gate, (void*)&smax, (void*)&tstamp};
+        VL_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grids[i]), dim3(kRowsThreads), args, smem,
+                                            C.stream));
+      }
+    }
+  };
+  if (fwd) {
+    if (head) run_head(main_slots, main_slots + hgrid);
+    run_main(0);
+  } else {
+    run_main(0);
+    if (head) run_head(main_slots, main_slots + hgrid);
   }
   if (ev) prof_end(C, ev);
 }

@@ -140,11 +140,11 @@ void op_trsv(Ctx& C, const Factor& F, bool transpose, int t, int ld, const doubl
     constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(u)::value;
     if (!transpose) {
       DepsEll deps{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
-      launch_trsv<G, NU, U, 0>(C, P, true, t, ld, deps, x, TrsvPlain{b, ld},
+      launch_trsv<G, NU, U, 0>(C, F,true, t, ld, deps, x, TrsvPlain{b, ld},
                                Fin0<0>{});
     } else {
       DepsCsr deps{P.tptr.as<int32_t>(), P.tidx.as<int32_t>(), F.valT.as<double>()};
-      launch_trsv<G, NU, U, 0>(C, P, false, t, ld, deps, x, TrsvPlain{b, ld},
+      launch_trsv<G, NU, U, 0>(C, F,false, t, ld, deps, x, TrsvPlain{b, ld},
                                Fin0<0>{});
     }
   });

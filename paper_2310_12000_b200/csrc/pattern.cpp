@@ -356,6 +356,50 @@ void pattern_build_host(Pattern& P, const double* xy, const int32_t* nbr, std::v
     }
   for (int64_t s = 0; s < n; ++s) maxc = std::max(maxc, tptr[s + 1] - tptr[s]);
   P.max_children = maxc;
+
+  // ---- dense head block -----------------------------------------------------
+  // Rows of forward levels < Lh form a closed block (their neighbours have
+  // lower levels) and no row outside it has a child inside it.  Its inverse
+  // X = B_HH^-1 (dense, recomputed per factor) replaces Lh dependency hops in
+  // both solves: forward x_H = X y_H first; backward x_H = X^T (y_H - B_RH^T x_R)
+  // last.  Lh is the largest prefix with at most head_max rows.
+  std::vector<int64_t> lsize(nlev, 0);
+  for (int64_t i = 0; i < n; ++i) lsize[lev[i]]++;
+  int Lh = 0;
+  int64_t H = 0;
+  while (Lh < nlev && H + lsize[Lh] <= P.head_max) H += lsize[Lh++];
+  if (Lh < 8 || Lh >= nlev) { Lh = 0; H = 0; }
+  P.head_L = Lh;
+  P.head_H = H;
+  P.head_rows_h.clear();
+  P.head_pos_h.assign(n, -1);
+  for (int32_t p = P.fwd_level_ptr[0]; p < (Lh ? P.fwd_level_ptr[Lh] : 0); ++p) {
+    const int32_t s = fwd[p];
+    if (s < 0) continue;
+    P.head_pos_h[s] = (int32_t)P.head_rows_h.size();
+    P.head_rows_h.push_back(s);
+  }
+  P.head_nbr_h.assign((size_t)std::max<int64_t>(H, 1) * std::max(m, 1), -1);
+  for (int64_t h = 0; h < H; ++h) {
+    const int32_t s = P.head_rows_h[h];
+    for (int k = 0; k < cnt[s]; ++k) {
+      const int32_t hp = P.head_pos_h[ell[s * m + k]];
+      if (hp < 0) fail(kEInternal, "head block is not closed");
+      P.head_nbr_h[h * m + k] = hp;
+    }
+  }
+  // backward schedule restricted to the rows outside the head (by height)
+  {
+    std::vector<int64_t> size(nhgt, 0);
+    for (int64_t s = 0; s < n; ++s)
+      if (P.head_pos_h[s] < 0) size[hgt[P.sperm[s]]]++;
+    P.bwdnh_level_ptr.assign(nhgt + 1, 0);
+    for (int l = 0; l < nhgt; ++l) P.bwdnh_level_ptr[l + 1] = P.bwdnh_level_ptr[l] + (int32_t)((size[l] + 31) / 32 * 32);
+    P.bwdnh_order_h.assign(P.bwdnh_level_ptr[nhgt], -1);
+    std::vector<int32_t> fl(P.bwdnh_level_ptr.begin(), P.bwdnh_level_ptr.end() - 1);
+    for (int64_t s = 0; s < n; ++s)
+      if (P.head_pos_h[s] < 0) P.bwdnh_order_h[fl[hgt[P.sperm[s]]]++] = (int32_t)s;
+  }
 }
 
 }  // namespace vl

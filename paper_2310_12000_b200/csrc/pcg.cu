@@ -301,9 +301,9 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
     // init
     ProfScope ps_init(C, t == 1 ? "cg1_init" : "cgT_init", 0.0);
     launch_rows<G, NU, U, 1, 0>(C, n, t, InitBody{b, r.as<double>(), u, hb[0], ld}, InitFin{K, tol});
-    launch_trsv<G, NU, U, 0>(C, P, false, t, ld, dbw, w.as<double>(),
+    launch_trsv<G, NU, U, 0>(C, F, false, t, ld, dbw, w.as<double>(),
                              RhsPlainActive{r.as<double>(), ld}, Fin0<0>{}, gate);
-    launch_trsv<G, NU, U, 1>(C, P, true, t, ld, dfw, z.as<double>(),
+    launch_trsv<G, NU, U, 1>(C, F, true, t, ld, dfw, z.as<double>(),
                              RhsScaleDot{w.as<double>(), S.dinv, r.as<double>(), ld}, RzInitFin{K}, gate);
     int status[3] = {0, 0, 0};
     int l = 0;
@@ -326,13 +326,13 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
         }
         {
           ProfScope ps(C, t == 1 ? "cg1_trsv_Bt" : "cgT_trsv_Bt", bapply_bytes(P, t, 0));
-          launch_trsv<G, NU, U, 1>(C, P, false, t, ld, dbw, w.as<double>(),
+          launch_trsv<G, NU, U, 1>(C, F, false, t, ld, dbw, w.as<double>(),
                                    K3Rhs{r.as<double>(), u, v.as<double>(), hn, K.alpha, K.active, ld},
                                    K3Fin{K, l}, gate);
         }
         {
           ProfScope ps(C, t == 1 ? "cg1_trsv_B" : "cgT_trsv_B", bapply_bytes(P, t, 1));
-          launch_trsv<G, NU, U, 1>(C, P, true, t, ld, dfw, z.as<double>(),
+          launch_trsv<G, NU, U, 1>(C, F, true, t, ld, dfw, z.as<double>(),
                                    RhsScaleDot{w.as<double>(), S.dinv, r.as<double>(), ld}, K4Fin{K, l, cap}, gate);
         }
       }

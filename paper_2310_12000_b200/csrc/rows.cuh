@@ -224,7 +224,10 @@ VL_D void trsv_row(int64_t p, int64_t pend_, int t, int ld, const int32_t* __res
                    double* __restrict__ x, const Body& body, unsigned smax, long long* __restrict__ tstamp, int gl,
                    double (&acc0)[NU * U]) {
   constexpr int NC = NU * U;
-  constexpr int BATCH = (NC == 1) ? 32 : (NC == 2 ? 16 : 8);
+#ifndef VL_BATCH2
+#define VL_BATCH2 16
+#endif
+  constexpr int BATCH = (NC == 1) ? 32 : (NC == 2 ? VL_BATCH2 : 8);
   using CL = Cols<G, NU, U>;
   const int32_t so = (p < pend_) ? order[p] : -1;
   const bool valid = so >= 0;
@@ -369,7 +372,8 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
                                                              double* __restrict__ partials,
                                                              unsigned* __restrict__ counter,
                                                              const int* __restrict__ gate, unsigned smax,
-                                                             long long* __restrict__ tstamp) {
+                                                             long long* __restrict__ tstamp, int slot_base,
+                                                             int total_slots) {
   if (gate != nullptr && *((volatile const int*)gate) == 0) return;
   extern __shared__ double rsh[];
   constexpr int NRR = NR > 0 ? NR : 1;
@@ -434,8 +438,8 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
     }
   }
   if constexpr (NR > 0) {
-    block_reduce_cols<1, 1, 1, NR, 0>(acc, 1, partials + (size_t)blockIdx.x * NR, rsh);
-    grid_finalize<NR, 0>(partials, counter, 1, fin, rsh);
+    block_reduce_cols<1, 1, 1, NR, 0>(acc, 1, partials + (size_t)(slot_base + blockIdx.x) * NR, rsh);
+    grid_finalize<NR, 0>(partials, counter, 1, fin, rsh, total_slots);
   }
 }
 
