@@ -59,7 +59,7 @@ struct Ctx {
   int num_sms = 148;
   std::string last_error;
   // CTAs per SM for the dependency-driven solves (bounds the spinning warps)
-  int trsv_blocks_per_sm = 2;
+  int trsv_blocks_per_sm = 4;
   // max nanosleep backoff while spinning on a dependency (0 = pure polling)
   int spin_max_ns = 64;
   // thin solve levels: <= thin_passes * (1024 / G) rows run on a single CTA

@@ -117,46 +117,42 @@ struct RzInitFin {
   }
 };
 
-// ---- K1: h = z + beta hprev; tmp = Dinv (B h) ------------------------------
-struct K1Body {
-  BView B;
+// ---- K0: h = z + beta h (elementwise, in place) ------------------------------
+struct HUpdBody {
   const double* z;
-  const double* hprev;
   double* h;
-  double* tmp;
-  const double* Dinv;
   const double* beta;
   int ld;
   template <int G, int NU, int U, int NR>
   VL_D void run(int64_t s, bool valid, int gl, int t, double (&)[NR][NU * U]) const {
-    double bt[NU * U];
+    if (!valid) return;
+    double zs[NU * U], hs[NU * U];
+    load_row<G, NU, U>(z, ld, s, gl, t, zs);
+    load_row<G, NU, U>(h, ld, s, gl, t, hs);
 #pragma unroll
     for (int i = 0; i < NU * U; ++i) {
       const int c = vl::Cols<G, NU, U>::col(gl, i);
-      bt[i] = c < t ? beta[c] : 0.0;
-    }
-    auto load = [&](int64_t j, int c, double* out) {
-      double zz[U], hh[U];
-      load_unit<U>(z + j * ld + c, zz);
-      load_unit<U>(hprev + j * ld + c, hh);
-      const int i0 = U * ((c / U - gl) / G);
-#pragma unroll
-      for (int i = 0; i < U; ++i) out[i] = zz[i] + bt[i0 + i] * hh[i];
-    };
-    double a[NU * U];
-    zero(a);
-    gather_B<G, NU, U>(B, B.val, s, valid, gl, t, load, a);
-    if (!valid) return;
-    double hs[NU * U];
-#pragma unroll
-    for (int k = 0; k < NU; ++k) {
-      const int c = U * (gl + G * k);
-      if (c < t) load(s, c, &hs[U * k]);
-      else
-#pragma unroll
-        for (int i = 0; i < U; ++i) hs[U * k + i] = 0.0;
+      hs[i] = zs[i] + (c < t ? beta[c] : 0.0) * hs[i];
     }
     store_row<G, NU, U>(h, ld, s, gl, t, hs);
+  }
+};
+
+// ---- K1: tmp = Dinv (B h) ------------------------------------------------------
+struct K1Body {
+  BView B;
+  const double* h;
+  double* tmp;
+  const double* Dinv;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&)[NR][NU * U]) const {
+    double a[NU * U];
+    zero(a);
+    gather_B<G, NU, U>(B, B.val, s, valid, gl, t, LoadU<U>{h, ld}, a);
+    if (!valid) return;
+    double hs[NU * U];
+    load_row<G, NU, U>(h, ld, s, gl, t, hs);
     const double di = Dinv[s];
 #pragma unroll
     for (int i = 0; i < NU * U; ++i) a[i] = di * (hs[i] + a[i]);
@@ -311,13 +307,14 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
     while (l < max_iter) {
       const int lim = std::min(max_iter, l + chunk);
       for (; l < lim; ++l) {
-        double* hp = hb[l & 1];
-        double* hn = hb[(l + 1) & 1];
+        double* hn = hb[0];
+        {
+          ProfScope ps(C, t == 1 ? "cg1_hupd" : "cgT_hupd", 24.0 * n * t);
+          launch_rows<G, NU, U, 0, 0>(C, n, t, HUpdBody{z.as<double>(), hn, K.beta, ld}, Fin0<0>{}, gate);
+        }
         {
           ProfScope ps(C, t == 1 ? "cg1_spmm_B" : "cgT_spmm_B", bapply_bytes(P, t, 1));
-          launch_rows<G, NU, U, 0, 0>(C, n, t,
-                                      K1Body{B, z.as<double>(), hp, hn, tmp.as<double>(), S.Dinv, K.beta, ld},
-                                      Fin0<0>{}, gate);
+          launch_rows<G, NU, U, 0, 0>(C, n, t, K1Body{B, hn, tmp.as<double>(), S.Dinv, ld}, Fin0<0>{}, gate);
         }
         {
           ProfScope ps(C, t == 1 ? "cg1_spmm_Bt" : "cgT_spmm_Bt", bapply_bytes(P, t, 1));

@@ -225,7 +225,7 @@ VL_D void trsv_row(int64_t p, int64_t pend_, int t, int ld, const int32_t* __res
                    double (&acc0)[NU * U]) {
   constexpr int NC = NU * U;
 #ifndef VL_BATCH2
-#define VL_BATCH2 16
+#define VL_BATCH2 4
 #endif
   constexpr int BATCH = (NC == 1) ? 32 : (NC == 2 ? VL_BATCH2 : 8);
   using CL = Cols<G, NU, U>;
