@@ -162,6 +162,49 @@ int vl_grad_probe_pass(vl_ctx* ctx, const vl_factor* f, const double* W_dev, con
                        const double* V_dev, int64_t t, double* s_dev, double* cols4_host, const double* md3x_dev,
                        double* xicols2_host);
 
+/* ---- LRAC preconditioner and the eq7 system (preconditioners.py:167-214,
+ * 249-320; laplace.py:118-182) ------------------------------------------------ */
+typedef struct vl_lrac vl_lrac;    /* rank-k pivoted Cholesky of Sigma (theta only) */
+typedef struct vl_lracw vl_lracw;  /* Woodbury core M = I + L^T W L for one W       */
+
+/* greedy pivoted Cholesky (pivoted_cholesky_with_pivots, preconditioners.py:288-320);
+ * piv_host: factor-order pivots (>= k entries), keff: achieved rank */
+int vl_lrac_create(vl_ctx* ctx, const vl_factor* f, int k, double tol, vl_lrac** out, int32_t* piv_host, int* keff);
+int vl_lrac_destroy(vl_lrac* l);
+/* L (n x k row-major, storage order) to host */
+int vl_lrac_get_L(vl_ctx* ctx, const vl_lrac* l, double* host);
+/* LowRankPlusDiagonal(L, 1/W) (preconditioners.py:176-190); out2 = [log det M, sum log W];
+ * VL_ECAPABILITY when some W <= 0 (laplace.py:122-127) */
+int vl_lrac_prepare(vl_ctx* ctx, const vl_lrac* l, const double* W_dev, vl_lracw** out, double* out2_host);
+int vl_lracw_destroy(vl_lracw* w);
+/* z = P^-1 r (Woodbury, preconditioners.py:192-196), n x t */
+int vl_lrac_apply_inv(vl_ctx* ctx, const vl_lracw* w, int64_t t, const double* r_dev, double* z_dev);
+/* PCG on (SigmaTilde + W^-1) U = Bm with the LRAC preconditioner (eq7 probes) */
+int vl_lrac_pcg(vl_ctx* ctx, const vl_lracw* w, int64_t t, const double* B_dev, double* U_dev, double tol,
+                int max_iter, int capture, int32_t* iters_host, int32_t* conv_host, double* res_host,
+                double* alpha_host, double* beta_host, int hist_cap);
+/* u = (W + SigmaTilde^-1)^-1 rhs through the eq7 form (laplace.py:176-179) */
+int vl_lrac_solve_system(vl_ctx* ctx, const vl_lracw* w, int64_t t, const double* rhs_dev, double* u_dev, double tol,
+                         int max_iter, int32_t* iters_host);
+/* y = SigmaTilde x = B^-1 (D o B^-T x) (vecchia.py:185-192) */
+int vl_apply_sigma_tilde(vl_ctx* ctx, const vl_factor* f, int64_t t, const double* x_dev, double* y_dev);
+/* Z = sqrt(1/W) o Gn + L Gk (preconditioners.py:204-207), V = P^-1 Z, w_c = z_c . v_c */
+int vl_lrac_probes(vl_ctx* ctx, const vl_lracw* w, int64_t t, const double* Gn_dev, const double* Gk_dev,
+                   double* Z_dev, double* V_dev, double* w_host);
+/* find_mode with the LRAC preconditioner / eq7 system */
+int vl_find_mode_lrac(vl_ctx* ctx, const vl_factor* f, const vl_lrac* l, const vl_lik* lik, const vl_newton_cfg* cfg,
+                      const double* y_dev, const double* F_dev, double* b_dev, double* W_dev, double* d1_dev,
+                      double* d3_dev, double* out_host, int32_t* cg_iters_host, int cg_iters_cap);
+/* LRAC gradient pieces (replaces the preconditioner == "lrac" branches of
+ * laplace.py:421-431 d logdet/d mu, 369-386 _lrac_dL, 527-533 dP_trace/dP_op and
+ * the eq7 dA_op = -SigmaTilde dQ SigmaTilde of 493-541).  U = A^-1 Z, V = P^-1 Z
+ * (n x t device).  s_dev (n) = 0.5 d logdet / d mu; host outputs: hcols/rcols
+ * 2 x t (sigma2, rho) STE samples, dPt 2 control-variate traces; md3x_dev
+ * (gamma only, else NULL): xicols 2 x t (h_xi, r_xi), xis = [sum G2 m3, sum m3/W]. */
+int vl_lrac_grad(vl_ctx* ctx, const vl_lracw* w, int64_t t, const double* U_dev, const double* V_dev,
+                 const double* d3_dev, const double* md3x_dev, double* s_dev, double* hcols_host, double* rcols_host,
+                 double* dPt_host, double* xicols_host, double* xis_host);
+
 /* Probe-sharded split of vl_grad_probe_pass for multi-GPU runs (the per-row
  * control-variate weights need all t_glob probes):
  *   mode 1: rowA = [sum_c U*V, sum_c (BV)^2] over the local t columns (n x 2,

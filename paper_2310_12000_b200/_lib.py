@@ -122,3 +122,22 @@ _SIGS.update({
                                  c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
 })
 EXPORTED = sorted(_SIGS)
+
+_SIGS.update({
+    "vl_lrac_create": [c_void_p, c_void_p, c_int, c_double, C.POINTER(c_void_p), c_void_p, C.POINTER(c_int)],
+    "vl_lrac_destroy": [c_void_p],
+    "vl_lrac_get_L": [c_void_p, c_void_p, c_void_p],
+    "vl_lrac_prepare": [c_void_p, c_void_p, c_void_p, C.POINTER(c_void_p), c_void_p],
+    "vl_lracw_destroy": [c_void_p],
+    "vl_lrac_apply_inv": [c_void_p, c_void_p, c_int64, c_void_p, c_void_p],
+    "vl_lrac_pcg": [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_double, c_int, c_int, c_void_p, c_void_p,
+                    c_void_p, c_void_p, c_void_p, c_int],
+    "vl_lrac_solve_system": [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_double, c_int, c_void_p],
+    "vl_apply_sigma_tilde": [c_void_p, c_void_p, c_int64, c_void_p, c_void_p],
+    "vl_lrac_probes": [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    "vl_lrac_grad": [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                     c_void_p, c_void_p, c_void_p],
+    "vl_find_mode_lrac": [c_void_p, c_void_p, c_void_p, C.POINTER(VlLik), C.POINTER(VlNewtonCfg), c_void_p, c_void_p,
+                          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int],
+})
+EXPORTED = sorted(_SIGS)

@@ -11,6 +11,7 @@
 
 #include "../../include/vlgpx.h"
 #include "laplace.h"
+#include "lrac.h"
 #include "ops.h"
 #include "pcg.h"
 
@@ -23,6 +24,13 @@ struct vl_pattern {
 };
 struct vl_factor {
   vl::Factor f;
+};
+struct vl_lrac {
+  vl::LracFactor lf;
+  const vl_factor* f;
+};
+struct vl_lracw {
+  vl::LracPrec p;
 };
 
 namespace vl {
@@ -448,6 +456,144 @@ int vl_find_mode(vl_ctx* h, const vl_factor* f, const vl_lik* lik, const vl_newt
     };
     try {
       newton_mode(h->c, f->f, L, nc, y, Fv, b, W, d1, d3, &no);
+    } catch (...) {
+      fill();
+      throw;
+    }
+    fill();
+  });
+}
+
+// ---- LRAC -----------------------------------------------------------------------
+
+int vl_lrac_create(vl_ctx* h, const vl_factor* f, int k, double tol, vl_lrac** out, int32_t* piv_host, int* keff) {
+  return guard([&] {
+    auto* l = new vl_lrac();
+    l->f = f;
+    try {
+      lrac_pchol(h->c, f->f, l->lf, k, tol);
+    } catch (...) {
+      delete l;
+      throw;
+    }
+    if (keff) *keff = l->lf.keff;
+    if (piv_host)
+      for (int q = 0; q < l->lf.keff; ++q) piv_host[q] = l->lf.piv_f[q];
+    *out = l;
+  });
+}
+
+int vl_lrac_destroy(vl_lrac* l) {
+  return guard([&] { delete l; });
+}
+
+int vl_lrac_get_L(vl_ctx* h, const vl_lrac* l, double* host) {
+  return guard([&] {
+    const size_t cnt = (size_t)l->f->f.pat->n * l->lf.k;
+    VL_CUDA(cudaMemcpyAsync(host, l->lf.L.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, h->c.stream));
+    VL_CUDA(cudaStreamSynchronize(h->c.stream));
+  });
+}
+
+int vl_lrac_prepare(vl_ctx* h, const vl_lrac* l, const double* W, vl_lracw** out, double* out2) {
+  return guard([&] {
+    const int64_t n = l->f->f.pat->n;
+    if (count_nonpos(h->c, n, W) > 0)
+      fail(kECapability, "lrac preconditions SigmaTilde + W^{-1} and needs W > 0 everywhere (eq7 split; log W "
+                         "undefined); switch to an eq6 preconditioner such as vadu");
+    auto* w = new vl_lracw();
+    try {
+      lrac_prepare(h->c, l->f->f, l->lf, W, w->p);
+      w->p.sumlogW = lrac_sumlogW(h->c, n, W);
+    } catch (...) {
+      delete w;
+      throw;
+    }
+    if (out2) {
+      out2[0] = w->p.logdetM;
+      out2[1] = w->p.sumlogW;
+    }
+    *out = w;
+  });
+}
+
+int vl_lracw_destroy(vl_lracw* w) {
+  return guard([&] { delete w; });
+}
+
+int vl_lrac_apply_inv(vl_ctx* h, const vl_lracw* w, int64_t t, const double* r, double* z) {
+  return guard([&] { lrac_apply_inv(h->c, w->p, (int)t, r, z); });
+}
+
+int vl_lrac_pcg(vl_ctx* h, const vl_lracw* w, int64_t t, const double* bm, double* u, double tol, int max_iter,
+                int capture, int32_t* iters, int32_t* conv, double* res, double* alpha, double* beta, int hist_cap) {
+  return guard([&] {
+    if (t < 1 || t > 128) fail(kECapacity, "right-hand sides per call must be in [1, 128]");
+    PcgResult pr;
+    pcg_lrac(h->c, w->p, (int)t, bm, u, tol, max_iter, capture != 0, &pr);
+    for (int c = 0; c < t; ++c) {
+      if (iters) iters[c] = pr.iters[c];
+      if (conv) conv[c] = pr.converged[c];
+      if (res) res[c] = pr.res[c];
+    }
+    if (capture && alpha && beta)
+      for (int q = 0; q < std::min(pr.max_iters, hist_cap); ++q)
+        for (int c = 0; c < t; ++c) {
+          alpha[(size_t)q * t + c] = pr.alpha[(size_t)q * t + c];
+          beta[(size_t)q * t + c] = pr.beta[(size_t)q * t + c];
+        }
+  });
+}
+
+int vl_lrac_solve_system(vl_ctx* h, const vl_lracw* w, int64_t t, const double* rhs, double* u, double tol,
+                         int max_iter, int32_t* iters) {
+  return guard([&] {
+    PcgResult pr;
+    lrac_solve_system(h->c, w->p, (int)t, rhs, u, tol, max_iter, &pr);
+    if (iters)
+      for (int c = 0; c < t; ++c) iters[c] = pr.iters[c];
+  });
+}
+
+int vl_apply_sigma_tilde(vl_ctx* h, const vl_factor* f, int64_t t, const double* x, double* y) {
+  return guard([&] {
+    DevBuf scr;
+    scr.alloc(sizeof(double) * (size_t)f->f.pat->n * t);
+    apply_sigma_tilde(h->c, f->f, (int)t, x, y, scr.as<double>());
+  });
+}
+
+int vl_lrac_probes(vl_ctx* h, const vl_lracw* w, int64_t t, const double* Gn, const double* Gk, double* Z, double* V,
+                   double* w_host) {
+  return guard([&] { lrac_probes(h->c, w->p, (int)t, Gn, Gk, Z, V, w_host); });
+}
+
+int vl_lrac_grad(vl_ctx* h, const vl_lracw* w, int64_t t, const double* U, const double* V, const double* d3,
+                 const double* md3x, double* s, double* hcols, double* rcols, double* dPt, double* xicols,
+                 double* xis) {
+  return guard([&] { lrac_grad(h->c, w->p, (int)t, U, V, d3, md3x, s, hcols, rcols, dPt, xicols, xis); });
+}
+
+int vl_find_mode_lrac(vl_ctx* h, const vl_factor* f, const vl_lrac* l, const vl_lik* lik, const vl_newton_cfg* cfg,
+                      const double* y, const double* Fv, double* b, double* W, double* d1, double* d3, double* out,
+                      int32_t* cg_iters, int cg_iters_cap) {
+  return guard([&] {
+    LikSpec L{lik->family, lik->shape};
+    NewtonCfg nc{cfg->mode_cg_tol, cfg->cg_max_iter, cfg->newton_max_iter, cfg->newton_grad_tol, cfg->newton_obj_tol};
+    NewtonOut no;
+    auto fill = [&] {
+      out[0] = no.logp;
+      out[1] = no.quad;
+      out[2] = no.objective;
+      out[3] = no.grad_norm;
+      out[4] = no.iters;
+      out[5] = no.converged;
+      out[6] = (double)no.cg_iters.size();
+      if (cg_iters)
+        for (int i = 0; i < (int)no.cg_iters.size() && i < cg_iters_cap; ++i) cg_iters[i] = no.cg_iters[i];
+    };
+    try {
+      newton_mode(h->c, f->f, L, nc, y, Fv, b, W, d1, d3, &no, &l->lf);
     } catch (...) {
       fill();
       throw;

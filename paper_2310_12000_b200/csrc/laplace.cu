@@ -5,6 +5,7 @@
 #include "bodies.cuh"
 #include "laplace.h"
 #include "launch.cuh"
+#include "lrac.h"
 #include "ops.h"
 
 namespace vl {
@@ -204,8 +205,26 @@ void vadu_diags(Ctx& C, const Factor& F, const double* W, double* Dinv, double* 
   launch_rows<1, 1, 1, 0, 0>(C, F.pat->n, 1, DiagsBody{F.D.as<double>(), W, Dinv, dinv}, Fin0<0>{});
 }
 
+namespace {
+struct CountNonPosBody {  // #{W <= 0} (LRAC / eq7 require W > 0)
+  const double* W;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int, int, double (&acc)[NR][NU * U]) const {
+    if (valid && !(W[s] > 0.0)) acc[0][0] += 1.0;
+  }
+};
+}  // namespace
+
+double count_nonpos(Ctx& C, int64_t n, const double* W) {
+  double* sums = C.dev_scalars.as<double>();
+  launch_rows<1, 1, 1, 1, 0>(C, n, 1, CountNonPosBody{W}, CopySums<1>{sums});
+  double g;
+  read_sums(C, sums, &g, 1);
+  return g;
+}
+
 void newton_mode(Ctx& C, const Factor& F, const LikSpec& LS, const NewtonCfg& cfg, const double* y, const double* Fv,
-                 double* b, double* W, double* d1, double* d3, NewtonOut* out) {
+                 double* b, double* W, double* d1, double* d3, NewtonOut* out, const LracFactor* lrac) {
   const Pattern& P = *F.pat;
   const int64_t n = P.n;
   const Lik L = make_lik(LS);
@@ -249,7 +268,17 @@ void newton_mode(Ctx& C, const Factor& F, const LikSpec& LS, const NewtonCfg& cf
     if (rn > 0.0) tol = std::min(tol, std::max(safety * 0.25 * gnorm / rn, 1e-14));
     vadu_diags(C, F, W, Dinv.as<double>(), dinv.as<double>());
     PcgResult pr;
-    pcg_vadu(C, S, 1, 1, rhs.as<double>(), bnew.as<double>(), tol, cfg.cg_max_iter, false, &pr);
+    if (lrac == nullptr) {
+      pcg_vadu(C, S, 1, 1, rhs.as<double>(), bnew.as<double>(), tol, cfg.cg_max_iter, false, &pr);
+    } else {
+      if (count_nonpos(C, n, W) > 0)
+        fail(kECapability,
+             "lrac preconditions SigmaTilde + W^{-1} and needs W > 0 everywhere (eq7 split; log W undefined); "
+             "switch to an eq6 preconditioner such as vadu");
+      LracPrec Pr;
+      lrac_prepare(C, F, *lrac, W, Pr);
+      lrac_solve_system(C, Pr, 1, rhs.as<double>(), bnew.as<double>(), tol, cfg.cg_max_iter, &pr);
+    }
     out->cg_iters.push_back(pr.iters[0]);
     launch_rows<1, 1, 1, 0, 0>(C, n, 1, DiffBody{bnew.as<double>(), b, delta.as<double>()}, Fin0<0>{});
     double step = 1.0, obj_try = 0.0, quad_try = 0.0;

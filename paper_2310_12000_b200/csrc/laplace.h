@@ -31,8 +31,15 @@ struct NewtonOut {
 
 // Damped Newton for b* (laplace.py:204-287).  Device vectors (storage order,
 // length n): y, F in; b, W, d1, d3 out.  Throws kEConvergence (state valid).
+struct LracFactor;
+// lrac != nullptr selects the LRAC preconditioner with the eq7 system
+// (laplace.py:118-127 CapabilityError when some W <= 0).
 void newton_mode(Ctx& C, const Factor& F, const LikSpec& L, const NewtonCfg& cfg, const double* y,
-                 const double* Fv, double* b, double* W, double* d1, double* d3, NewtonOut* out);
+                 const double* Fv, double* b, double* W, double* d1, double* d3, NewtonOut* out,
+                 const LracFactor* lrac = nullptr);
+
+// number of entries with W <= 0 (eq7 / LRAC capability check)
+double count_nonpos(Ctx& C, int64_t n, const double* W);
 
 // 1/D and 1/(W + 1/D) (VADU diagonal)
 void vadu_diags(Ctx& C, const Factor& F, const double* W, double* Dinv, double* dinv);

@@ -1,0 +1,1061 @@
+// LRAC: low-rank pivoted Cholesky of the exact covariance + diag(1/W),
+// Woodbury solves, eq7 operator SigmaTilde + W^-1 (preconditioners.py:167-214,
+// 249-320; laplace.py:118-182).
+//
+// Hand-written: the pivoted Cholesky step (Matern row of the pivot + the
+// n x j GEMV against the previous columns + diagonal update + deterministic
+// argmax of the next pivot, all in one kernel per step), the sparse
+// operator applies, all elementwise/reduction passes.  Library: the plain
+// n x k GEMMs / k x k triangular solves of the Woodbury core (cuBLAS) and the
+// k x k Cholesky of M (cuSOLVER potrf).
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <cmath>
+#include <mutex>
+
+#include "bodies.cuh"
+#include "launch.cuh"
+#include "lrac.h"
+#include "ops.h"
+#include "pcg_common.cuh"
+
+namespace vl {
+
+namespace {
+
+std::mutex g_h_mu;
+cublasHandle_t g_blas[16] = {};
+cusolverDnHandle_t g_solv[16] = {};
+
+cublasHandle_t blas(Ctx& C) {
+  std::lock_guard<std::mutex> lk(g_h_mu);
+  cublasHandle_t& h = g_blas[C.device & 15];
+  if (!h) {
+    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) fail(kECuda, "cublasCreate failed");
+  }
+  cublasSetStream(h, C.stream);
+  return h;
+}
+cusolverDnHandle_t solver(Ctx& C) {
+  std::lock_guard<std::mutex> lk(g_h_mu);
+  cusolverDnHandle_t& h = g_solv[C.device & 15];
+  if (!h) {
+    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) fail(kECuda, "cusolverDnCreate failed");
+  }
+  cusolverDnSetStream(h, C.stream);
+  return h;
+}
+void blas_ok(cublasStatus_t s, const char* what) {
+  if (s != CUBLAS_STATUS_SUCCESS) fail(kECuda, std::string("cuBLAS failure in ") + what);
+}
+
+struct MaternK {
+  double s2, rho, c;
+  int nu;
+  VL_D double val(double r) const {
+    if (nu == 0) return s2 * exp(-r / rho);
+    const double u = c * r;
+    if (nu == 1) return s2 * (1.0 + u) * exp(-u);
+    return s2 * (1.0 + u + u * u / 3.0) * exp(-u);
+  }
+};
+
+MaternK make_matern(const Factor& F) {
+  MaternK K;
+  K.s2 = F.sigma2;
+  K.rho = F.rho;
+  if (F.nu == 0.5) { K.nu = 0; K.c = 1.0 / F.rho; }
+  else if (F.nu == 1.5) { K.nu = 1; K.c = std::sqrt(3.0) / F.rho; }
+  else { K.nu = 2; K.c = std::sqrt(5.0) / F.rho; }
+  return K;
+}
+
+// pivoted-Cholesky state (device): [0] pivot storage index, [1] stop, [2] err, [3] keff ; dp in doubles
+struct PcState {
+  int* i;
+  double* dp;
+};
+
+constexpr int kPcThreads = 256;
+
+__global__ void fill_kernel(int64_t n, double v, double* d) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = v;
+}
+
+// One greedy step j (preconditioners.py:308-319): col = (Sigma[:, p] - L[:, :j] L[p, :j]) / sqrt(d_p),
+// col_p = sqrt(d_p), d -= col^2, d_p = 0; then min(d), sum(max(d, 0)) and the argmax (ties -> lowest
+// factor index) for step j+1, finalised by the last CTA.
+__global__ void __launch_bounds__(kPcThreads) pchol_step_kernel(int64_t n, int dim, const double* __restrict__ xy,
+                                                               const int32_t* __restrict__ fidx, MaternK K, int j,
+                                                               int k, double* __restrict__ L, double* __restrict__ d,
+                                                               PcState st, double tol, double* __restrict__ part,
+                                                               unsigned* __restrict__ counter,
+                                                               int32_t* __restrict__ piv_s) {
+  if (((volatile int*)st.i)[1] != 0) return;
+  __shared__ double s_min[kPcThreads / 32], s_sum[kPcThreads / 32], s_max[kPcThreads / 32];
+  __shared__ int s_arg[kPcThreads / 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int p = st.i[0];
+  const double dp = *st.dp;
+  const double sq = sqrt(dp);
+  const double* Lp = L + (int64_t)p * k;
+  const double* xp = xy + (int64_t)p * dim;
+  double wmin = 1e300, wsum = 0.0, wmax = -1.0;
+  int warg = 0x7fffffff;  // factor index of the best
+  int wsrow = -1;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = gw; i < n; i += nw) {
+    double* Li = L + i * k;
+    double dot = 0.0;
+    for (int l = lane; l < j; l += 32) dot += Li[l] * Lp[l];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if (lane == 0) {
+      double r2 = 0.0;
+      for (int q = 0; q < dim; ++q) {
+        const double df = xy[i * dim + q] - xp[q];
+        r2 += df * df;
+      }
+      double col = (K.val(sqrt(r2)) - dot) / sq;
+      double di = fmax(d[i], 0.0);  // np.clip(d, 0) of this step
+      if (i == p) col = sq;
+      Li[j] = col;
+      di = di - col * col;
+      if (i == p) di = 0.0;
+      d[i] = di;
+      wmin = fmin(wmin, di);
+      const double dc = fmax(di, 0.0);
+      wsum += dc;
+      const int fi = fidx[i];
+      if (dc > wmax || (dc == wmax && fi < warg)) {
+        wmax = dc;
+        warg = fi;
+        wsrow = (int)i;
+      }
+    }
+  }
+  // block reduction (lane 0 of each warp holds the warp's values)
+  if (lane == 0) {
+    s_min[wib] = wmin;
+    s_sum[wib] = wsum;
+    s_max[wib] = wmax;
+    s_arg[wib] = wsrow;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bmin = 1e300, bsum = 0.0, bmax = -1.0;
+    int brow = -1, bf = 0x7fffffff;
+    for (int w = 0; w < kPcThreads / 32; ++w) {
+      bmin = fmin(bmin, s_min[w]);
+      bsum += s_sum[w];
+      if (s_arg[w] >= 0) {
+        const int f = fidx[s_arg[w]];
+        if (s_max[w] > bmax || (s_max[w] == bmax && f < bf)) {
+          bmax = s_max[w];
+          bf = f;
+          brow = s_arg[w];
+        }
+      }
+    }
+    double* pb = part + (size_t)blockIdx.x * 4;
+    pb[0] = bmin;
+    pb[1] = bsum;
+    pb[2] = bmax;
+    pb[3] = (double)brow;
+    __threadfence();
+    const unsigned tk = atomicAdd(counter, 1u);
+    if (tk == gridDim.x - 1) {
+      __threadfence();
+      double gmin = 1e300, gsum = 0.0, gmax = -1.0;
+      int grow = -1, gf = 0x7fffffff;
+      for (unsigned b = 0; b < gridDim.x; ++b) {
+        const double* q = part + (size_t)b * 4;
+        gmin = fmin(gmin, __ldcg(q));
+        gsum += __ldcg(q + 1);
+        const int row = (int)__ldcg(q + 3);
+        const double mx = __ldcg(q + 2);
+        if (row >= 0) {
+          const int f = fidx[row];
+          if (mx > gmax || (mx == gmax && f < gf)) {
+            gmax = mx;
+            gf = f;
+            grow = row;
+          }
+        }
+      }
+      piv_s[j] = p;
+      st.i[3] = j + 1;
+      if (j + 1 < k) {
+        if (gmin < -1e-10) {
+          st.i[2] = 1;
+          st.i[1] = 1;
+        } else if (gsum <= tol || !(gmax > 0.0)) {
+          st.i[1] = 1;
+        } else {
+          st.i[0] = grow;
+          *st.dp = gmax;
+        }
+      }
+      *counter = 0u;
+    }
+  }
+}
+
+__global__ void scale_rows_kernel(int64_t n, int k, const double* __restrict__ W, const double* __restrict__ L,
+                                  double* __restrict__ S) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * k; e += (int64_t)gridDim.x * blockDim.x)
+    S[e] = sqrt(W[e / k]) * L[e];
+}
+
+__global__ void add_identity_kernel(int k, double* M) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) M[(size_t)i * k + i] += 1.0;
+}
+
+__global__ void sumlog_diag_kernel(int k, const double* __restrict__ M, double* out) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) s += log(M[(size_t)i * k + i]);
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int i = 0; i < (int)blockDim.x; ++i) a += sh[i];
+    *out = 2.0 * a;
+  }
+}
+
+// ---- elementwise bodies -----------------------------------------------------------
+struct MulWBody {  // x = W o r
+  const double* W;
+  const double* r;
+  double* x;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&)[NR][NU * U]) const {
+    if (!valid) return;
+    double a[NU * U];
+    load_row<G, NU, U>(r, ld, s, gl, t, a);
+    const double w = W[s];
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) a[i] *= w;
+    store_row<G, NU, U>(x, ld, s, gl, t, a);
+  }
+};
+template <bool DOT>
+struct WoodFinishBody {  // z = x - W o y ; acc += r . z
+  const double* W;
+  const double* x;
+  const double* y;
+  const double* r;
+  double* z;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    if (!valid) return;
+    double a[NU * U], b[NU * U], rr[NU * U];
+    load_row<G, NU, U>(x, ld, s, gl, t, a);
+    load_row<G, NU, U>(y, ld, s, gl, t, b);
+    const double w = W[s];
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) a[i] = a[i] - w * b[i];
+    store_row<G, NU, U>(z, ld, s, gl, t, a);
+    if (DOT) {
+      load_row<G, NU, U>(r, ld, s, gl, t, rr);
+#pragma unroll
+      for (int i = 0; i < NU * U; ++i) acc[0][i] += rr[i] * a[i];
+    }
+  }
+};
+struct Eq7FinishBody {  // v = sx + h / W ; acc += h . v
+  const double* W;
+  const double* sx;
+  const double* h;
+  double* v;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    if (!valid) return;
+    double a[NU * U], hs[NU * U];
+    load_row<G, NU, U>(sx, ld, s, gl, t, a);
+    load_row<G, NU, U>(h, ld, s, gl, t, hs);
+    const double w = W[s];
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) {
+      a[i] = a[i] + hs[i] / w;
+      acc[0][i] += hs[i] * a[i];
+    }
+    store_row<G, NU, U>(v, ld, s, gl, t, a);
+  }
+};
+struct UpdBody {  // r -= alpha v ; u += alpha h ; acc += r^2  (active columns)
+  double* r;
+  double* u;
+  const double* v;
+  const double* h;
+  const double* alpha;
+  const int* active;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    if (!valid) return;
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) {
+      const int c = vl::Cols<G, NU, U>::col(gl, i);
+      if (c >= t || !active[c]) continue;
+      const int64_t o = s * ld + c;
+      const double al = alpha[c];
+      const double rn = r[o] - al * v[o];
+      r[o] = rn;
+      u[o] = u[o] + al * h[o];
+      acc[0][i] += rn * rn;
+    }
+  }
+};
+struct DivWBody {  // y = x / W
+  const double* W;
+  const double* x;
+  double* y;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&)[NR][NU * U]) const {
+    if (!valid) return;
+    double a[NU * U];
+    load_row<G, NU, U>(x, ld, s, gl, t, a);
+    const double w = W[s];
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) a[i] /= w;
+    store_row<G, NU, U>(y, ld, s, gl, t, a);
+  }
+};
+struct RhsScaleD {  // trsv rhs = D o w
+  const double* w;
+  const double* D;
+  int ld;
+  VL_D double rhs(int64_t s, int c, double&) const { return w[s * ld + c] * D[s]; }
+  VL_D void out(int64_t, int, double, double&) const {}
+};
+struct RzFin {
+  cg::CgCols K;
+  VL_D void operator()(const double* sums, int t) const {
+    for (int c = threadIdx.x; c < t; c += blockDim.x) K.rz[c] = sums[c];
+  }
+};
+
+}  // namespace
+
+void lrac_free_handles() {
+  std::lock_guard<std::mutex> lk(g_h_mu);
+  for (auto& h : g_blas)
+    if (h) { cublasDestroy(h); h = nullptr; }
+  for (auto& h : g_solv)
+    if (h) { cusolverDnDestroy(h); h = nullptr; }
+}
+
+void lrac_pchol(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol) {
+  const Pattern& P = *F.pat;
+  const int64_t n = P.n;
+  if (k < 1 || k > n) fail(kEConfig, "rank k must be in [1, " + std::to_string(n) + "]");
+  LF.k = k;
+  LF.L.alloc(sizeof(double) * (size_t)n * k);
+  VL_CUDA(cudaMemsetAsync(LF.L.p, 0, sizeof(double) * (size_t)n * k, C.stream));
+  LF.piv_s.alloc(sizeof(int32_t) * k);
+  DevBuf d, st, part;
+  d.alloc(sizeof(double) * n);
+  st.alloc(64);
+  const int grid = std::min<int64_t>(C.num_sms * 8, (n * 32 + kPcThreads - 1) / kPcThreads);
+  part.alloc(sizeof(double) * 4 * (size_t)grid);
+  fill_kernel<<<C.num_sms * 4, 256, 0, C.stream>>>(n, F.sigma2, d.as<double>());
+  int h_i[4] = {P.iperm[0], 0, 0, 0};  // first pivot: all d equal -> lowest factor index
+  double h_dp = F.sigma2;
+  VL_CUDA(cudaMemcpyAsync(st.p, h_i, sizeof(h_i), cudaMemcpyHostToDevice, C.stream));
+  VL_CUDA(cudaMemcpyAsync(st.as<char>() + 32, &h_dp, sizeof(double), cudaMemcpyHostToDevice, C.stream));
+  PcState S{st.as<int>(), reinterpret_cast<double*>(st.as<char>() + 32)};
+  const MaternK K = make_matern(F);
+  unsigned* counter = next_counter(C);
+  ProfScope ps(C, "lrac_pchol", 0.0);
+  for (int j = 0; j < k; ++j) {
+    pchol_step_kernel<<<grid, kPcThreads, 0, C.stream>>>(n, P.d, P.xy.as<double>(), P.fidx.as<int32_t>(), K, j, k,
+                                                         LF.L.as<double>(), d.as<double>(), S, tol,
+                                                         part.as<double>(), counter, LF.piv_s.as<int32_t>());
+    VL_LAUNCH_CHECK();
+    C.prof.launches++;
+  }
+  VL_CUDA(cudaMemcpyAsync(h_i, st.p, sizeof(h_i), cudaMemcpyDeviceToHost, C.stream));
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+  if (h_i[2]) fail(kEFactorization, "pivoted Cholesky: diagonal went negative; input not PSD");
+  LF.keff = h_i[3];
+  std::vector<int32_t> ps_(LF.keff);
+  if (LF.keff) VL_CUDA(cudaMemcpy(ps_.data(), LF.piv_s.p, sizeof(int32_t) * LF.keff, cudaMemcpyDeviceToHost));
+  LF.piv_f.resize(LF.keff);
+  for (int q = 0; q < LF.keff; ++q) LF.piv_f[q] = P.sperm[ps_[q]];
+}
+
+void lrac_prepare(Ctx& C, const Factor& F, const LracFactor& LF, const double* W, LracPrec& Pr) {
+  const Pattern& P = *F.pat;
+  const int64_t n = P.n;
+  const int k = LF.keff;
+  Pr.F = &F;
+  Pr.LF = &LF;
+  Pr.W = W;
+  if (k == 0) {
+    Pr.logdetM = 0.0;
+    return;
+  }
+  ProfScope ps(C, "lrac_prepare", 0.0);
+  DevBuf S, info, ld;
+  S.alloc(sizeof(double) * (size_t)n * LF.k);
+  scale_rows_kernel<<<C.num_sms * 8, 256, 0, C.stream>>>(n, LF.k, W, LF.L.as<double>(), S.as<double>());
+  VL_LAUNCH_CHECK();
+  Pr.Lm.alloc(sizeof(double) * (size_t)k * k);
+  // M = S_k S_k^T with S viewed column-major as (LF.k x n); only the leading keff rows are used
+  const double one = 1.0, zero = 0.0;
+  blas_ok(cublasDsyrk(blas(C), CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, k, (int)n, &one, S.as<double>(), LF.k, &zero,
+                      Pr.Lm.as<double>(), k),
+          "dsyrk");
+  add_identity_kernel<<<8, 256, 0, C.stream>>>(k, Pr.Lm.as<double>());
+  VL_LAUNCH_CHECK();
+  cusolverDnHandle_t sh = solver(C);
+  int lwork = 0;
+  if (cusolverDnDpotrf_bufferSize(sh, CUBLAS_FILL_MODE_LOWER, k, Pr.Lm.as<double>(), k, &lwork) !=
+      CUSOLVER_STATUS_SUCCESS)
+    fail(kECuda, "potrf buffer size");
+  DevBuf work;
+  work.alloc(sizeof(double) * std::max(lwork, 1));
+  info.alloc(64);
+  if (cusolverDnDpotrf(sh, CUBLAS_FILL_MODE_LOWER, k, Pr.Lm.as<double>(), k, work.as<double>(), lwork,
+                       info.as<int>()) != CUSOLVER_STATUS_SUCCESS)
+    fail(kECuda, "potrf");
+  ld.alloc(64);
+  sumlog_diag_kernel<<<1, 256, 0, C.stream>>>(k, Pr.Lm.as<double>(), ld.as<double>());
+  int h_info = 0;
+  VL_CUDA(cudaMemcpyAsync(&h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+  VL_CUDA(cudaMemcpyAsync(&Pr.logdetM, ld.p, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+  if (h_info != 0) fail(kEFactorization, "LRAC Woodbury core M is not positive definite");
+}
+
+// z = W o r - W o (L M^-1 L^T (W o r))
+template <bool DOT, class Fin>
+static void woodbury(Ctx& C, const LracPrec& Pr, int t, const double* r, double* z, const Fin& fin, const int* gate) {
+  const Pattern& P = *Pr.F->pat;
+  const int64_t n = P.n;
+  const int k = Pr.LF->keff, kl = Pr.LF->k;
+  DevBuf x, y, w;
+  x.alloc(sizeof(double) * (size_t)n * t);
+  y.alloc(sizeof(double) * (size_t)n * t);
+  w.alloc(sizeof(double) * (size_t)std::max(k, 1) * t);
+  dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
+    constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
+    launch_rows<G, NU, U, 0, 0>(C, n, t, MulWBody{Pr.W, r, x.as<double>(), t}, Fin0<0>{}, gate);
+  });
+  if (k > 0) {
+    const double one = 1.0, zero = 0.0;
+    cublasHandle_t hb = blas(C);
+    // w (k x t) = A (k x n) * Xc^T ; A = L^T viewed column-major (lda = kl), Xc = x viewed (t x n, ld t)
+    blas_ok(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, k, t, (int)n, &one, Pr.LF->L.as<double>(), kl, x.as<double>(),
+                        t, &zero, w.as<double>(), k),
+            "dgemm Lt x");
+    blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, k, t, &one,
+                        Pr.Lm.as<double>(), k, w.as<double>(), k),
+            "dtrsm");
+    blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, k, t, &one,
+                        Pr.Lm.as<double>(), k, w.as<double>(), k),
+            "dtrsm T");
+    // Yc (t x n) = w^T (t x k) * A (k x n)
+    blas_ok(cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, t, (int)n, k, &one, w.as<double>(), k, Pr.LF->L.as<double>(),
+                        kl, &zero, y.as<double>(), t),
+            "dgemm L w");
+  } else {
+    VL_CUDA(cudaMemsetAsync(y.p, 0, sizeof(double) * (size_t)n * t, C.stream));
+  }
+  dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
+    constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
+    launch_rows<G, NU, U, DOT ? 1 : 0, 0>(C, n, t, WoodFinishBody<DOT>{Pr.W, x.as<double>(), y.as<double>(), r, z, t},
+                                         fin, gate);
+  });
+}
+
+void lrac_apply_inv(Ctx& C, const LracPrec& Pr, int t, const double* r, double* z) {
+  woodbury<false>(C, Pr, t, r, z, Fin0<0>{}, nullptr);
+}
+
+void apply_sigma_tilde(Ctx& C, const Factor& F, int t, const double* x, double* y, double* scratch) {
+  const Pattern& P = *F.pat;
+  DepsEll dfw{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
+  DepsCsr dbw{P.tptr.as<int32_t>(), P.tidx.as<int32_t>(), F.valT.as<double>()};
+  dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
+    constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
+    launch_trsv<G, NU, U, 0>(C, F, false, t, t, dbw, scratch, TrsvPlain{x, t}, Fin0<0>{});
+    launch_trsv<G, NU, U, 0>(C, F, true, t, t, dfw, y, RhsScaleD{scratch, F.D.as<double>(), t}, Fin0<0>{});
+  });
+}
+
+void pcg_lrac(Ctx& C, const LracPrec& Pr, int t, const double* b, double* u, double tol, int max_iter, bool capture,
+              PcgResult* out) {
+  using namespace cg;
+  const Factor& F = *Pr.F;
+  const Pattern& P = *F.pat;
+  const int64_t n = P.n;
+  if (!(tol > 0)) fail(kEConfig, "tol must be > 0");
+  const size_t vb = sizeof(double) * (size_t)n * t;
+  DevBuf r, z, v, h, sx, scr;
+  r.alloc(vb); z.alloc(vb); v.alloc(vb); h.alloc(vb); sx.alloc(vb); scr.alloc(vb);
+  const int cap = capture ? std::max(max_iter, 1) : 1;
+  DevBuf colsd, colsi, hist;
+  colsd.alloc(sizeof(double) * (7 * (size_t)t + 1));
+  colsi.alloc(sizeof(int) * (3 * (size_t)t + 4));
+  hist.alloc(sizeof(double) * 2 * (size_t)cap * t);
+  CgCols K;
+  double* cd = colsd.as<double>();
+  K.nb = cd; K.rz = cd + t; K.alpha = cd + 2 * t; K.beta = cd + 3 * t; K.res = cd + 4 * t; K.tolnb = cd + 5 * t;
+  K.errval = cd + 7 * t;
+  int* ci = colsi.as<int>();
+  K.active = ci; K.iters = ci + t; K.conv = ci + 2 * t; K.status = ci + 3 * t;
+  K.ah = hist.as<double>();
+  K.bh = K.ah + (size_t)cap * t;
+  const int* gate = K.status;
+  const Pattern& PP = P;
+  DepsEll dfw{PP.nbr.as<int32_t>(), PP.cnt.as<int32_t>(), F.val.as<double>(), PP.m};
+  DepsCsr dbw{PP.tptr.as<int32_t>(), PP.tidx.as<int32_t>(), F.valT.as<double>()};
+  int status[3] = {0, 0, 0};
+  dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
+    constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
+    ProfScope ps(C, t == 1 ? "lrac1_cg" : "lracT_cg", 0.0);
+    launch_rows<G, NU, U, 1, 0>(C, n, t, InitBody{b, r.as<double>(), u, h.as<double>(), t}, InitFin{K, tol});
+    woodbury<true>(C, Pr, t, r.as<double>(), z.as<double>(), RzFin{K}, gate);
+    int l = 0, chunk = 4;
+    while (l < max_iter) {
+      const int lim = std::min(max_iter, l + chunk);
+      for (; l < lim; ++l) {
+        launch_rows<G, NU, U, 0, 0>(C, n, t, HUpdBody{z.as<double>(), h.as<double>(), K.beta, t}, Fin0<0>{}, gate);
+        // v = SigmaTilde h + h / W
+        launch_trsv<G, NU, U, 0>(C, F, false, t, t, dbw, scr.as<double>(), TrsvPlain{h.as<double>(), t}, Fin0<0>{},
+                                 gate);
+        launch_trsv<G, NU, U, 0>(C, F, true, t, t, dfw, sx.as<double>(), RhsScaleD{scr.as<double>(), F.D.as<double>(), t},
+                                 Fin0<0>{}, gate);
+        launch_rows<G, NU, U, 1, 0>(C, n, t, Eq7FinishBody{Pr.W, sx.as<double>(), h.as<double>(), v.as<double>(), t},
+                                    K2Fin{K, l, cap}, gate);
+        launch_rows<G, NU, U, 1, 0>(C, n, t,
+                                    UpdBody{r.as<double>(), u, v.as<double>(), h.as<double>(), K.alpha, K.active, t},
+                                    K3Fin{K, l}, gate);
+        woodbury<true>(C, Pr, t, r.as<double>(), z.as<double>(), K4Fin{K, l, cap}, gate);
+      }
+      VL_CUDA(cudaMemcpyAsync(status, K.status, sizeof(status), cudaMemcpyDeviceToHost, C.stream));
+      VL_CUDA(cudaStreamSynchronize(C.stream));
+      if (status[1] != 0 || status[0] == 0) break;
+      chunk = std::min(chunk * 2, 16);
+    }
+  });
+  if (status[1] != 0) {
+    double ev = 0;
+    VL_CUDA(cudaMemcpy(&ev, K.errval, sizeof(double), cudaMemcpyDeviceToHost));
+    char buf[200];
+    snprintf(buf, sizeof(buf), "CG breakdown in column %d: curvature %.3e <= 0", status[2], ev);
+    fail(kEBreakdown, buf);
+  }
+  if (out) {
+    out->iters.assign(t, 0);
+    out->converged.assign(t, 0);
+    out->res.assign(t, 0.0);
+    VL_CUDA(cudaMemcpyAsync(out->iters.data(), K.iters, sizeof(int) * t, cudaMemcpyDeviceToHost, C.stream));
+    VL_CUDA(cudaMemcpyAsync(out->converged.data(), K.conv, sizeof(int) * t, cudaMemcpyDeviceToHost, C.stream));
+    VL_CUDA(cudaMemcpyAsync(out->res.data(), K.res, sizeof(double) * t, cudaMemcpyDeviceToHost, C.stream));
+    VL_CUDA(cudaStreamSynchronize(C.stream));
+    int mx = 0;
+    for (int c = 0; c < t; ++c) mx = std::max(mx, out->iters[c]);
+    out->max_iters = mx;
+    if (capture && mx > 0) {
+      out->alpha.assign((size_t)mx * t, 0.0);
+      out->beta.assign((size_t)mx * t, 0.0);
+      VL_CUDA(cudaMemcpy(out->alpha.data(), K.ah, sizeof(double) * mx * t, cudaMemcpyDeviceToHost));
+      VL_CUDA(cudaMemcpy(out->beta.data(), K.bh, sizeof(double) * mx * t, cudaMemcpyDeviceToHost));
+    }
+  }
+}
+
+namespace {
+struct SumLogWBody {
+  const double* W;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int, int, double (&acc)[NR][NU * U]) const {
+    if (valid) acc[0][0] += log(W[s]);
+  }
+};
+struct CopySum1 {
+  double* dst;
+  VL_D void operator()(const double* sums, int) const {
+    if (threadIdx.x == 0) dst[0] = sums[0];
+  }
+};
+struct ProbeZLBody {  // Z = sqrt(1/W) o Gn + ZL ; (ZL already = L Gk)
+  const double* W;
+  const double* Gn;
+  double* Z;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&)[NR][NU * U]) const {
+    if (!valid) return;
+    double g[NU * U], z[NU * U];
+    load_row<G, NU, U>(Gn, ld, s, gl, t, g);
+    load_row<G, NU, U>(Z, ld, s, gl, t, z);
+    const double se = sqrt(1.0 / W[s]);
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) z[i] = se * g[i] + z[i];
+    store_row<G, NU, U>(Z, ld, s, gl, t, z);
+  }
+};
+struct DotZVBody {
+  const double* Z;
+  const double* V;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    if (!valid) return;
+    double a[NU * U], b[NU * U];
+    load_row<G, NU, U>(Z, ld, s, gl, t, a);
+    load_row<G, NU, U>(V, ld, s, gl, t, b);
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) acc[0][i] += a[i] * b[i];
+  }
+};
+template <int NRv>
+struct CopySumsL {
+  double* dst;
+  VL_D void operator()(const double* sums, int t) const {
+    for (int i = threadIdx.x; i < NRv * t; i += blockDim.x) dst[i] = sums[i];
+  }
+};
+}  // namespace
+
+double lrac_sumlogW(Ctx& C, int64_t n, const double* W) {
+  double* d = C.dev_scalars.as<double>();
+  launch_rows<1, 1, 1, 1, 0>(C, n, 1, SumLogWBody{W}, CopySum1{d});
+  double h;
+  VL_CUDA(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+  return h;
+}
+
+// Z = sqrt(e) o Gn + L Gk (preconditioners.py:204-207), V = P^-1 Z, w_c = z_c . v_c
+void lrac_probes(Ctx& C, const LracPrec& Pr, int t, const double* Gn, const double* Gk, double* Z, double* V,
+                 double* w_host) {
+  const int64_t n = Pr.F->pat->n;
+  const int k = Pr.LF->keff, kl = Pr.LF->k;
+  ProfScope ps(C, "lrac_probes", 0.0);
+  if (k > 0) {
+    const double one = 1.0, zero = 0.0;
+    blas_ok(cublasDgemm(blas(C), CUBLAS_OP_N, CUBLAS_OP_N, t, (int)n, k, &one, Gk, t, Pr.LF->L.as<double>(), kl,
+                        &zero, Z, t),
+            "dgemm L Gk");
+  } else {
+    VL_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * (size_t)n * t, C.stream));
+  }
+  double* sums = C.dev_scalars.as<double>();
+  dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
+    constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
+    launch_rows<G, NU, U, 0, 0>(C, n, t, ProbeZLBody{Pr.W, Gn, Z, t}, Fin0<0>{});
+  });
+  lrac_apply_inv(C, Pr, t, Z, V);
+  dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
+    constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
+    launch_rows<G, NU, U, 1, 0>(C, n, t, DotZVBody{Z, V, t}, CopySumsL<1>{sums});
+  });
+  VL_CUDA(cudaMemcpyAsync(w_host, sums, sizeof(double) * t, cudaMemcpyDeviceToHost, C.stream));
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+}
+
+// ---------------------------------------------------------------------------
+// Gradient pieces (laplace.py:369-386 _lrac_dL, 421-431 LRAC mu-derivative,
+// 527-533 LRAC dP_trace / dP_op, eq7 dA_op = -SigmaTilde dQ SigmaTilde)
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void colnorm2_kernel(int64_t n, int k, int ldk, const double* __restrict__ Y, double* __restrict__ g2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double* c = Y + i * ldk;
+    double s = 0.0;
+    for (int l = 0; l < k; ++l) s += c[l] * c[l];
+    g2[i] = s;
+  }
+}
+
+// dS[i][q] = d Sigma(x_i, x_piv_q) / d rho   (n x k row-major, lda kl)
+__global__ void dsigma_kernel(int64_t n, int dim, int k, int kl, const double* __restrict__ xy,
+                              const int32_t* __restrict__ piv_s, MaternK K, double* __restrict__ dS) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * k; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / k;
+    const int q = (int)(e % k);
+    const int64_t p = piv_s[q];
+    double r2 = 0.0;
+    for (int a = 0; a < dim; ++a) {
+      const double df = xy[i * dim + a] - xy[p * dim + a];
+      r2 += df * df;
+    }
+    const double r = sqrt(r2);
+    double v;
+    if (K.nu == 0) {
+      const double u = r / K.rho;
+      v = K.s2 * exp(-u) * u / K.rho;
+    } else {
+      const double u = K.c * r;
+      v = (K.nu == 1) ? K.s2 * u * u * exp(-u) / K.rho : K.s2 * u * u * (1.0 + u) * exp(-u) / (3.0 * K.rho);
+    }
+    dS[i * kl + q] = v;
+  }
+}
+
+// rows at the pivots: out (k x k, column-major, ld k): out[a + b*k] = src[piv_a][b]
+__global__ void gather_piv_rows_kernel(int k, int kl, const int32_t* __restrict__ piv_s, const double* __restrict__ src,
+                                       double* __restrict__ out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * k; e += gridDim.x * blockDim.x) {
+    const int a = e % k, b = e / k;
+    out[a + (size_t)b * k] = src[(int64_t)piv_s[a] * kl + b];
+  }
+}
+
+// Phi = tril(X, -1) + 0.5 diag(X) in place (column-major)
+__global__ void phi_kernel(int k, double* X) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * k; e += gridDim.x * blockDim.x) {
+    const int a = e % k, b = e / k;
+    if (a < b) X[e] = 0.0;
+    else if (a == b) X[e] *= 0.5;
+  }
+}
+
+__global__ void diag_sum_kernel(int k, const double* __restrict__ A, double* out) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) s += A[(size_t)i * k + i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int i = 0; i < (int)blockDim.x; ++i) a += sh[i];
+    *out = a;
+  }
+}
+
+template <int G>
+VL_D double gsum_l(double v) {
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// LRAC mu-derivative (laplace.py:421-431): H = U V / W^2, R = (V/W)^2, per-row
+// control variate c; s = 0.5 md3 (1/W + c (G2 - 1/W) - mean(H - c R)).
+// Column sums for the xi STE: h_xi = -sum m3/W^2 U V, r_xi = -sum m3/W^2 V^2.
+template <bool XI>
+struct LracMuBody {
+  const double* U_;
+  const double* V_;
+  const double* W;
+  const double* G2;
+  const double* d3;
+  const double* md3x;
+  double* s_out;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    constexpr int NC = NU * U;
+    double us[NC], vs[NC], H[NC], R[NC];
+    load_row<G, NU, U>(U_, ld, valid ? s : 0, gl, valid ? t : 0, us);
+    load_row<G, NU, U>(V_, ld, valid ? s : 0, gl, valid ? t : 0, vs);
+    const double w = valid ? W[s] : 1.0;
+    double sh = 0.0, sr = 0.0;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int c = vl::Cols<G, NU, U>::col(gl, i);
+      const bool on = valid && c < t;
+      H[i] = on ? us[i] * vs[i] / (w * w) : 0.0;
+      const double vw = vs[i] / w;
+      R[i] = on ? vw * vw : 0.0;
+      sh += H[i];
+      sr += R[i];
+    }
+    sh = gsum_l<G>(sh);
+    sr = gsum_l<G>(sr);
+    const double hm = sh / t, rm = sr / t;
+    double svr = 0.0, scv = 0.0;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int c = vl::Cols<G, NU, U>::col(gl, i);
+      if (valid && c < t) {
+        svr += (R[i] - rm) * (R[i] - rm);
+        scv += (H[i] - hm) * (R[i] - rm);
+      }
+    }
+    svr = gsum_l<G>(svr);
+    scv = gsum_l<G>(scv);
+    double cw = 0.0;
+    if (t >= 2) {
+      const double vr = svr / (t - 1), cv = scv / (t - 1);
+      cw = (vr >= 1e-300) ? cv / vr : 0.0;
+    }
+    double sm = 0.0;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int c = vl::Cols<G, NU, U>::col(gl, i);
+      if (valid && c < t) sm += H[i] - cw * R[i];
+    }
+    sm = gsum_l<G>(sm);
+    if (!valid) return;
+    if (gl == 0) {
+      const double exact = 1.0 / w + cw * (G2[s] - 1.0 / w);
+      s_out[s] = 0.5 * ((-d3[s]) * (exact - sm / t));
+    }
+    if constexpr (XI) {
+      const double q = md3x[s] / (w * w);
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        const int c = vl::Cols<G, NU, U>::col(gl, i);
+        if (c >= t) continue;
+        acc[0][i] += -(q * us[i] * vs[i]);
+        acc[1][i] += -(q * vs[i] * vs[i]);
+      }
+    }
+  }
+};
+
+// h_k = -(SigmaTilde u)^T dQ_k (SigmaTilde v): forward-only dQ dot with
+// U' = SigmaTilde U, V' = SigmaTilde V (columns: h_sigma2, h_rho)
+struct DQDotBody {
+  BView B;
+  const double* dval;
+  const double* U_;
+  const double* V_;
+  const double* D;
+  const double* dDs;
+  const double* dDr;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    constexpr int NC = NU * U;
+    if (!valid) return;
+    double BU[NC], BV[NC], dBU[NC], dBV[NC], us[NC], vs[NC];
+    zero(BU);
+    zero(BV);
+    zero(dBU);
+    zero(dBV);
+    gather_B<G, NU, U>(B, B.val, s, true, gl, t, LoadU<U>{U_, ld}, BU);
+    gather_B<G, NU, U>(B, B.val, s, true, gl, t, LoadU<U>{V_, ld}, BV);
+    gather_B<G, NU, U>(B, dval, s, true, gl, t, LoadU<U>{U_, ld}, dBU);
+    gather_B<G, NU, U>(B, dval, s, true, gl, t, LoadU<U>{V_, ld}, dBV);
+    load_row<G, NU, U>(U_, ld, s, gl, t, us);
+    load_row<G, NU, U>(V_, ld, s, gl, t, vs);
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      BU[i] += us[i];
+      BV[i] += vs[i];
+    }
+    const double Dinv = 1.0 / D[s];
+    const double qs = dDs[s] * Dinv * Dinv, qr = dDr[s] * Dinv * Dinv;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int c = vl::Cols<G, NU, U>::col(gl, i);
+      if (c >= t) continue;
+      acc[0][i] += (BU[i] * qs * BV[i]);  // -(-qs ...) : h = -(u'^T dQ v')
+      acc[1][i] += -((dBU[i] * BV[i] + BU[i] * dBV[i]) * Dinv - BU[i] * qr * BV[i]);
+    }
+  }
+};
+
+}  // namespace
+
+// out: s (n, device); hcols (2 x t: h_s2, h_rho), rcols (2 x t: r_s2, r_rho),
+// dPt (2); with md3x: xih (t), xir (t), xi_scalars [sum G2 m3, sum m3 / W]
+void lrac_grad(Ctx& C, const LracPrec& Pr, int t, const double* U, const double* V, const double* d3,
+               const double* md3x, double* s_out, double* hcols, double* rcols, double* dPt, double* xicols,
+               double* xis) {
+  const Factor& F = *Pr.F;
+  const Pattern& P = *F.pat;
+  const int64_t n = P.n;
+  const int k = Pr.LF->keff, kl = Pr.LF->k;
+  if (!F.has_grad) fail(kEConfig, "factor was built without gradient");
+  ProfScope ps(C, "lrac_grad", 0.0);
+  cublasHandle_t hb = blas(C);
+  const double one = 1.0, zero = 0.0, mone = -1.0;
+  // G2 = diag(L M^-1 L^T) = column norms of Lm^-1 L^T
+  DevBuf Y, G2;
+  Y.alloc(sizeof(double) * (size_t)n * kl);
+  G2.alloc(sizeof(double) * n);
+  if (k > 0) {
+    VL_CUDA(cudaMemcpyAsync(Y.p, Pr.LF->L.p, sizeof(double) * (size_t)n * kl, cudaMemcpyDeviceToDevice, C.stream));
+    blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, k, (int)n,
+                        &one, Pr.Lm.as<double>(), k, Y.as<double>(), kl),
+            "trsm G2");
+    colnorm2_kernel<<<C.num_sms * 4, 256, 0, C.stream>>>(n, k, kl, Y.as<double>(), G2.as<double>());
+  } else {
+    VL_CUDA(cudaMemsetAsync(G2.p, 0, sizeof(double) * n, C.stream));
+  }
+  double* sums = C.dev_scalars.as<double>();
+  dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
+    constexpr int G_ = decltype(g)::value, NU = decltype(nu)::value, U_ = decltype(uu)::value;
+    if (md3x)
+      launch_rows<G_, NU, U_, 2, 0>(C, n, t, LracMuBody<true>{U, V, Pr.W, G2.as<double>(), d3, md3x, s_out, t},
+                                    CopySumsL<2>{sums});
+    else
+      launch_rows<G_, NU, U_, 0, 0>(C, n, t, LracMuBody<false>{U, V, Pr.W, G2.as<double>(), d3, nullptr, s_out, t},
+                                    Fin0<0>{});
+  });
+  if (md3x) {
+    VL_CUDA(cudaMemcpyAsync(xicols, sums, sizeof(double) * 2 * t, cudaMemcpyDeviceToHost, C.stream));
+    VL_CUDA(cudaStreamSynchronize(C.stream));
+  }
+  // h via SigmaTilde U, SigmaTilde V and the forward-only dQ dot
+  DevBuf SU, SV, scr;
+  SU.alloc(sizeof(double) * (size_t)n * t);
+  SV.alloc(sizeof(double) * (size_t)n * t);
+  scr.alloc(sizeof(double) * (size_t)n * t);
+  apply_sigma_tilde(C, F, t, U, SU.as<double>(), scr.as<double>());
+  apply_sigma_tilde(C, F, t, V, SV.as<double>(), scr.as<double>());
+  BView Bv = bview(F, false);
+  dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
+    constexpr int G_ = decltype(g)::value, NU = decltype(nu)::value, U_ = decltype(uu)::value;
+    launch_rows<G_, NU, U_, 2, 0>(C, n, t,
+                                  DQDotBody{Bv, F.dval.as<double>(), SU.as<double>(), SV.as<double>(), F.D.as<double>(),
+                                            F.dD_sig.as<double>(), F.dD_rho.as<double>(), t},
+                                  CopySumsL<2>{sums});
+  });
+  VL_CUDA(cudaMemcpyAsync(hcols, sums, sizeof(double) * 2 * t, cudaMemcpyDeviceToHost, C.stream));
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+  if (k == 0) {
+    for (int i = 0; i < 2 * t; ++i) rcols[i] = 0.0;
+    dPt[0] = dPt[1] = 0.0;
+    return;
+  }
+  // A1 = L^T V (k x t)
+  DevBuf A1, A2;
+  A1.alloc(sizeof(double) * (size_t)k * t);
+  A2.alloc(sizeof(double) * (size_t)k * t);
+  blas_ok(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, k, t, (int)n, &one, Pr.LF->L.as<double>(), kl, V, t, &zero,
+                      A1.as<double>(), k),
+          "A1");
+  std::vector<double> a1((size_t)k * t), a2((size_t)k * t);
+  VL_CUDA(cudaMemcpyAsync(a1.data(), A1.p, sizeof(double) * a1.size(), cudaMemcpyDeviceToHost, C.stream));
+  // --- sigma2: dL = L / (2 sigma2): r = 2 (L^T v).(dL^T v) = (L^T v)^2 / sigma2 ;
+  //     dPt = 2 tr(M^-1 L^T W L) / (2 sigma2) = (k - tr M^-1) / sigma2
+  DevBuf Minv, tr;
+  Minv.alloc(sizeof(double) * (size_t)k * k);
+  tr.alloc(64);
+  {
+    std::vector<double> I((size_t)k * k, 0.0);
+    for (int i = 0; i < k; ++i) I[(size_t)i * k + i] = 1.0;
+    VL_CUDA(cudaMemcpyAsync(Minv.p, I.data(), sizeof(double) * I.size(), cudaMemcpyHostToDevice, C.stream));
+    blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, k, k, &one,
+                        Pr.Lm.as<double>(), k, Minv.as<double>(), k),
+            "minv1");
+    blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, k, k, &one,
+                        Pr.Lm.as<double>(), k, Minv.as<double>(), k),
+            "minv2");
+    diag_sum_kernel<<<1, 256, 0, C.stream>>>(k, Minv.as<double>(), tr.as<double>());
+  }
+  double trMinv = 0.0;
+  VL_CUDA(cudaMemcpyAsync(&trMinv, tr.p, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+  for (int c = 0; c < t; ++c) {
+    double s = 0.0;
+    for (int l = 0; l < k; ++l) s += a1[(size_t)c * k + l] * a1[(size_t)c * k + l];
+    rcols[c] = s / Pr.F->sigma2;
+  }
+  dPt[0] = ((double)k - trMinv) / Pr.F->sigma2;
+  // --- rho: dL = (dS - L dR^T) R^-T, dR = R Phi(R^-1 dS_pp R^-T), R = L[piv]
+  const MaternK Km = make_matern(F);
+  DevBuf dS, R, X, dR;
+  dS.alloc(sizeof(double) * (size_t)n * kl);
+  R.alloc(sizeof(double) * (size_t)k * k);
+  X.alloc(sizeof(double) * (size_t)k * k);
+  dR.alloc(sizeof(double) * (size_t)k * k);
+  dsigma_kernel<<<C.num_sms * 8, 256, 0, C.stream>>>(n, P.d, k, kl, P.xy.as<double>(), Pr.LF->piv_s.as<int32_t>(), Km,
+                                                     dS.as<double>());
+  gather_piv_rows_kernel<<<64, 256, 0, C.stream>>>(k, kl, Pr.LF->piv_s.as<int32_t>(), Pr.LF->L.as<double>(),
+                                                   R.as<double>());
+  gather_piv_rows_kernel<<<64, 256, 0, C.stream>>>(k, kl, Pr.LF->piv_s.as<int32_t>(), dS.as<double>(), X.as<double>());
+  VL_LAUNCH_CHECK();
+  // X = R^-1 dSpp R^-T
+  blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, k, k, &one,
+                      R.as<double>(), k, X.as<double>(), k),
+          "X1");
+  blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, k, k, &one,
+                      R.as<double>(), k, X.as<double>(), k),
+          "X2");
+  phi_kernel<<<64, 256, 0, C.stream>>>(k, X.as<double>());
+  // dR = R Phi
+  blas_ok(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, k, k, k, &one, R.as<double>(), k, X.as<double>(), k, &zero,
+                      dR.as<double>(), k),
+          "dR");
+  // dL^T (k x n col-major view of row-major dL) = R^-1 (dS^T - dR L^T) : work on the (kl x n) views
+  // dS^T - dR L^T  ->  dS view (k x n, ld kl) -= dR (k x k) * L view (k x n, ld kl)
+  blas_ok(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, k, (int)n, k, &mone, dR.as<double>(), k, Pr.LF->L.as<double>(), kl,
+                      &one, dS.as<double>(), kl),
+          "dS - dR L^T");
+  blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, k, (int)n, &one,
+                      R.as<double>(), k, dS.as<double>(), kl),
+          "dL");
+  // now dS holds dL (row-major n x k, ld kl).  A2 = dL^T V
+  blas_ok(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, k, t, (int)n, &one, dS.as<double>(), kl, V, t, &zero,
+                      A2.as<double>(), k),
+          "A2");
+  // T1 = L^T (W o dL) (k x k): scale dL rows by W into scr-sized buffer, GEMM
+  DevBuf WdL, T1, MT;
+  WdL.alloc(sizeof(double) * (size_t)n * kl);
+  T1.alloc(sizeof(double) * (size_t)k * k);
+  MT.alloc(sizeof(double) * (size_t)k * k);
+  // W o dL = sqrt(W) o (sqrt(W) o dL)   (W > 0 is guaranteed for LRAC)
+  scale_rows_kernel<<<C.num_sms * 8, 256, 0, C.stream>>>(n, kl, Pr.W, dS.as<double>(), WdL.as<double>());
+  scale_rows_kernel<<<C.num_sms * 8, 256, 0, C.stream>>>(n, kl, Pr.W, WdL.as<double>(), WdL.as<double>());
+  // T1 (k x k) = Lv (k x n) * WdLv^T (n x k)
+  blas_ok(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, k, k, (int)n, &one, Pr.LF->L.as<double>(), kl, WdL.as<double>(), kl,
+                      &zero, T1.as<double>(), k),
+          "T1");
+  // tr(M^-1 T1) = sum_ij Minv_ij T1_ji
+  blas_ok(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, k, k, k, &one, Minv.as<double>(), k, T1.as<double>(), k, &zero,
+                      MT.as<double>(), k),
+          "MT");
+  diag_sum_kernel<<<1, 256, 0, C.stream>>>(k, MT.as<double>(), tr.as<double>());
+  double trMT = 0.0;
+  VL_CUDA(cudaMemcpyAsync(&trMT, tr.p, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  VL_CUDA(cudaMemcpyAsync(a2.data(), A2.p, sizeof(double) * a2.size(), cudaMemcpyDeviceToHost, C.stream));
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+  dPt[1] = 2.0 * trMT;
+  for (int c = 0; c < t; ++c) {
+    double s = 0.0;
+    for (int l = 0; l < k; ++l) s += a1[(size_t)c * k + l] * a2[(size_t)c * k + l];
+    rcols[t + c] = 2.0 * s;
+  }
+  if (md3x && xis) {
+    // xi dP_trace pieces: sum G2 m3, sum m3 / W (host sums over device arrays)
+    std::vector<double> g2h(n), mh(n), wh(n);
+    VL_CUDA(cudaMemcpyAsync(g2h.data(), G2.p, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
+    VL_CUDA(cudaMemcpyAsync(mh.data(), md3x, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
+    VL_CUDA(cudaMemcpyAsync(wh.data(), Pr.W, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
+    VL_CUDA(cudaStreamSynchronize(C.stream));
+    double a = 0.0, b = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      a += g2h[i] * mh[i];
+      b += mh[i] / wh[i];
+    }
+    xis[0] = a;
+    xis[1] = b;
+  }
+}
+
+void lrac_solve_system(Ctx& C, const LracPrec& Pr, int t, const double* rhs, double* u, double tol, int max_iter,
+                       PcgResult* out) {
+  const int64_t n = Pr.F->pat->n;
+  DevBuf srhs, scr, us;
+  srhs.alloc(sizeof(double) * (size_t)n * t);
+  scr.alloc(sizeof(double) * (size_t)n * t);
+  us.alloc(sizeof(double) * (size_t)n * t);
+  apply_sigma_tilde(C, *Pr.F, t, rhs, srhs.as<double>(), scr.as<double>());
+  pcg_lrac(C, Pr, t, srhs.as<double>(), us.as<double>(), tol, max_iter, false, out);
+  dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
+    constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
+    launch_rows<G, NU, U, 0, 0>(C, n, t, DivWBody{Pr.W, us.as<double>(), u, t}, Fin0<0>{});
+  });
+}
+
+}  // namespace vl

@@ -1,0 +1,55 @@
+// LRAC preconditioner (preconditioners.py:167-214, 288-320; laplace.py:118-153)
+// and the eq7 system  A = SigmaTilde + W^-1  (laplace.py:156-182).
+#pragma once
+
+#include <vector>
+
+#include "context.h"
+#include "pcg.h"
+
+namespace vl {
+
+// Rank-k pivoted Cholesky of the exact covariance, kept with the factor
+// (theta-only, laplace.py:128-136).  L: n x k row-major, storage order.
+struct LracFactor {
+  int k = 0, keff = 0;
+  DevBuf L;                 // n x k
+  std::vector<int32_t> piv_f;  // pivots, factor order
+  DevBuf piv_s;             // pivots, storage order
+};
+
+// Woodbury pieces for one W: M = I + L^T diag(W) L = Lm Lm^T.
+struct LracPrec {
+  const Factor* F = nullptr;
+  const LracFactor* LF = nullptr;
+  const double* W = nullptr;
+  DevBuf Lm;                // k x k column-major lower Cholesky factor of M
+  double logdetM = 0.0;
+  double sumlogW = 0.0;
+};
+
+void lrac_pchol(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol);
+void lrac_prepare(Ctx& C, const Factor& F, const LracFactor& LF, const double* W, LracPrec& P);
+// z = P^-1 r for t columns (n x t)
+void lrac_apply_inv(Ctx& C, const LracPrec& P, int t, const double* r, double* z);
+// PCG on (SigmaTilde + W^-1) U = Bm  (iterative.py:104-178 per column)
+void pcg_lrac(Ctx& C, const LracPrec& P, int t, const double* b, double* u, double tol, int max_iter, bool capture,
+              PcgResult* out);
+// y = SigmaTilde x = B^-1 (D o B^-T x)  (vecchia.py:185-192), t columns
+void apply_sigma_tilde(Ctx& C, const Factor& F, int t, const double* x, double* y, double* scratch);
+// u = (W + SigmaTilde^-1)^-1 rhs via the eq7 form (laplace.py:176-179)
+void lrac_solve_system(Ctx& C, const LracPrec& P, int t, const double* rhs, double* u, double tol, int max_iter,
+                       PcgResult* out);
+
+void lrac_free_handles();
+// LRAC gradient pieces (laplace.py:369-436, 493-576 eq7 with the LRAC preconditioner):
+// s (n, device) = 0.5 dlogdet/dmu; host: hcols/rcols (2 x t: sigma2, rho), dPt (2);
+// with md3x (gamma): xicols (2 x t: h_xi, r_xi), xis = [sum G2 m3, sum m3 / W].
+void lrac_grad(Ctx& C, const LracPrec& Pr, int t, const double* U, const double* V, const double* d3,
+               const double* md3x, double* s_out, double* hcols, double* rcols, double* dPt, double* xicols,
+               double* xis);
+double lrac_sumlogW(Ctx& C, int64_t n, const double* W);
+void lrac_probes(Ctx& C, const LracPrec& Pr, int t, const double* Gn, const double* Gk, double* Z, double* V,
+                 double* w_host);
+
+}  // namespace vl

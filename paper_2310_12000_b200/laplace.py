@@ -25,7 +25,12 @@ from .iterative import (CG_MAX_ITER_DEFAULT, CG_TOL_DEFAULT, ProbeSet, slq_from_
 
 MODE_CG_TOL_CAP = 1e-4
 EQ5_VARIANTS = ("lrac", "l2")
-SUPPORTED_PRECONDITIONERS = ("vadu", "l1")
+SUPPORTED_PRECONDITIONERS = ("vadu", "l1", "lrac")
+
+
+def default_rank(n):
+    """Default low-rank size: 200 scaled by n/1e4, clamped to [20, 200] (preconditioners.py:390-392)."""
+    return int(np.clip(np.ceil(200 * min(1.0, n / 1e4)), 20, 200))
 
 
 @dataclass(frozen=True)
@@ -69,8 +74,52 @@ def _check_supported(cfg):
     if cfg.preconditioner not in SUPPORTED_PRECONDITIONERS:
         raise CapabilityError(f"preconditioner {cfg.preconditioner!r} is not available on the device backend "
                               f"(supported: {', '.join(SUPPORTED_PRECONDITIONERS)})")
-    if cfg.resolved_split() != "eq6":
-        raise CapabilityError("the VADU device path uses the eq6 log-determinant split")
+    want = "eq7" if cfg.preconditioner == "lrac" else "eq6"
+    if cfg.resolved_split() != want:
+        raise CapabilityError(f"the device {cfg.preconditioner} path uses the {want} log-determinant split")
+
+
+class LracFactorHandle:
+    """Rank-k pivoted Cholesky of the exact covariance, cached on the factor
+    like the reference's factor.cache[("sigma_pchol", k)] (laplace.py:128-136)."""
+
+    def __init__(self, factor, k, tol=0.0):
+        self.factor = factor
+        self.k = int(k)
+        piv = np.zeros(self.k, dtype=np.int32)
+        keff = C.c_int(0)
+        h = C.c_void_p()
+        _lib.call("vl_lrac_create", factor.ctx.h, factor.h, self.k, float(tol), C.byref(h), _lib.ptr(piv),
+                  C.byref(keff))
+        self.h = h
+        self.keff = int(keff.value)
+        self.pivots = piv[: self.keff].astype(int)
+
+    def L(self):
+        """L (n x k) in factor order (numpy)."""
+        f = self.factor
+        out = np.empty((f.n, self.k))
+        _lib.call("vl_lrac_get_L", f.ctx.h, self.h, _lib.ptr(out))
+        res = np.empty_like(out)
+        res[f.pattern.sperm] = out
+        return res[:, : self.keff]
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                _lib.lib().vl_lrac_destroy(self.h)
+        except Exception:
+            pass
+
+
+def lrac_factor(factor, cfg):
+    k = cfg.rank if cfg.rank is not None else default_rank(factor.n)
+    key = ("sigma_pchol", int(k))
+    lf = factor.cache.get(key)
+    if lf is None:
+        lf = LracFactorHandle(factor, k)
+        factor.cache[key] = lf
+    return lf
 
 
 class LaplaceState:
@@ -153,9 +202,15 @@ def find_mode(factor, lik, y, F, cfg, trace=None):
                           float(cfg.newton_grad_tol), float(cfg.newton_obj_tol))
     out = (C.c_double * 8)()
     cg_its = np.zeros(max(cfg.newton_max_iter, 1), dtype=np.int32)
-    st = _lib.lib().vl_find_mode(ctx.h, factor.h, C.byref(lk), C.byref(nc), _lib.ptr(y_d), _lib.ptr(F_d),
-                                 _lib.ptr(b), _lib.ptr(W), _lib.ptr(d1), _lib.ptr(d3), out,
-                                 _lib.ptr(cg_its), int(cg_its.size))
+    if cfg.preconditioner == "lrac":
+        lf = lrac_factor(factor, cfg)
+        st = _lib.lib().vl_find_mode_lrac(ctx.h, factor.h, lf.h, C.byref(lk), C.byref(nc), _lib.ptr(y_d),
+                                          _lib.ptr(F_d), _lib.ptr(b), _lib.ptr(W), _lib.ptr(d1), _lib.ptr(d3), out,
+                                          _lib.ptr(cg_its), int(cg_its.size))
+    else:
+        st = _lib.lib().vl_find_mode(ctx.h, factor.h, C.byref(lk), C.byref(nc), _lib.ptr(y_d), _lib.ptr(F_d),
+                                     _lib.ptr(b), _lib.ptr(W), _lib.ptr(d1), _lib.ptr(d3), out,
+                                     _lib.ptr(cg_its), int(cg_its.size))
     state = LaplaceState(pat, {"b": b, "W": W, "d1": d1, "d3": d3, "y": y_d, "F": F_d}, y, F,
                          out[0], out[1], out[2], int(out[4]), bool(out[5]), cg_its[: int(out[6])].tolist())
     if trace is not None:
@@ -189,8 +244,59 @@ class VaduPreconditioner:
         return float(self.sums()[1])
 
 
+class LracPreconditioner:
+    """P = L L^T + diag(1/W) on the device (preconditioners.py:167-214)."""
+
+    name = "lrac"
+
+    def __init__(self, factor, W_dev, lf):
+        self.factor = factor
+        self.W_dev = W_dev
+        self.lf = lf
+        out = np.zeros(2)
+        h = C.c_void_p()
+        _lib.call("vl_lrac_prepare", factor.ctx.h, lf.h, _lib.ptr(W_dev), C.byref(h), _lib.ptr(out))
+        self.h = h
+        self.logdet_M = float(out[0])
+        self.sumlogW = float(out[1])
+        self.pivots = lf.pivots
+        self._sums = None
+
+    def logdet(self):
+        return -self.sumlogW + self.logdet_M
+
+    @property
+    def k(self):
+        return self.lf.keff
+
+    @property
+    def U(self):
+        return self.lf.L()
+
+    def sums(self):
+        if self._sums is None:
+            out = np.zeros(6)
+            _lib.call("vl_factor_sums", self.factor.ctx.h, self.factor.h, _lib.ptr(self.W_dev), _lib.ptr(out))
+            self._sums = out
+        return self._sums
+
+    def solve_dev(self, r_dev):
+        z = dev.empty(self.factor.ctx, *r_dev.shape)
+        _lib.call("vl_lrac_apply_inv", self.factor.ctx.h, self.h, int(r_dev.shape[1]), _lib.ptr(r_dev), _lib.ptr(z))
+        return z
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                _lib.lib().vl_lracw_destroy(self.h)
+        except Exception:
+            pass
+
+
 def build_preconditioner(factor, W_dev, cfg):
     _check_supported(cfg)
+    if cfg.preconditioner == "lrac":
+        return LracPreconditioner(factor, W_dev, lrac_factor(factor, cfg))
     return VaduPreconditioner(factor, W_dev, cfg.preconditioner)
 
 
@@ -216,9 +322,39 @@ def base_normals(factor, seed, t, cols=None):
     return Gd
 
 
+def _lrac_normals(factor, seed, t, k, cols=None):
+    """LRAC sample_block draws (preconditioners.py:204-207): g_n (n x t) then
+    g_k (k x t) from one default_rng(seed) stream; cached on the device."""
+    pat = factor.pattern
+    key = ("lrac", seed, t, k, cols)
+    for ent in _G_CACHE:
+        if ent[0] is pat and ent[1] == key:
+            return ent[2]
+    rng = np.random.default_rng(seed)
+    Gn = rng.standard_normal((factor.n, t))
+    Gk = rng.standard_normal((k, t))
+    if cols is not None:
+        Gn, Gk = Gn[:, cols[0]:cols[1]], Gk[:, cols[0]:cols[1]]
+    val = (pat.to_dev(np.ascontiguousarray(Gn)), dev.upload(factor.ctx, np.ascontiguousarray(Gk)))
+    _G_CACHE.append((pat, key, val))
+    del _G_CACHE[:-2]
+    return val
+
+
 def make_probes(factor, state, cfg, cols=None):
     """Fresh N(0, P) probes for the current mode, deterministic in the seed."""
     P = build_preconditioner(factor, state._dev["W"], cfg)
+    if cfg.preconditioner == "lrac":
+        Gn, Gk = _lrac_normals(factor, cfg.probe_seed, cfg.t, P.k, cols)
+        t = int(Gn.shape[1])
+        Z = dev.empty(factor.ctx, factor.n, t)
+        V = dev.empty(factor.ctx, factor.n, t)
+        w = np.zeros(t)
+        _lib.call("vl_lrac_probes", factor.ctx.h, P.h, t, _lib.ptr(Gn), _lib.ptr(Gk), _lib.ptr(Z), _lib.ptr(V),
+                  _lib.ptr(w))
+        ps = ProbeSet(Z, cfg.probe_seed, P.name, pattern=factor.pattern, psolves_dev=V, weights=w,
+                      shard=(0 if cols is None else cols[0], cfg.t))
+        return ps, P
     G = base_normals(factor, cfg.probe_seed, cfg.t, cols)
     t = int(G.shape[1])
     Z = dev.empty(factor.ctx, factor.n, t)
@@ -259,20 +395,31 @@ def _run_probe_solves(factor, state, P, cfg, probes):
     res = np.zeros(t)
     al = np.zeros((max(cap, 1), t))
     be = np.zeros((max(cap, 1), t))
-    _lib.call("vl_pcg_vadu", factor.ctx.h, factor.h, _lib.ptr(state._dev["W"]), t, _lib.ptr(probes.Z_dev),
-              _lib.ptr(U), float(cfg.mode_cg_tol), int(cfg.cg_max_iter), 1, _lib.ptr(its), _lib.ptr(conv),
-              _lib.ptr(res), _lib.ptr(al), _lib.ptr(be), max(cap, 1))
+    if cfg.preconditioner == "lrac":
+        _lib.call("vl_lrac_pcg", factor.ctx.h, P.h, t, _lib.ptr(probes.Z_dev), _lib.ptr(U), float(cfg.mode_cg_tol),
+                  int(cfg.cg_max_iter), 1, _lib.ptr(its), _lib.ptr(conv), _lib.ptr(res), _lib.ptr(al), _lib.ptr(be),
+                  max(cap, 1))
+    else:
+        _lib.call("vl_pcg_vadu", factor.ctx.h, factor.h, _lib.ptr(state._dev["W"]), t, _lib.ptr(probes.Z_dev),
+                  _lib.ptr(U), float(cfg.mode_cg_tol), int(cfg.cg_max_iter), 1, _lib.ptr(its), _lib.ptr(conv),
+                  _lib.ptr(res), _lib.ptr(al), _lib.ptr(be), max(cap, 1))
     probes.solves_dev = U
     probes.iters = its
     probes.tridiags = [tridiag_from_cg(al[:, c], be[:, c], int(its[c])) for c in range(t)]
 
 
-def solve_system(factor, state, rhs_dev, cfg, tol=None):
-    """u = (W + SigmaTilde^-1)^-1 rhs (eq6, VADU) for device rhs (n x k)."""
+def solve_system(factor, state, rhs_dev, cfg, tol=None, P=None):
+    """u = (W + SigmaTilde^-1)^-1 rhs for device rhs (n x k): eq6 with VADU,
+    or the eq7 form with LRAC (laplace.py:168-182)."""
     tol = cfg.cg_tol if tol is None else tol
     k = int(rhs_dev.shape[1])
     u = dev.empty(factor.ctx, factor.n, k)
     its = np.zeros(k, dtype=np.int32)
+    if cfg.preconditioner == "lrac":
+        P = P if P is not None else build_preconditioner(factor, state._dev["W"], cfg)
+        _lib.call("vl_lrac_solve_system", factor.ctx.h, P.h, k, _lib.ptr(rhs_dev), _lib.ptr(u), float(tol),
+                  int(cfg.cg_max_iter), _lib.ptr(its))
+        return u, its
     conv = np.zeros(k, dtype=np.int32)
     res = np.zeros(k)
     _lib.call("vl_pcg_vadu", factor.ctx.h, factor.h, _lib.ptr(state._dev["W"]), k, _lib.ptr(rhs_dev), _lib.ptr(u),
@@ -301,6 +448,8 @@ def logdet_system(factor, state, cfg, probes=None, P=None, comm=None):
     if comm is not None:
         parts = comm.allgather_cols(parts, probes.shard)
     slq = float(sum(parts[i] for i in range(len(parts)))) / len(parts)
+    if cfg.resolved_split() == "eq7":
+        return P.sumlogW + P.logdet() + slq
     sums = P.sums()
     return float(sums[0]) + float(sums[1]) + slq
 
@@ -336,6 +485,8 @@ def gradient(state, factor, lik, X, cfg, probes=None, P=None, comm=None):
     s = dev.empty(ctx, n, 1)
     cols = np.zeros((4, t))
     xicols = np.zeros((2, t))
+    if cfg.preconditioner == "lrac":
+        return _gradient_lrac(state, factor, lik, X, cfg, probes, P, comm, md3x, s)
     if comm is not None and (comm.world > 1 or getattr(comm, "force_split", False)):
         s, cols, xicols = comm.grad_probe_pass(factor, state, probes, md3x)
     else:
@@ -366,6 +517,51 @@ def gradient(state, factor, lik, X, cfg, probes=None, P=None, comm=None):
     dbeta = np.zeros(p)
     if p:
         Xd = pat.to_dev(np.ascontiguousarray(X))
+        _lib.call("vl_grad_dbeta", ctx.h, n, _lib.ptr(dv["d1"]), _lib.ptr(s), _lib.ptr(dv["W"]), _lib.ptr(tvec),
+                  _lib.ptr(Xd), p, _lib.ptr(dbeta))
+    return {"dtheta": dtheta, "dbeta": dbeta, "dxi": dxi}
+
+
+def _gradient_lrac(state, factor, lik, X, cfg, probes, P, comm, md3x, s):
+    """eq7 + LRAC branch of laplace.py:439-580: d logdet/d mu with the LRAC
+    control variate (421-431), dA_op = -SigmaTilde dQ SigmaTilde, ex = 0,
+    dP from d L (369-386, 527-533); xi: ex = sum m3/W, dA = dP = -m3/W^2."""
+    if comm is not None and comm.world > 1:
+        raise CapabilityError("probe-sharded gradients are implemented for the vadu preconditioner only")
+    ctx, n, dv, t = factor.ctx, factor.n, state._dev, probes.t
+    gamma = md3x is not None
+    hcols = np.zeros((2, t))
+    rcols = np.zeros((2, t))
+    dPt = np.zeros(2)
+    xicols = np.zeros((2, t))
+    xis = np.zeros(2)
+    _lib.call("vl_lrac_grad", ctx.h, P.h, t, _lib.ptr(probes.solves_dev), _lib.ptr(probes.psolves_dev),
+              _lib.ptr(dv["d3"]), _lib.ptr(md3x) if gamma else None, _lib.ptr(s), _lib.ptr(hcols),
+              _lib.ptr(rcols), _lib.ptr(dPt), _lib.ptr(xicols), _lib.ptr(xis))
+    tvec, _ = solve_system(factor, state, s, cfg, tol=cfg.mode_cg_tol, P=P)
+    terms = np.zeros(4)
+    _lib.call("vl_grad_scalar_terms", ctx.h, factor.h, _lib.ptr(dv["b"]), _lib.ptr(tvec), _lib.ptr(terms))
+    dtheta = np.empty(2)
+    for k in (0, 1):
+        ste = ste_combine(hcols[k], rcols[k], float(dPt[k]))
+        dtheta[k] = 0.5 * terms[2 * k] + 0.5 * (0.0 + ste) - terms[2 * k + 1]
+    dxi = np.empty(lik.n_xi)
+    if gamma:
+        g3 = np.zeros(3)
+        _lib.call("vl_gamma_xi_terms", ctx.h, factor.h, _lib.ptr(dv["y"]), _lib.ptr(dv["F"]), _lib.ptr(dv["b"]),
+                  _lib.ptr(dv["W"]), _lib.ptr(tvec), _lib.ptr(md3x), _lib.ptr(g3))
+        a = lik.shape
+        dlogp = n * (np.log(a) + 1.0 - digamma(a)) + g3[0]
+        ex = float(xis[1])
+        ste = ste_combine(xicols[0], xicols[1], float(xis[0] - xis[1]))
+        dxi[0] = -dlogp + 0.5 * (ex + ste) + g3[1]
+    X = np.asarray(X, dtype=float)
+    if X.ndim == 1:
+        X = X[:, None]
+    p = X.shape[1]
+    dbeta = np.zeros(p)
+    if p:
+        Xd = factor.pattern.to_dev(np.ascontiguousarray(X))
         _lib.call("vl_grad_dbeta", ctx.h, n, _lib.ptr(dv["d1"]), _lib.ptr(s), _lib.ptr(dv["W"]), _lib.ptr(tvec),
                   _lib.ptr(Xd), p, _lib.ptr(dbeta))
     return {"dtheta": dtheta, "dbeta": dbeta, "dxi": dxi}

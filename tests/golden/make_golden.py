@@ -134,6 +134,8 @@ def main():
     laplace_case("gamma_vadu_n300", 300, seed=15, rho=0.1, m=8, t=6, family="gamma",
                  shape=2.0, nu=0.5)
     laplace_case("logit_lrac_n300", 300, seed=16, rho=0.1, m=8, t=6, precond="lrac", rank=30)
+    laplace_case("gamma_lrac_cov_n300", 300, seed=17, rho=0.1, m=8, t=6, precond="lrac", rank=25,
+                 family="gamma", shape=1.5, nu=2.5, p=2)
     knn_case("knn_n6000_m12", 6000, 12, seed=21, ordering_seed=22)
 
 

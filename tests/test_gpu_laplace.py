@@ -10,6 +10,7 @@ from _golden import LAPLACE_CASES, load, scal, tridiags
 pytestmark = pytest.mark.gpu
 
 VADU_CASES = [c for c in LAPLACE_CASES if "lrac" not in c]
+LRAC_CASES = [c for c in LAPLACE_CASES if "lrac" in c]
 
 
 @pytest.fixture(scope="module")
@@ -116,3 +117,34 @@ def test_sharded_gradient_path_matches_fused(vg):
     finally:
         dist.destroy_process_group()
     np.testing.assert_allclose(got["dtheta"], ref["dtheta"], rtol=1e-10, atol=1e-12)
+
+
+def test_lrac_pivoted_cholesky_matches_oracle(vg):
+    from oracle import vl_oracle as O
+    from paper_2310_12000_b200.laplace import LracFactorHandle
+    g = load("logit_lrac_n300")
+    f, lik, cfg, y, F, X = _setup(vg, g)
+    lf = LracFactorHandle(f, int(g["rank"]))
+    L_o, piv_o = O.pchol_sigma(f.coords, 1.0, float(g["rho"]), 1.5, int(g["rank"]))
+    assert np.array_equal(lf.pivots, piv_o)
+    assert _rel(lf.L(), L_o) <= 1e-10
+
+
+@pytest.mark.parametrize("name", LRAC_CASES)
+def test_lrac_nll_and_gradient_match_reference(vg, name):
+    g = load(name)
+    f, lik, cfg, y, F, X = _setup(vg, g)
+    cfg = vg.BackendConfig(preconditioner="lrac", t=int(g["t"]), probe_seed=int(g["probe_seed"]),
+                           rank=int(g["rank"]))
+    st = vg.find_mode(f, lik, y, F, cfg)
+    assert st.newton_iters == int(g["newton_iters"])
+    assert _rel(st.b, g["b"]) <= 1e-8
+    probes, P = vg.make_probes(f, st, cfg)
+    assert _rel(probes.Z, g["Z"]) <= 1e-8
+    assert P.logdet() == pytest.approx(float(g["logdet_P"]), rel=1e-8)   # W at a mode agreeing to ~1e-8
+    val = vg.neg_marginal_loglik(st, f, cfg, probes=probes, P=P)
+    assert val == pytest.approx(float(g["nll"]), rel=1e-8)
+    grad = vg.gradient(st, f, lik, X, cfg, probes=probes, P=P)
+    np.testing.assert_allclose(grad["dtheta"], g["dtheta"], rtol=1e-7, atol=1e-9)
+    np.testing.assert_allclose(grad["dbeta"], g["dbeta"], rtol=1e-7, atol=1e-9)
+    np.testing.assert_allclose(grad["dxi"], g["dxi"], rtol=1e-7, atol=1e-9)

@@ -40,7 +40,9 @@ def test_evaluation_matches_reference(name):
     st, pr = info["state"], info["probes"]
     assert st.newton_iters == int(g["newton_iters"])
     assert np.abs(st.b - g["b"]).max() <= 1e-10 * max(1.0, np.abs(g["b"]).max())
-    assert np.abs(pr.Z - g["Z"]).max() <= 1e-12 * np.abs(g["Z"]).max()
+    # LRAC probes carry sqrt(1/W) at the mode (b agrees to ~1e-10)
+    ztol = 1e-10 if "lrac" in name else 1e-12
+    assert np.abs(pr.Z - g["Z"]).max() <= ztol * np.abs(g["Z"]).max()
     ref_tri = tridiags(g)
     assert [len(d) for d, _ in pr.tri] == [len(d) for d, _ in ref_tri]
     assert val == pytest.approx(float(g["nll"]), rel=1e-11)
