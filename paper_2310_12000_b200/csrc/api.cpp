@@ -184,6 +184,49 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
     }
     return it;
   };
+  auto slabs = [&](const std::vector<int32_t>& order, const std::vector<uint32_t>& its, bool fwd_dir,
+                   Pattern::Slabs& S) {
+    std::vector<uint32_t> off(std::max<size_t>(its.size(), 1), 0), w(std::max<size_t>(its.size(), 1), 0);
+    int64_t tot = 0;
+    auto deg = [&](int32_t s) { return fwd_dir ? cnt[s] : (tptr[s + 1] - tptr[s]); };
+    for (size_t k = 0; k < its.size(); ++k) {
+      if (its[k] & 0x80000000u) continue;
+      const int32_t c = (int32_t)its[k];
+      int wk = 0;
+      for (int32_t p = c; p < c + 32; ++p)
+        if (order[p] >= 0) wk = std::max(wk, deg(order[p]));
+      off[k] = (uint32_t)tot;
+      w[k] = (uint32_t)wk;
+      tot += wk;
+    }
+    if (tot * 32 > (int64_t)INT32_MAX * 2) fail(kECapacity, "single-RHS slab too large");
+    std::vector<int32_t> idx((size_t)tot * 32, -1), map((size_t)tot * 32, -1);
+    for (size_t k = 0; k < its.size(); ++k) {
+      if (its[k] & 0x80000000u) continue;
+      const int32_t c = (int32_t)its[k];
+      for (int l = 0; l < 32; ++l) {
+        const int32_t s = order[c + l];
+        if (s < 0) continue;
+        const int d = deg(s);
+        for (int e = 0; e < d; ++e) {
+          const size_t q = ((size_t)off[k] + e) * 32 + l;
+          if (fwd_dir) {
+            idx[q] = ell[(size_t)s * P.m + e];
+            map[q] = (int32_t)((int64_t)s * P.m + e);
+          } else {
+            const int32_t pos = tptr[s] + e;
+            idx[q] = tidx[pos];
+            map[q] = tmap[pos];
+          }
+        }
+      }
+    }
+    S.nent = tot * 32;
+    upload(C, S.off, off);
+    upload(C, S.w, w);
+    upload(C, S.idx, idx);
+    upload(C, S.map, map);
+  };
   auto fi = items(fwd, P.fwd_level_ptr, true);
   auto bi = items(bwd, P.bwd_level_ptr, false);
   P.fwd_nitems = (int64_t)fi.size();
@@ -204,6 +247,9 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
   auto bni = items(P.bwdnh_order_h, P.bwdnh_level_ptr, false);
   P.bwdnh_nitems = (int64_t)bni.size();
   upload(C, P.bwdnh_items, bni);
+  slabs(fwd, fi, true, P.fwd_sl);
+  slabs(bwd, bi, false, P.bwd_sl);
+  slabs(P.bwdnh_order_h, bni, false, P.bwdnh_sl);
   VL_CUDA(cudaStreamSynchronize(C.stream));
 }
 
@@ -235,6 +281,7 @@ int vl_ctx_create(int device, void* stream, vl_ctx** out) {
     if (const char* e = std::getenv("VL_THIN_PASSES")) C.thin_passes = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("VL_MIN_THICK")) C.min_thick_levels = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("VL_USE_HEAD")) C.use_head = std::atoi(e) != 0;
+    if (const char* e = std::getenv("VL_USE_SLABS")) C.use_slabs = std::atoi(e) != 0;
     try {
       // NULL selects the legacy default stream (same as torch's default stream)
       C.stream = (cudaStream_t)stream;

@@ -66,6 +66,7 @@ struct Ctx {
   int thin_passes = 0;
   int min_thick_levels = 4;
   // dense head block of the solves (see head.cuh) and its scratch
+  bool use_slabs = true;  // coalesced dependency slabs for the single-RHS solves
   bool use_head = true;
   DevBuf head_Y, head_Xh;
   // debug: per-row completion timestamps of the next triangular solves (n entries)
@@ -120,6 +121,15 @@ struct Pattern {
   DevBuf tptr;      // n+1  int32 children CSR (= CSR of B^T) in storage order
   DevBuf tidx;      // nnz  int32 child storage row
   DevBuf tmap;      // nnz  int32 ELL slot (child*m + k) holding B[child, s]
+  // Coalesced dependency slabs of the light single-RHS items: item k owns
+  // entry columns [off[k], off[k] + w[k]) (w = max deps of its 32 rows);
+  // entry e of lane l sits at (off + e) * 32 + l, idx = dependency storage
+  // row or -1, map = ELL slot of its value in Factor::val or -1.
+  struct Slabs {
+    DevBuf off, w, idx, map;
+    int64_t nent = 0;  // entries (multiple of 32)
+  };
+  Slabs fwd_sl, bwd_sl, bwdnh_sl;
 };
 
 // Factor values at one theta (device resident, storage order).
@@ -136,6 +146,7 @@ struct Factor {
   DevBuf err;     // 4 ints: [code, row(factor idx) ...]
   DevBuf headX;   // H*H  dense B_HH^-1, column-major (head order), lower triangular
   DevBuf headXr;  // H*H  the same, row-major
+  DevBuf sv_fwd, sv_bwd, sv_bwdnh;  // slab values (Pattern::Slabs::map gathered from val)
 };
 
 }  // namespace vl

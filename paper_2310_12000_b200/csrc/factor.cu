@@ -308,6 +308,14 @@ void factor_head_inverse(Ctx& C, Factor& F) {
   if (ev) prof_end(C, ev);
 }
 
+__global__ void slab_values_kernel(int64_t ne, const int32_t* __restrict__ map, const double* __restrict__ val,
+                                   double* __restrict__ sv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ne; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t q = map[i];
+    sv[i] = q >= 0 ? val[q] : 0.0;
+  }
+}
+
 void factor_refresh_transpose(Ctx& C, Factor& F) {
   const Pattern& P = *F.pat;
   if (P.nnz_off > 0) {
@@ -316,6 +324,17 @@ void factor_refresh_transpose(Ctx& C, Factor& F) {
                                                        F.valT.as<double>());
     VL_LAUNCH_CHECK();
   }
+  auto slab = [&](const Pattern::Slabs& S, DevBuf& sv) {
+    sv.alloc(sizeof(double) * std::max<int64_t>(S.nent, 1));
+    if (S.nent > 0) {
+      slab_values_kernel<<<C.num_sms * 8, 256, 0, C.stream>>>(S.nent, S.map.as<int32_t>(), F.val.as<double>(),
+                                                              sv.as<double>());
+      VL_LAUNCH_CHECK();
+    }
+  };
+  slab(P.fwd_sl, F.sv_fwd);
+  slab(P.bwd_sl, F.sv_bwd);
+  slab(P.bwdnh_sl, F.sv_bwdnh);
   factor_head_inverse(C, F);  // dense B_HH^-1 for the solves' head block
 }
 

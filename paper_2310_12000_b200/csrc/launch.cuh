@@ -110,6 +110,14 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
   int L0;
   const uint32_t* items;
   int64_t nitems, npos;
+  Slab sl{nullptr, nullptr, nullptr, nullptr};
+  auto pick = [&](const Pattern::Slabs& S, const DevBuf& sv, int64_t skip) {
+    if (!C.use_slabs || S.nent == 0 || sv.p == nullptr) return;
+    sl.off = S.off.as<uint32_t>() + skip;
+    sl.w = S.w.as<uint32_t>() + skip;
+    sl.idx = S.idx.as<int32_t>();
+    sl.val = sv.as<double>();
+  };
   if (fwd) {
     order = P.fwd_order.as<int32_t>();
     lptr_d = P.fwd_lptr.as<int32_t>();
@@ -118,6 +126,7 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
     items = P.fwd_items.as<uint32_t>() + (head ? P.fwd_items_head_end : 0);
     nitems = P.fwd_nitems - (head ? P.fwd_items_head_end : 0);
     npos = P.fwd_len;
+    pick(P.fwd_sl, F.sv_fwd, head ? P.fwd_items_head_end : 0);
   } else if (head) {
     order = P.bwdnh_order.as<int32_t>();
     lptr_d = P.bwdnh_lptr.as<int32_t>();
@@ -126,6 +135,7 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
     items = P.bwdnh_items.as<uint32_t>();
     nitems = P.bwdnh_nitems;
     npos = P.bwdnh_len;
+    pick(P.bwdnh_sl, F.sv_bwdnh, 0);
   } else {
     order = P.bwd_order.as<int32_t>();
     lptr_d = P.bwd_lptr.as<int32_t>();
@@ -134,6 +144,7 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
     items = P.bwd_items.as<uint32_t>();
     nitems = P.bwd_nitems;
     npos = P.bwd_len;
+    pick(P.bwd_sl, F.sv_bwd, 0);
   }
   const bool single = (G == 1 && NU == 1 && U == 1) && C.thin_passes == 0;
   // launch geometry and slot counts
@@ -217,7 +228,8 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
       int sb = slot0;
       void* args[] = {(void*)&nitems, (void*)&npos,  (void*)&items,    (void*)&order,  (void*)&deps,
                       (void*)&x,      (void*)&body,  (void*)&fin,      (void*)&partials, (void*)&counter,
-                      (void*)&gate,   (void*)&smax,  (void*)&tstamp,   (void*)&sb,     (void*)&total};
+                      (void*)&gate,   (void*)&smax,  (void*)&tstamp,   (void*)&sb,     (void*)&total,
+                      (void*)&sl};
       if (nitems > 0)
         VL_CUDA(cudaLaunchCooperativeKernel((const void*)k1, dim3(grid1), dim3(kRowsThreads), args, smem1,
                                             C.stream));

@@ -319,6 +319,233 @@ VL_D void trsv_row(int64_t p, int64_t pend_, int t, int ld, const int32_t* __res
   }
 }
 
+// Single-column row per lane with per-lane early completion: every lane runs
+// the same converged loop (one batch of 32 dependencies at a time), but a lane
+// stores its row as soon as ITS dependencies are in, instead of waiting for
+// the slowest row of the warp.  Without this, a row of level l+1 effectively
+// waits for the slowest of ~32 x deg rows of level l (a per-level barrier with
+// tail latency); with it, each row waits only for its own dependencies.
+#ifndef VL_POLL_ONE
+#define VL_POLL_ONE 0
+#endif
+template <class Deps, class Body>
+VL_D void trsv_row1(int64_t p, int64_t pend_, const int32_t* __restrict__ order, const Deps& deps,
+                    double* __restrict__ x, const Body& body, unsigned smax, long long* __restrict__ tstamp,
+                    double& acc0) {
+  constexpr int B = 32;
+  const int32_t so = (p < pend_) ? order[p] : -1;
+  const bool valid = so >= 0;
+  const int64_t s = valid ? so : 0;
+  double xs = valid ? body.rhs(s, 0, acc0) : 0.0;
+  const int cs = valid ? deps.count(s) : 0;
+  const int64_t b0 = valid ? deps.base(s) : 0;
+#ifdef VL_TS_EXT
+  long long rounds = 0;
+  if (tstamp != nullptr && valid) {
+    long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    tstamp[VL_TS_EXT + s] = g;
+  }
+#endif
+  int e0 = 0;
+  int32_t j[B];
+  double w[B], v[B];
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    const bool on = q < cs;
+    j[q] = on ? deps.idx(b0 + q) : 0;
+    w[q] = on ? deps.w(b0 + q) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    if (q < cs) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
+    else v[q] = 0.0;
+  }
+  bool done = !valid;
+  unsigned ns = 8;
+  int pq = -1;
+  for (;;) {
+    if (!done) {
+      bool pend = false;
+#pragma unroll
+      for (int q = 0; q < B; ++q) pend |= is_sentinel(v[q]);
+#ifdef VL_TS_EXT
+      ++rounds;
+      if (!pend && tstamp != nullptr) {
+        long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        tstamp[2LL * VL_TS_EXT + s] = g;
+        tstamp[3LL * VL_TS_EXT + s] = rounds;
+      }
+#endif
+      if (!pend) {
+#pragma unroll
+        for (int q = 0; q < B; ++q) xs -= w[q] * v[q];
+        e0 += B;
+        if (e0 >= cs) {
+          body.out(s, 0, xs, acc0);
+          __stcg(x + s, sanitize(xs));
+          if (tstamp != nullptr) {
+            long long g;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+            tstamp[s] = g;
+          }
+          done = true;
+        } else {
+#pragma unroll
+          for (int q = 0; q < B; ++q) {
+            const bool on = e0 + q < cs;
+            j[q] = on ? deps.idx(b0 + e0 + q) : 0;
+            w[q] = on ? deps.w(b0 + e0 + q) : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < B; ++q) {
+            if (e0 + q < cs) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
+            else v[q] = 0.0;
+          }
+          pq = -1;
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
+    if (smax) {
+      __nanosleep(ns);
+      ns = ns < smax ? ns * 2 : smax;
+    }
+    if (!done) {
+#if VL_POLL_ONE
+      // Re-poll only one pending dependency (pq) while it is pending; once it
+      // has arrived, re-poll every still-pending one in a single round.  Keeps
+      // the L2 request rate of thousands of waiting warps low.
+      bool pq_pending = false;
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+        if (q == pq && is_sentinel(v[q])) pq_pending = true;
+      if (pq_pending) {
+#pragma unroll
+        for (int q = 0; q < B; ++q)
+          if (q == pq) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
+      } else {
+        int nq = -1;
+#pragma unroll
+        for (int q = 0; q < B; ++q)
+          if (is_sentinel(v[q])) {
+            ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
+            nq = nq < 0 ? q : nq;
+          }
+        pq = nq;
+      }
+#else
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+        if (is_sentinel(v[q])) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
+#endif
+    }
+  }
+}
+
+// Coalesced dependency slab of the light single-RHS items (Pattern::Slabs).
+struct Slab {
+  const uint32_t* off;
+  const uint32_t* w;
+  const int32_t* idx;
+  const double* val;
+};
+
+// trsv_row1 over the item's slab: the 32 lanes read entry e of their rows as
+// one 128-byte (index) and one 256-byte (value) transaction, instead of 32
+// scattered row segments; padded entries have idx -1 / value 0.  Same
+// per-lane early completion and the same summation order as trsv_row1.
+template <class Body>
+VL_D void trsv_row1s(int64_t p, int64_t pend_, const int32_t* __restrict__ order, uint32_t off, int wk,
+                     const Slab& sl, int lane, double* __restrict__ x, const Body& body, unsigned smax,
+                     long long* __restrict__ tstamp, double& acc0) {
+  constexpr int B = 32;
+  const int32_t so = (p < pend_) ? order[p] : -1;
+  const bool valid = so >= 0;
+  const int64_t s = valid ? so : 0;
+  double xs = valid ? body.rhs(s, 0, acc0) : 0.0;
+#ifdef VL_TS_EXT
+  long long rounds = 0;
+  if (tstamp != nullptr && valid) {
+    long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    tstamp[VL_TS_EXT + s] = g;
+  }
+#endif
+  const int32_t* ip = sl.idx + (int64_t)off * 32 + lane;
+  const double* vp = sl.val + (int64_t)off * 32 + lane;
+  int e0 = 0;
+  int32_t j[B];
+  double w[B], v[B];
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    const bool on = q < wk;
+    j[q] = on ? __ldg(ip + q * 32) : -1;
+    w[q] = on ? __ldg(vp + q * 32) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    if (j[q] >= 0) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
+    else v[q] = 0.0;
+  }
+  bool done = !valid;
+  unsigned ns = 8;
+  for (;;) {
+    if (!done) {
+      bool pend = false;
+#pragma unroll
+      for (int q = 0; q < B; ++q) pend |= is_sentinel(v[q]);
+#ifdef VL_TS_EXT
+      ++rounds;
+      if (!pend && tstamp != nullptr) {
+        long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        tstamp[2LL * VL_TS_EXT + s] = g;
+        tstamp[3LL * VL_TS_EXT + s] = rounds;
+      }
+#endif
+      if (!pend) {
+#pragma unroll
+        for (int q = 0; q < B; ++q) xs -= w[q] * v[q];
+        e0 += B;
+        if (e0 >= wk) {
+          body.out(s, 0, xs, acc0);
+          __stcg(x + s, sanitize(xs));
+          if (tstamp != nullptr) {
+            long long g;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+            tstamp[s] = g;
+          }
+          done = true;
+        } else {
+#pragma unroll
+          for (int q = 0; q < B; ++q) {
+            const bool on = e0 + q < wk;
+            j[q] = on ? __ldg(ip + (e0 + q) * 32) : -1;
+            w[q] = on ? __ldg(vp + (e0 + q) * 32) : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < B; ++q) {
+            if (j[q] >= 0) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
+            else v[q] = 0.0;
+          }
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
+    if (smax) {
+      __nanosleep(ns);
+      ns = ns < smax ? ns * 2 : smax;
+    }
+    if (!done) {
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+        if (is_sentinel(v[q])) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
+    }
+  }
+}
+
 struct TrsvLaunch {
   int64_t p0, p1;          // position range (thick) ; unused by thin
   int L0, L1;              // level range (thin)
@@ -363,6 +590,9 @@ __global__ void __launch_bounds__(kRowsThreads) trsv_kernel(TrsvLaunch L, int t,
 // one row solved warp-per-row with the lanes over its dependencies (rows of
 // thin levels / rows with many children), then a shuffle reduction.
 constexpr uint32_t kHeavyBit = 0x80000000u;
+#ifndef VL_PREFETCH
+#define VL_PREFETCH 1
+#endif
 
 template <int NR, class Deps, class Body, class Fin>
 __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int64_t npos,
@@ -373,7 +603,7 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
                                                              unsigned* __restrict__ counter,
                                                              const int* __restrict__ gate, unsigned smax,
                                                              long long* __restrict__ tstamp, int slot_base,
-                                                             int total_slots) {
+                                                             int total_slots, Slab sl) {
   if (gate != nullptr && *((volatile const int*)gate) == 0) return;
   extern __shared__ double rsh[];
   constexpr int NRR = NR > 0 ? NR : 1;
@@ -384,10 +614,40 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
   double acc[NRR][1];
 #pragma unroll
   for (int r = 0; r < NRR; ++r) acc[r][0] = 0.0;
+  // Two-deep item pipeline: while item i is processed, the descriptors of
+  // item i + 2W are in flight and the structure of item i + W (its order
+  // entries and slab lines) is prefetched into L2, so a warp reaching its next
+  // item finds the dependent-load chain mostly in L2 instead of HBM.
+  auto desc = [&](int64_t i, uint32_t& d, uint32_t& o, uint32_t& w) {
+    if (i < nitems) {
+      d = __ldg(items + i);
+      o = sl.idx ? __ldg(sl.off + i) : 0u;
+      w = sl.idx ? __ldg(sl.w + i) : 0u;
+    } else {
+      d = kHeavyBit; o = 0u; w = 0u;
+    }
+  };
+  uint32_t c_d, c_o, c_w, n_d, n_o, n_w;
+  desc(gwarp, c_d, c_o, c_w);
+  desc(gwarp + nwarps, n_d, n_o, n_w);
   for (int64_t it = gwarp; it < nitems; it += nwarps) {
-    const uint32_t item = items[it];
+    const uint32_t item = c_d;
+    const uint32_t off = c_o, wk = c_w;
+    if (VL_PREFETCH && sl.idx != nullptr && it + nwarps < nitems && !(n_d & kHeavyBit)) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(order + n_d + lane));
+      for (uint32_t l = lane; l < 3 * n_w; l += 32) {
+        const char* a = l < n_w ? reinterpret_cast<const char*>(sl.idx + ((int64_t)n_o + l) * 32)
+                                : reinterpret_cast<const char*>(sl.val + (int64_t)n_o * 32) + (int64_t)(l - n_w) * 128;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+      }
+    }
+    c_d = n_d; c_o = n_o; c_w = n_w;
+    desc(it + 2 * nwarps, n_d, n_o, n_w);
     if (!(item & kHeavyBit)) {
-      trsv_row<1, 1, 1, true>((int64_t)item + lane, npos, 1, 1, order, deps, x, body, smax, tstamp, 0, acc[0]);
+      if (sl.idx != nullptr)
+        trsv_row1s((int64_t)item + lane, npos, order, off, (int)wk, sl, lane, x, body, smax, tstamp, acc[0][0]);
+      else
+        trsv_row1((int64_t)item + lane, npos, order, deps, x, body, smax, tstamp, acc[0][0]);
       continue;
     }
     const int32_t so = order[item & ~kHeavyBit];

@@ -47,8 +47,8 @@ for t in [int(x) for x in os.environ.get("KP_TS", "1,50").split(",")]:
     L.vl_debug_set_tstamp(f.ctx.h, None)
     tsf = np.empty(n, dtype=np.int64)
     tsf[pat.sperm] = ts.cpu().numpy()  # factor order
-    t0 = tsf.min()
-    tsf = tsf - t0
+    t0 = tsf[tsf > 0].min()
+    tsf = np.where(tsf > 0, tsf - t0, 0)
     nl = lev.max() + 1
     lev_end = np.full(nl, -1, dtype=np.int64)
     np.maximum.at(lev_end, lev, tsf)
@@ -67,3 +67,19 @@ for t in [int(x) for x in os.environ.get("KP_TS", "1,50").split(",")]:
     print("  hop latency us: p50 %.2f p90 %.2f p99 %.2f max %.2f" % tuple(np.percentile(hop[lev > 0], [50, 90, 99, 100]) / 1e3))
     marks = [0, 10, 20, 50, 100, 150, 200, 250, 300, 330, nl - 1]
     print("  " + " ".join(f"L{Lv}({size[Lv]}):{lev_end[Lv]/1e3:.0f}" for Lv in marks if Lv < nl))
+    # critical chain: from the last-finished row follow the latest-finishing dependency
+    if not TR:
+        cur = int(np.argmax(tsf))
+        chain = []
+        while True:
+            row = nb[cur][nb[cur] >= 0]
+            if row.size == 0:
+                break
+            j = int(row[np.argmax(tsf[row])])
+            chain.append((lev[cur], tsf[cur] - tsf[j]))
+            cur = j
+        hops = np.array([h for _, h in chain])
+        print("  critical chain: %d hops, sum %.1fus, hop p50 %.2f p90 %.2f max %.2f us" %
+              (len(hops), hops.sum() / 1e3, *(np.percentile(hops, [50, 90, 100]) / 1e3)))
+        print("  chain (level:hop_ns) " + " ".join(f"{lv}:{h}" for lv, h in chain))
+    print("  level end (us): " + " ".join(f"{Lv}:{lev_end[Lv]/1e3:.1f}" for Lv in range(0, nl, 5)))
