@@ -7,8 +7,11 @@
 // One iteration = 4 kernels:
 //   K1  h = z + beta h_prev (fused into the gather),  tmp = D^-1 (B h)
 //   K2  v = W h + B^T tmp,  h.v -> alpha            (last-CTA finalize)
-//   K3  r -= alpha v, u += alpha h (fused rhs),  w = B^-T r,  ||r|| -> converged?
-//   K4  z = B^-1 (w / d),  r.z -> beta
+//   K3  w = B^-T (r - alpha v),  ||r - alpha v|| -> converged?
+//   K4  z = B^-1 (w / d),  (r - alpha v).z -> beta
+// The r/u updates themselves (r -= alpha v, u += alpha h) are deferred to
+// the next iteration's elementwise h-update (and a final flush), so the
+// solves' rows read two vectors instead of read-modify-writing four.
 #include <cmath>
 #include <cstring>
 
@@ -30,13 +33,20 @@ struct RhsPlainActive {  // w = B^-T r  (init)
   VL_D double rhs(int64_t s, int c, double&) const { return r[s * ld + c]; }
   VL_D void out(int64_t, int, double, double&) const {}
 };
-struct RhsScaleDot {  // z = B^-1 (w * dinv) ; acc += r . z
+template <bool DEFER>
+struct RhsScaleDot {  // z = B^-1 (w * dinv) ; acc += (r - alpha v) . z
   const double* w;
   const double* dinv;
   const double* r;
+  const double* v;
+  const double* alpha;
   int ld;
   VL_D double rhs(int64_t s, int c, double&) const { return w[s * ld + c] * dinv[s]; }
-  VL_D void out(int64_t s, int c, double x, double& acc) const { acc += r[s * ld + c] * x; }
+  VL_D void out(int64_t s, int c, double x, double& acc) const {
+    const int64_t o = s * ld + c;
+    const double rn = DEFER ? fma(-alpha[c], v[o], r[o]) : r[o];
+    acc += rn * x;
+  }
 };
 struct RzInitFin {
   CgCols K;
@@ -95,24 +105,58 @@ struct K2Body {
 };
 // ---- K3: r -= alpha v, u += alpha h (rhs of w = B^-T r); ||r|| -------------
 struct K3Rhs {
-  double* r;
-  double* u;
+  const double* r;
   const double* v;
-  const double* h;
   const double* alpha;
-  const int* active;
   int ld;
   VL_D double rhs(int64_t s, int c, double& acc) const {
     const int64_t o = s * ld + c;
-    if (!active[c]) return r[o];
-    const double al = alpha[c];
-    const double rn = r[o] - al * v[o];
-    r[o] = rn;
-    u[o] = u[o] + al * h[o];
+    const double rn = fma(-alpha[c], v[o], r[o]);  // alpha = 0 for frozen columns
     acc += rn * rn;
     return rn;
   }
   VL_D void out(int64_t, int, double, double&) const {}
+};
+// ---- deferred update: r -= alpha v, u += alpha h; then h = z + beta h -------
+template <bool HUPD>
+struct DeferBody {
+  const double* z;
+  double* h;
+  double* r;
+  double* u;
+  const double* v;
+  const double* alpha;
+  const double* beta;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&)[NR][NU * U]) const {
+    if (!valid) return;
+    constexpr int NC = NU * U;
+    double hs[NC], rs[NC], us[NC], vs[NC];
+    load_row<G, NU, U>(h, ld, s, gl, t, hs);
+    load_row<G, NU, U>(r, ld, s, gl, t, rs);
+    load_row<G, NU, U>(u, ld, s, gl, t, us);
+    load_row<G, NU, U>(v, ld, s, gl, t, vs);
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int c = vl::Cols<G, NU, U>::col(gl, i);
+      const double al = c < t ? alpha[c] : 0.0;
+      rs[i] = fma(-al, vs[i], rs[i]);
+      us[i] = fma(al, hs[i], us[i]);
+    }
+    store_row<G, NU, U>(r, ld, s, gl, t, rs);
+    store_row<G, NU, U>(u, ld, s, gl, t, us);
+    if constexpr (HUPD) {
+      double zs[NC];
+      load_row<G, NU, U>(z, ld, s, gl, t, zs);
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        const int c = vl::Cols<G, NU, U>::col(gl, i);
+        hs[i] = zs[i] + (c < t ? beta[c] : 0.0) * hs[i];
+      }
+      store_row<G, NU, U>(h, ld, s, gl, t, hs);
+    }
+  }
 };
 // ---- K4: z = B^-1 (w / d); r.z -> beta -------------------------------------
 }  // namespace
@@ -127,6 +171,7 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
   const size_t vb = sizeof(double) * (size_t)n * ld;
   DevBuf r, z, w, v, tmp, h0, h1;
   r.alloc(vb); z.alloc(vb); w.alloc(vb); v.alloc(vb); tmp.alloc(vb); h0.alloc(vb); h1.alloc(vb);
+  VL_CUDA(cudaMemsetAsync(v.p, 0, vb, C.stream));  // read (times alpha = 0) by the first deferred update
   const int cap = capture ? std::max(max_iter, 1) : 1;
   DevBuf colsd, colsi, hist;
   colsd.alloc(sizeof(double) * (7 * (size_t)t + 1));
@@ -154,7 +199,8 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
     launch_trsv<G, NU, U, 0>(C, F, false, t, ld, dbw, w.as<double>(),
                              RhsPlainActive{r.as<double>(), ld}, Fin0<0>{}, gate);
     launch_trsv<G, NU, U, 1>(C, F, true, t, ld, dfw, z.as<double>(),
-                             RhsScaleDot{w.as<double>(), S.dinv, r.as<double>(), ld}, RzInitFin{K}, gate);
+                             RhsScaleDot<false>{w.as<double>(), S.dinv, r.as<double>(), nullptr, nullptr, ld},
+                             RzInitFin{K}, gate);
     int status[3] = {0, 0, 0};
     int l = 0;
     int chunk = 4;
@@ -164,7 +210,10 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
         double* hn = hb[0];
         {
           ProfScope ps(C, t == 1 ? "cg1_hupd" : "cgT_hupd", 24.0 * n * t);
-          launch_rows<G, NU, U, 0, 0>(C, n, t, HUpdBody{z.as<double>(), hn, K.beta, ld}, Fin0<0>{}, gate);
+          launch_rows<G, NU, U, 0, 0>(C, n, t,
+                                      DeferBody<true>{z.as<double>(), hn, r.as<double>(), u, v.as<double>(),
+                                                      K.alpha, K.beta, ld},
+                                      Fin0<0>{}, gate);
         }
         {
           ProfScope ps(C, t == 1 ? "cg1_spmm_B" : "cgT_spmm_B", bapply_bytes(P, t, 1));
@@ -178,13 +227,15 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
         {
           ProfScope ps(C, t == 1 ? "cg1_trsv_Bt" : "cgT_trsv_Bt", bapply_bytes(P, t, 0));
           launch_trsv<G, NU, U, 1>(C, F, false, t, ld, dbw, w.as<double>(),
-                                   K3Rhs{r.as<double>(), u, v.as<double>(), hn, K.alpha, K.active, ld},
+                                   K3Rhs{r.as<double>(), v.as<double>(), K.alpha, ld},
                                    K3Fin{K, l}, gate);
         }
         {
           ProfScope ps(C, t == 1 ? "cg1_trsv_B" : "cgT_trsv_B", bapply_bytes(P, t, 1));
           launch_trsv<G, NU, U, 1>(C, F, true, t, ld, dfw, z.as<double>(),
-                                   RhsScaleDot{w.as<double>(), S.dinv, r.as<double>(), ld}, K4Fin{K, l, cap}, gate);
+                                   RhsScaleDot<true>{w.as<double>(), S.dinv, r.as<double>(), v.as<double>(),
+                                                     K.alpha, ld},
+                                   K4Fin{K, l, cap}, gate);
         }
       }
       VL_CUDA(cudaMemcpyAsync(status, K.status, sizeof(status), cudaMemcpyDeviceToHost, C.stream));
@@ -192,6 +243,11 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
       if (status[1] != 0 || status[0] == 0) break;
       chunk = std::min(chunk * 2, 16);
     }
+    // flush the last deferred update (alpha = 0 when nothing is pending)
+    launch_rows<G, NU, U, 0, 0>(C, n, t,
+                                DeferBody<false>{nullptr, hb[0], r.as<double>(), u, v.as<double>(), K.alpha, nullptr,
+                                                 ld},
+                                Fin0<0>{});
     if (status[1] != 0) {
       double ev = 0;
       VL_CUDA(cudaMemcpy(&ev, K.errval, sizeof(double), cudaMemcpyDeviceToHost));

@@ -76,6 +76,7 @@ struct InitFin {
       K.conv[c] = act ? 0 : 1;
       K.iters[c] = 0;
       K.beta[c] = 0.0;
+      K.alpha[c] = 0.0;
       K.rz[c] = 0.0;
       K.res[c] = nb;
     }
@@ -111,7 +112,10 @@ struct K2Fin {
   int cap;
   VL_D void operator()(const double* sums, int t) const {
     for (int c = threadIdx.x; c < t; c += blockDim.x) {
-      if (!K.active[c]) continue;
+      if (!K.active[c]) {
+        K.alpha[c] = 0.0;  // a deferred r/u update of a frozen column is then exact no-op
+        continue;
+      }
       const double hv = sums[c];
       if (hv <= 0.0) set_error(K, kEBreakdown, c, hv);
       const double al = K.rz[c] / hv;
