@@ -834,16 +834,16 @@ struct DQDotBody {
   template <int G, int NU, int U, int NR>
   VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
     constexpr int NC = NU * U;
-    if (!valid) return;
     double BU[NC], BV[NC], dBU[NC], dBV[NC], us[NC], vs[NC];
     zero(BU);
     zero(BV);
     zero(dBU);
     zero(dBV);
-    gather_B<G, NU, U>(B, B.val, s, true, gl, t, LoadU<U>{U_, ld}, BU);
-    gather_B<G, NU, U>(B, B.val, s, true, gl, t, LoadU<U>{V_, ld}, BV);
-    gather_B<G, NU, U>(B, dval, s, true, gl, t, LoadU<U>{U_, ld}, dBU);
-    gather_B<G, NU, U>(B, dval, s, true, gl, t, LoadU<U>{V_, ld}, dBV);
+    gather_B<G, NU, U>(B, B.val, s, valid, gl, t, LoadU<U>{U_, ld}, BU);
+    gather_B<G, NU, U>(B, B.val, s, valid, gl, t, LoadU<U>{V_, ld}, BV);
+    gather_B<G, NU, U>(B, dval, s, valid, gl, t, LoadU<U>{U_, ld}, dBU);
+    gather_B<G, NU, U>(B, dval, s, valid, gl, t, LoadU<U>{V_, ld}, dBV);
+    if (!valid) return;
     load_row<G, NU, U>(U_, ld, s, gl, t, us);
     load_row<G, NU, U>(V_, ld, s, gl, t, vs);
 #pragma unroll
