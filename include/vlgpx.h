@@ -64,6 +64,15 @@ int vl_ctx_info(vl_ctx* ctx, int64_t* info);
  * out_host: n x m int32, row i = indices (< i) of the min(i,m) nearest earlier
  * points, nearest first, ties to the smaller index; padded with -1. */
 int vl_knn_previous(const double* xy_host, int64_t n, int d, int m, int32_t* out_host, int n_threads);
+/* The same search on the device (1 <= d <= 3, m <= 256): brute force below
+ * 4096 points, uniform grids over growing prefixes above; identical output. */
+int vl_knn_previous_dev(vl_ctx* ctx, const double* xy_host, int64_t n, int d, int m, int32_t* out_host);
+/* Nearest TRAINING neighbours of prediction points (replaces the cKDTree query
+ * + lexsort of vecchia.py:411-421): row q = the min(m, n) training indices
+ * closest to query q, nearest first, ties to the smaller index; dmin_host[q] =
+ * distance to the nearest (the caller rejects duplicates, vecchia.py:416-420). */
+int vl_knn_query(vl_ctx* ctx, const double* train_host, int64_t n, const double* q_host, int64_t nq, int d, int m,
+                 int32_t* out_host, double* dmin_host);
 
 /* ---- pattern (once per dataset) ---------------------------------------------
  * Replaces the structural part of vecchia.py:220-283 (CSR layout of B,

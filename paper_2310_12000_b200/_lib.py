@@ -32,6 +32,8 @@ _SIGS = {
     "vl_ctx_sync": [c_void_p],
     "vl_ctx_info": [c_void_p, P_int64],
     "vl_knn_previous": [c_void_p, c_int64, c_int, c_int, c_void_p, c_int],
+    "vl_knn_previous_dev": [c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p],
+    "vl_knn_query": [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_int, c_int, c_void_p, c_void_p],
     "vl_pattern_create": [c_void_p, c_int64, c_int, c_int, c_void_p, c_void_p, c_int, C.POINTER(c_void_p)],
     "vl_pattern_destroy": [c_void_p],
     "vl_pattern_perm": [c_void_p, c_void_p],

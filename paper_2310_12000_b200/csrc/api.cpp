@@ -329,6 +329,21 @@ int vl_knn_previous(const double* xy, int64_t n, int d, int m, int32_t* out, int
   });
 }
 
+int vl_knn_previous_dev(vl_ctx* h, const double* xy, int64_t n, int d, int m, int32_t* out) {
+  return guard([&] {
+    if (!xy || !out) fail(kEConfig, "null pointer");
+    knn_previous_dev(h->c, xy, n, d, m, out);
+  });
+}
+
+int vl_knn_query(vl_ctx* h, const double* train, int64_t n, const double* q, int64_t nq, int d, int m, int32_t* out,
+                 double* dmin) {
+  return guard([&] {
+    if (!train || (nq > 0 && (!q || !out || !dmin))) fail(kEConfig, "null pointer");
+    knn_query_dev(h->c, train, n, q, nq, d, m, out, dmin);
+  });
+}
+
 int vl_pattern_create(vl_ctx* h, int64_t n, int d, int m, const double* xy, const int32_t* nbr, int order_kind,
                       vl_pattern** out) {
   return guard([&] {

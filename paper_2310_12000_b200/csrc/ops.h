@@ -7,6 +7,9 @@
 namespace vl {
 
 void knn_previous(const double* xy, int64_t n, int d, int m, int32_t* out, int nthreads);
+void knn_previous_dev(Ctx& C, const double* xy_host, int64_t n, int d, int m, int32_t* out_host);
+void knn_query_dev(Ctx& C, const double* train_host, int64_t n, const double* q_host, int64_t nq, int d, int m,
+                   int32_t* out_host, double* dmin_host);
 void pattern_build_host(Pattern& P, const double* xy, const int32_t* nbr, std::vector<int32_t>& ell,
                         std::vector<int32_t>& cnt, std::vector<int32_t>& fwd, std::vector<int32_t>& bwd,
                         std::vector<int32_t>& tptr, std::vector<int32_t>& tidx, std::vector<int32_t>& tmap);

@@ -43,17 +43,51 @@ def _coords(locs):
     return np.ascontiguousarray(c, dtype=float)
 
 
-def neighbor_array(locs, perm, m, n_threads=0):
+def _knn_on_device(d, m, where):
+    if where == "host":
+        return False
+    if where == "device":
+        return True
+    return 1 <= d <= 3 and m <= 256 and dev.torch().cuda.is_available()
+
+
+def neighbor_array(locs, perm, m, n_threads=0, where="auto"):
     """Exact nearest-preceding neighbours as an (n, m) int32 array padded with -1
-    (native multi-threaded grid search, same definition as find_neighbors)."""
+    (same definition as find_neighbors).  ``where``: "device" (the grid search
+    kernels, knn.cu), "host" (the native multi-threaded grid search) or
+    "auto" (device when a GPU is present and 1 <= d <= 3, m <= 256)."""
     if m < 0:
         raise ConfigError("m must be >= 0")
     xy = np.ascontiguousarray(_coords(locs)[np.asarray(perm, dtype=int)])
     n, d = xy.shape
     out = np.full((n, max(m, 0)), -1, dtype=np.int32)
     if m > 0 and n > 1:
-        _lib.call("vl_knn_previous", _lib.ptr(xy), n, d, m, _lib.ptr(out), int(n_threads))
+        if _knn_on_device(d, m, where):
+            _lib.call("vl_knn_previous_dev", dev.context().h, _lib.ptr(xy), n, d, m, _lib.ptr(out))
+        else:
+            _lib.call("vl_knn_previous", _lib.ptr(xy), n, d, m, _lib.ptr(out), int(n_threads))
     return out
+
+
+def knn_query(train_coords, query_coords, m):
+    """The min(m, n) nearest training points of every query point, nearest
+    first, ties to the smaller training index (vecchia.py:411-421), on the
+    device.  Returns (idx (n_q, take) int64, dmin (n_q,) distance to the nearest)."""
+    train = np.ascontiguousarray(np.atleast_2d(np.asarray(train_coords, dtype=float)))
+    q = np.ascontiguousarray(np.atleast_2d(np.asarray(query_coords, dtype=float)))
+    n, d = train.shape
+    if q.shape[1] != d:
+        raise ConfigError("prediction coordinates must have the training dimension")
+    if m < 1:
+        raise ConfigError("prediction requires m >= 1")
+    nq = q.shape[0]
+    take = min(m, n)
+    out = np.full((nq, take), -1, dtype=np.int32)
+    dmin = np.empty(nq)
+    if nq:
+        _lib.call("vl_knn_query", dev.context().h, _lib.ptr(train), n, _lib.ptr(q), nq, d, take, _lib.ptr(out),
+                  _lib.ptr(dmin))
+    return out.astype(np.int64), dmin
 
 
 def find_neighbors(locs, perm, m):
