@@ -173,6 +173,7 @@ int vl_grad_probe_pass(vl_ctx* ctx, const vl_factor* f, const double* W_dev, con
 
 /* ---- LRAC preconditioner and the eq7 system (preconditioners.py:167-214,
  * 249-320; laplace.py:118-182) ------------------------------------------------ */
+typedef struct vl_pred vl_pred;    /* prediction blocks Bpo, Dp (vecchia.py:364-441) */
 typedef struct vl_lrac vl_lrac;    /* rank-k pivoted Cholesky of Sigma (theta only) */
 typedef struct vl_lracw vl_lracw;  /* Woodbury core M = I + L^T W L for one W       */
 
@@ -241,6 +242,26 @@ int vl_grad_dbeta(vl_ctx* ctx, int64_t n, const double* d1_dev, const double* s_
  * sum(tvec (-1 + y e^{-mu})), sum(md3x / (W + 1/D))] */
 int vl_gamma_xi_terms(vl_ctx* ctx, const vl_factor* f, const double* y_dev, const double* F_dev, const double* b_dev,
                       const double* W_dev, const double* tvec_dev, double* md3x_dev, double* out3_host);
+
+/* ---- prediction (predict.py:45-101, vecchia.py:364-441) ----------------------
+ * vl_pred_create: Bpo rows (-A, A = K^-1 k over the `take` nearest training
+ * points given by nbr_host = np x take FACTOR-order indices, nearest first)
+ * and Dp = sigma2 - k.A for the np prediction points qxy_host (np x d);
+ * status 40 when a neighbour covariance submatrix is not positive definite
+ * (_chol_or_report).  vl_pred_get: which 0 = Bpo values (np x take), 1 = Dp.
+ * vl_pred_mean: omega = F_p - Bpo b* (device, b in storage order).
+ * vl_pred_z3: z3 = W^1/2 z1 + B^T (D^-1/2 z2) for c samples (n x c storage
+ * order; the rhs of one CG solve per sample, predict.py:90-93).
+ * vl_pred_accum: z4 = Bpo u for the c solved samples; acc[q] += sum_c z4^2 in
+ * sample order; cov (np x np, optional) += z4 z4^T (predict.py:94-98). */
+int vl_pred_create(vl_ctx* ctx, const vl_pattern* p, double sigma2, double rho, double nu, const double* qxy_host,
+                   int64_t np, const int32_t* nbr_host, int take, vl_pred** out);
+int vl_pred_destroy(vl_pred* b);
+int vl_pred_get(vl_ctx* ctx, const vl_pred* b, int which, double* out_host);
+int vl_pred_mean(vl_ctx* ctx, const vl_pred* b, const double* b_dev, const double* Fp_dev, double* omega_dev);
+int vl_pred_z3(vl_ctx* ctx, const vl_factor* f, const double* W_dev, int64_t c, const double* z1_dev,
+               const double* z2_dev, double* z3_dev);
+int vl_pred_accum(vl_ctx* ctx, const vl_pred* b, const double* U_dev, int64_t c, double* acc_dev, double* cov_dev);
 
 #ifdef __cplusplus
 }

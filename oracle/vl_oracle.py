@@ -339,7 +339,7 @@ _LOG_SQRT_2PI = 0.5 * np.log(2.0 * np.pi)
 
 class Lik:
     def __init__(self, family, shape=1.0):
-        if family not in ("bernoulli-logit", "bernoulli-probit", "gamma"):
+        if family not in ("bernoulli-logit", "bernoulli-probit", "gamma", "poisson"):
             raise ValueError(family)
         self.family = family
         self.shape = float(shape)
@@ -353,6 +353,8 @@ class Lik:
             return y * mu - np.logaddexp(0.0, mu)
         if self.family == "bernoulli-probit":         # likelihoods.py:104-106
             return log_ndtr((2.0 * y - 1.0) * mu)
+        if self.family == "poisson":                  # test-registered family (make_golden.register_poisson)
+            return y * mu - np.exp(mu) - gammaln(y + 1.0)
         a = self.shape                                # likelihoods.py:150-158
         return a * np.log(a) - gammaln(a) + (a - 1.0) * np.log(y) - a * mu - a * y * np.exp(-mu)
 
@@ -369,6 +371,9 @@ class Lik:
             d1 = z * g
             d2 = -g * (u + g)
             d3 = z * g * ((u + g) ** 2 + g * (u + g) - 1.0)
+        elif self.family == "poisson":
+            e = np.exp(mu)
+            d1, d2, d3 = y - e, -e, -e
         else:                                         # likelihoods.py:160-166
             a = self.shape
             w = a * y * np.exp(-mu)
@@ -949,3 +954,59 @@ def evaluate(xy, nbr, y, F, X, sigma2, rho, nu, lik, cfg, want_grad=True, G=None
         return val, None, info
     g = gradient(f, st, lik, X, cfg, pr, P, details=info)
     return val, g, info
+
+
+# --------------------------------------------------------------------------
+# Prediction (vecchia.py:364-441, predict.py:45-101)
+# --------------------------------------------------------------------------
+
+def prediction_blocks(train_xy_f, pred_xy, m, sigma2, rho, nu):
+    """vecchia.py:393-441: each prediction point conditions on its min(m, n)
+    nearest training points (factor order; ties to the smaller index);
+    Bpo row = -K^-1 k (LU solve as the reference), Dp = sigma2 - k.A.
+    Returns (nbr (n_p, take), Bpo values (n_p, take), Dp (n_p,))."""
+    n = train_xy_f.shape[0]
+    n_p = pred_xy.shape[0]
+    take = min(m, n)
+    nbr = np.empty((n_p, take), dtype=np.int64)
+    vals = np.empty((n_p, take))
+    Dp = np.empty(n_p)
+    for q in range(n_p):
+        d = np.sqrt(((train_xy_f - pred_xy[q]) ** 2).sum(axis=1))
+        if d.min() <= 1e-12:
+            raise ValueError(f"prediction point {q} duplicates a training point")
+        idx = np.lexsort((np.arange(n), d))[:take]
+        X = train_xy_f[idx]
+        K = matern(np.sqrt(((X[:, None, :] - X[None, :, :]) ** 2).sum(axis=2)), sigma2, rho, nu)
+        k = matern(d[idx], sigma2, rho, nu)
+        A = np.linalg.solve(K, k)
+        nbr[q] = idx
+        vals[q] = -A
+        Dp[q] = sigma2 - k @ A
+    return nbr, vals, Dp
+
+
+def latent_mean(b, nbr, vals, Fp):
+    """predict.py:45-50: omega = F_p - Bpo b*."""
+    return Fp + (-(vals * b[nbr]).sum(axis=1))
+
+
+def latent_var_sim(f, W, nbr, vals, Dp, s, seed, cg_tol, cg_max_iter=1000, full=False):
+    """predict.py:70-101 with the VADU eq6 system: per sample z3 = W^1/2 z1 +
+    B^T D^-1/2 z2 (z1, z2 drawn in that order from default_rng(seed)),
+    u = (W + Q)^-1 z3 by PCG at cg_tol, z4 = Bpo u, acc += z4^2."""
+    rng = np.random.default_rng(seed)
+    n = f.n
+    P = Vadu(f, W)
+    op = system_matvec(f, W, "eq6")
+    acc = np.zeros((len(Dp), len(Dp))) if full else np.zeros(len(Dp))
+    for _ in range(s):
+        z1 = rng.standard_normal(n)
+        z2 = rng.standard_normal(n)
+        z3 = np.sqrt(W) * z1 + f.B.T @ (z2 / np.sqrt(f.D))
+        res = pcg(op, z3, P.solve, cg_tol, cg_max_iter)
+        z4 = (vals * res.u[nbr]).sum(axis=1)
+        acc = acc + (np.outer(z4, z4) if full else z4 ** 2)
+    if full:
+        return Dp + np.diag(acc) / s, np.diag(Dp) + acc / s
+    return Dp + acc / s

@@ -31,3 +31,17 @@ __version__ = "0.1.0"
 from .laplace import BackendConfig, LaplaceState, find_mode, gradient, make_probes, neg_marginal_loglik
 from .likelihoods import get_likelihood
 from .iterative import ProbeSet, Tridiag
+from .predict import (
+    PredictionBlocks,
+    PredictiveDistribution,
+    crps_from_samples,
+    gaussian_log_score,
+    latent_mean,
+    latent_var_exact,
+    latent_var_sim,
+    predict_latent,
+    prediction_blocks,
+    response_moments,
+    rmse,
+    scores,
+)

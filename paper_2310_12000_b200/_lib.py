@@ -139,6 +139,13 @@ _SIGS.update({
     "vl_lrac_probes": [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "vl_lrac_grad": [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                      c_void_p, c_void_p, c_void_p],
+    "vl_pred_create": [c_void_p, c_void_p, c_double, c_double, c_double, c_void_p, c_int64, c_void_p, c_int,
+                       c_void_p],
+    "vl_pred_destroy": [c_void_p],
+    "vl_pred_get": [c_void_p, c_void_p, c_int, c_void_p],
+    "vl_pred_mean": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    "vl_pred_z3": [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p],
+    "vl_pred_accum": [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p],
     "vl_find_mode_lrac": [c_void_p, c_void_p, c_void_p, C.POINTER(VlLik), C.POINTER(VlNewtonCfg), c_void_p, c_void_p,
                           c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int],
 })

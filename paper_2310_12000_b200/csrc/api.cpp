@@ -13,6 +13,7 @@
 #include "laplace.h"
 #include "lrac.h"
 #include "ops.h"
+#include "predict.h"
 #include "pcg.h"
 
 struct vl_ctx {
@@ -24,6 +25,9 @@ struct vl_pattern {
 };
 struct vl_factor {
   vl::Factor f;
+};
+struct vl_pred {
+  vl::PredBlocks b;
 };
 struct vl_lrac {
   vl::LracFactor lf;
@@ -749,6 +753,49 @@ int vl_sptrsv(vl_ctx* h, const vl_factor* f, int transpose, int64_t t, const dou
     if (t < 1 || t > (1 << 20)) fail(kEConfig, "invalid column count");
     op_trsv(h->c, f->f, transpose != 0, (int)t, (int)t, x, y);
   });
+}
+
+
+int vl_pred_create(vl_ctx* h, const vl_pattern* p, double sigma2, double rho, double nu, const double* qxy, int64_t np,
+                   const int32_t* nbr, int take, vl_pred** out) {
+  return guard([&] {
+    if (!h || !p || !out || (np > 0 && (!qxy || !nbr))) fail(kEConfig, "null pointer");
+    auto* b = new vl_pred();
+    try {
+      pred_create(h->c, p->p, sigma2, rho, nu, qxy, np, nbr, take, b->b);
+    } catch (...) {
+      delete b;
+      throw;
+    }
+    *out = b;
+  });
+}
+
+int vl_pred_destroy(vl_pred* b) {
+  return guard([&] { delete b; });
+}
+
+int vl_pred_get(vl_ctx* h, const vl_pred* b, int which, double* out) {
+  return guard([&] {
+    const size_t cnt = which == 0 ? (size_t)b->b.np * b->b.take : (size_t)b->b.np;
+    const DevBuf& src = which == 0 ? b->b.val : b->b.Dp;
+    if (which != 0 && which != 1) fail(kEConfig, "unknown prediction field");
+    if (cnt) VL_CUDA(cudaMemcpyAsync(out, src.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, h->c.stream));
+    VL_CUDA(cudaStreamSynchronize(h->c.stream));
+  });
+}
+
+int vl_pred_mean(vl_ctx* h, const vl_pred* b, const double* b_dev, const double* Fp_dev, double* omega_dev) {
+  return guard([&] { pred_mean(h->c, b->b, b_dev, Fp_dev, omega_dev); });
+}
+
+int vl_pred_z3(vl_ctx* h, const vl_factor* f, const double* W_dev, int64_t c, const double* z1, const double* z2,
+               double* z3) {
+  return guard([&] { pred_z3(h->c, f->f, W_dev, (int)c, z1, z2, z3); });
+}
+
+int vl_pred_accum(vl_ctx* h, const vl_pred* b, const double* U_dev, int64_t c, double* acc_dev, double* cov_dev) {
+  return guard([&] { pred_accum(h->c, b->b, U_dev, (int)c, acc_dev, cov_dev); });
 }
 
 }  // extern "C"

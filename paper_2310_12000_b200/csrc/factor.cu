@@ -104,7 +104,9 @@ __global__ void __launch_bounds__(128) factor_build_kernel(
     const int32_t* __restrict__ cnt, const int32_t* __restrict__ fidx, Matern K, int want_grad,
     double* __restrict__ val, double* __restrict__ Dout, double* __restrict__ dval,
     double* __restrict__ dD_rho, double* __restrict__ dD_sig, int* __restrict__ err,
-    double* __restrict__ gscratch, int use_smem) {
+    double* __restrict__ gscratch, int use_smem, const double* __restrict__ txy, int dfloor) {
+  // txy: target coordinates of row s (prediction points) or null (row s = point s of xy);
+  // dfloor: report D_s < 1e-10 sigma2 (factor rows; prediction_blocks has no such check)
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -126,7 +128,8 @@ __global__ void __launch_bounds__(128) factor_build_kernel(
 
   for (int64_t s = gw; s < n; s += nw) {
     const int c = cnt[s];
-    const double* xi = xy + s * d;
+    const double* xi = (txy ? txy : xy) + s * d;
+    const int fs = fidx ? fidx[s] : (int)s;
     if (c == 0) {
       if (lane == 0) {
         Dout[s] = K.s2;
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(128) factor_build_kernel(
     }
     if (!ok) {
       if (lane == 0) {
-        atomicMin(err + 1, fidx[s]);
+        atomicMin(err + 1, fs);
         atomicMax(err + 0, 1);
       }
       __syncwarp();
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(128) factor_build_kernel(
     double Ds = K.s2 - kA;
     if (lane == 0) {
       Dout[s] = Ds;
-      if (!(Ds >= 1e-10 * K.s2)) { atomicMin(err + 2, fidx[s]); atomicMax(err + 0, 1); }
+      if (dfloor && !(Ds >= 1e-10 * K.s2)) { atomicMin(err + 2, fs); atomicMax(err + 0, 1); }
     }
     for (int j = lane; j < m; j += 32) val[s * m + j] = (j < c) ? -A[j] : 0.0;
     if (want_grad) {
@@ -364,7 +367,7 @@ static void launch_build(Ctx& C, const Pattern& P, Factor& F, const Matern& K, i
       P.n, P.d, P.m, P.xy.as<double>(), P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), P.fidx.as<int32_t>(), K, want_grad,
       F.val.as<double>(), F.D.as<double>(), want_grad ? F.dval.as<double>() : nullptr,
       want_grad ? F.dD_rho.as<double>() : nullptr, want_grad ? F.dD_sig.as<double>() : nullptr, F.err.as<int>(), gscr,
-      use_smem);
+      use_smem, nullptr, 1);
   VL_LAUNCH_CHECK();
   if (ev) prof_end(C, ev);
 }
@@ -427,6 +430,71 @@ void factor_build(Ctx& C, const Pattern& P, Factor& F, double sigma2, double rho
     fail(kEFactorization, "conditional variance D_" + std::to_string(h_err[2]) +
                               " below 1e-10 * sigma2 (near-duplicate inputs)");
   }
+}
+
+// ---------------------------------------------------------------------------
+// Prediction blocks (vecchia.py:393-441): each prediction point conditions on
+// its `take` nearest training points; A = K^-1 k (Bpo row = -A), Dp = sigma2 -
+// k.A, by the factor-build warp kernel with external target coordinates.
+// ---------------------------------------------------------------------------
+template <int Q, int DIM>
+static void launch_pred(Ctx& C, const Pattern& P, const Matern& K, int64_t np, int take, const double* qxy,
+                        const int32_t* nbr, const int32_t* cnt, double* A, double* Dp, int* err, size_t per) {
+  const int threads = 128;
+  const int wpb = threads / 32;
+  const size_t smem = per * wpb * sizeof(double);
+  const int use_smem = smem <= 200 * 1024 ? 1 : 0;
+  DevBuf gscr;
+  int blocks;
+  if (use_smem) {
+    if (smem > 48 * 1024)
+      VL_CUDA(cudaFuncSetAttribute(factor_build_kernel<Q, DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    int occ = 0;
+    VL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_build_kernel<Q, DIM>, threads, smem));
+    occ = occ > 0 ? occ : 1;
+    blocks = (int)std::max<int64_t>(1, std::min<int64_t>((np + wpb - 1) / wpb, (int64_t)occ * C.num_sms));
+  } else {
+    blocks = C.num_sms * 2;
+    gscr.alloc(per * sizeof(double) * (size_t)blocks * wpb);
+  }
+  factor_build_kernel<Q, DIM><<<blocks, threads, use_smem ? smem : 0, C.stream>>>(
+      np, P.d, take, P.xy.as<double>(), nbr, cnt, nullptr, K, 0, A, Dp, nullptr, nullptr, nullptr, err,
+      gscr.as<double>(), use_smem, qxy, 0);
+  VL_LAUNCH_CHECK();
+}
+
+void pred_build(Ctx& C, const Pattern& P, double sigma2, double rho, double nu, const double* qxy_dev, int64_t np,
+                int take, const int32_t* nbr_dev, const int32_t* cnt_dev, double* A_dev, double* Dp_dev) {
+  Matern K;
+  K.s2 = sigma2;
+  K.rho = rho;
+  if (nu == 0.5) { K.nu = 0; K.c = 1.0 / rho; }
+  else if (nu == 1.5) { K.nu = 1; K.c = sqrt(3.0) / rho; }
+  else if (nu == 2.5) { K.nu = 2; K.c = sqrt(5.0) / rho; }
+  else fail(kEConfig, "smoothness nu must be one of (0.5, 1.5, 2.5)");
+  if (np == 0) return;
+  if (take < 1 || take > 256) fail(kECapacity, "prediction neighbour count must be in [1, 256]");
+  DevBuf err;
+  err.alloc(sizeof(int) * 4);
+  int h_err[4] = {0, INT32_MAX, INT32_MAX, 0};
+  VL_CUDA(cudaMemcpyAsync(err.p, h_err, sizeof(h_err), cudaMemcpyHostToDevice, C.stream));
+  const size_t per = warp_scratch_doubles(take, P.d);
+  auto go = [&](auto qq) {
+    constexpr int Q = decltype(qq)::value;
+    if (P.d == 2) launch_pred<Q, 2>(C, P, K, np, take, qxy_dev, nbr_dev, cnt_dev, A_dev, Dp_dev, err.as<int>(), per);
+    else if (P.d == 1) launch_pred<Q, 1>(C, P, K, np, take, qxy_dev, nbr_dev, cnt_dev, A_dev, Dp_dev, err.as<int>(), per);
+    else launch_pred<Q, 0>(C, P, K, np, take, qxy_dev, nbr_dev, cnt_dev, A_dev, Dp_dev, err.as<int>(), per);
+  };
+  if (take <= 32) go(std::integral_constant<int, 1>{});
+  else if (take <= 64) go(std::integral_constant<int, 2>{});
+  else if (take <= 128) go(std::integral_constant<int, 4>{});
+  else go(std::integral_constant<int, 8>{});
+  VL_CUDA(cudaMemcpyAsync(h_err, err.p, sizeof(h_err), cudaMemcpyDeviceToHost, C.stream));
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+  if (h_err[0] && h_err[1] != INT32_MAX)
+    fail(kEFactorization, "neighbor covariance submatrix of prediction point " + std::to_string(h_err[1]) +
+                              " is not positive definite");
 }
 
 }  // namespace vl

@@ -39,6 +39,7 @@ struct Lik {
   VL_D double logdens(double y, double mu) const {
     if (fam == 0) return y * mu - logaddexp0(mu);
     if (fam == 1) return log_ndtr((2.0 * y - 1.0) * mu);
+    if (fam == 3) return y * mu - exp(mu) - lgamma(y + 1.0);
     return aloga + (a - 1.0) * log(y) - a * mu - a * y * exp(-mu);
   }
   // returns log p and writes d1, d2, d3
@@ -56,6 +57,11 @@ struct Lik {
       d1 = z * g;
       d2 = -g * (u + g);
       d3 = z * g * ((u + g) * (u + g) + g * (u + g) - 1.0);
+    } else if (fam == 3) {  // Poisson, log link (the prediction config's family; test-registered in the reference)
+      const double e = exp(mu);
+      d1 = y - e;
+      d2 = -e;
+      d3 = -e;
     } else {
       const double w = a * y * exp(-mu);
       d1 = -a + w;
@@ -71,7 +77,7 @@ static Lik make_lik(const LikSpec& L) {
   k.fam = L.family;
   k.a = L.shape;
   k.aloga = (L.family == 2) ? L.shape * std::log(L.shape) - std::lgamma(L.shape) : 0.0;
-  if (L.family < 0 || L.family > 2) fail(kEConfig, "unknown likelihood family");
+  if (L.family < 0 || L.family > 3) fail(kEConfig, "unknown likelihood family");
   if (L.family == 2 && !(L.shape > 0)) fail(kEConfig, "gamma shape must be > 0");
   return k;
 }

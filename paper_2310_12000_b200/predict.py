@@ -1,0 +1,319 @@
+"""Latent predictive distributions on the device (reference predict.py and
+vecchia.py:364-441).
+
+    omega_p = F_p - Bpo b*,
+    Omega_p = diag(Dp) + Bpo (W + SigmaTilde^-1)^-1 Bpo^T      (Bp = I).
+
+``prediction_blocks`` finds each prediction point's nearest training points
+with the device kNN and builds Bpo / Dp with the factor-build warp kernel;
+``latent_var_sim`` runs the reference's unbiased simulation estimator with
+the samples batched as the columns of one multi-RHS PCG (same draws, same
+per-sample CG recurrence, accumulation in sample order); samples shard across
+ranks with one n_p-vector allreduce.  Response moments and the
+scoring rules are small host computations, as in the reference.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+from . import device as dev
+from .covariance import Locations
+from .errors import CapabilityError, CapacityError, ConfigError, DataError, NumericalError
+from .vecchia import knn_query
+
+
+class PredictionBlocks:
+    """Device-resident blocks linking n_p prediction points to a trained
+    factor (vecchia.py:364-390): Bpo (n_p x n, rows = -K^-1 k over the take
+    nearest training points, factor-order columns) and Dp."""
+
+    def __init__(self, factor, handle, neighbors, n_p, take):
+        self.factor = factor
+        self.h = handle
+        self._nbr = neighbors  # (n_p, take) factor-order training indices
+        self._n_p = n_p
+        self.take = take
+        self._Dp = None
+        self._vals = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                _lib.lib().vl_pred_destroy(self.h)
+        except Exception:
+            pass
+
+    @property
+    def n_p(self):
+        return self._n_p
+
+    @property
+    def neighbors(self):
+        return [row.copy() for row in self._nbr]
+
+    @property
+    def Dp(self):
+        if self._Dp is None:
+            self._Dp = np.empty(self.n_p)
+            if self.n_p:
+                _lib.call("vl_pred_get", self.factor.ctx.h, self.h, 1, _lib.ptr(self._Dp))
+        return self._Dp
+
+    @property
+    def values(self):
+        """Bpo values (n_p, take), neighbour order."""
+        if self._vals is None:
+            self._vals = np.empty((self.n_p, self.take))
+            if self.n_p:
+                _lib.call("vl_pred_get", self.factor.ctx.h, self.h, 0, _lib.ptr(self._vals))
+        return self._vals
+
+    @property
+    def Bpo(self):
+        n = self.factor.n
+        indptr = np.arange(0, (self.n_p + 1) * self.take, self.take)
+        return sp.csr_matrix((self.values.ravel(), self._nbr.ravel(), indptr), shape=(self.n_p, n))
+
+    def bp_solve(self, v, transpose=False):
+        return np.asarray(v, dtype=float)
+
+    def conditional_mean_term(self, b):
+        return -(self.Bpo @ b)
+
+    def rhs_matrix(self):
+        return self.Bpo.T.tocsc()
+
+
+def prediction_blocks(factor, pred_locs, m=None, spec=None):
+    """Blocks for n_p prediction points (vecchia.py:393-441): each point
+    conditions on its min(m, n) nearest training points; a point within
+    1e-12 of a training point is rejected (DataError)."""
+    spec = factor.spec if spec is None else spec
+    m = factor.m if m is None else m
+    pred = pred_locs.coords if isinstance(pred_locs, Locations) else np.atleast_2d(np.asarray(pred_locs, float))
+    n, n_p = factor.n, pred.shape[0]
+    if m < 1:
+        raise ConfigError("prediction requires m >= 1")
+    take = min(m, n)
+    h = C.c_void_p()
+    if n_p == 0:
+        _lib.call("vl_pred_create", factor.ctx.h, factor.pattern.h, float(spec.sigma2), float(spec.rho),
+                  float(spec.nu), None, 0, None, take, C.byref(h))
+        return PredictionBlocks(factor, h, np.zeros((0, take), dtype=np.int64), 0, take)
+    pred = np.ascontiguousarray(pred, dtype=float)
+    idx, dmin = knn_query(factor.coords, pred, take)
+    if np.any(dmin <= 1e-12):
+        bad = int(np.argmin(dmin))
+        raise DataError(f"prediction point {bad} duplicates training point {int(idx[bad, 0])}")
+    nb32 = np.ascontiguousarray(idx, dtype=np.int32)
+    _lib.call("vl_pred_create", factor.ctx.h, factor.pattern.h, float(spec.sigma2), float(spec.rho), float(spec.nu),
+              _lib.ptr(pred), n_p, _lib.ptr(nb32), take, C.byref(h))
+    return PredictionBlocks(factor, h, idx, n_p, take)
+
+
+@dataclass
+class PredictiveDistribution:
+    omega: np.ndarray
+    var: np.ndarray
+    method: str
+    params: dict = field(default_factory=dict)
+    cov: np.ndarray | None = None
+    response_mean: np.ndarray | None = None
+    response_var: np.ndarray | None = None
+    response_samples: np.ndarray | None = None
+
+    @property
+    def n_p(self):
+        return self.omega.shape[0]
+
+
+def latent_mean(state, blocks, F_p):
+    """omega_p = F_p - Bpo b* (predict.py:45-50)."""
+    F_p = np.ascontiguousarray(np.asarray(F_p, dtype=float))
+    if F_p.shape[0] != blocks.n_p:
+        raise ConfigError("F_p length must match the number of prediction points")
+    if blocks.n_p == 0:
+        return np.empty(0)
+    ctx = blocks.factor.ctx
+    Fd = dev.upload(ctx, F_p)
+    out = dev.empty(ctx, blocks.n_p)
+    _lib.call("vl_pred_mean", ctx.h, blocks.h, _lib.ptr(state._dev["b"]), _lib.ptr(Fd), _lib.ptr(out))
+    return dev.download(out)
+
+
+def latent_var_sim(state, factor, blocks, s=2000, seed=0, cfg=None, full=False, chunk=64, comm=None):
+    """Unbiased simulation estimator of diag(Omega_p) (and the full matrix when
+    ``full``), predict.py:70-101: per sample z1, z2 ~ N(0, I) drawn in that
+    order from default_rng(seed), z3 = W^1/2 z1 + B^T D^-1/2 z2,
+    u = (W + SigmaTilde^-1)^-1 z3 at cfg.cg_tol, z4 = Bpo u.  ``chunk``
+    samples run as the columns of one multi-RHS solve; with ``comm`` the
+    samples are split contiguously across ranks (each rank replays the shared
+    stream) and the accumulators are summed."""
+    from .laplace import BackendConfig, build_preconditioner, solve_system
+
+    if s < 2:
+        raise ConfigError("simulation needs s >= 2")
+    cfg = BackendConfig() if cfg is None else cfg
+    rng = np.random.default_rng(seed)
+    n, n_p = factor.n, blocks.n_p
+    ctx, pat = factor.ctx, factor.pattern
+    P = build_preconditioner(factor, state._dev["W"], cfg) if cfg.preconditioner == "lrac" else None
+    lo, hi = 0, s
+    if comm is not None and comm.world > 1:
+        from .distributed import shard_bounds
+        lo, hi = shard_bounds(s, comm.world, comm.rank)
+    acc = dev.zeros(ctx, max(n_p, 1))
+    cov = dev.zeros(ctx, n_p, n_p) if full else None
+    done = 0
+    while done < s:
+        c = min(chunk, s - done)
+        G = rng.standard_normal((2 * c, n))  # z1_0, z2_0, z1_1, z2_1, ... (the reference's draw order)
+        a, b = max(lo, done), min(hi, done + c)
+        if a < b:
+            sel = slice(2 * (a - done), 2 * (b - done))
+            Gs = G[sel]
+            k = b - a
+            z1 = pat.to_dev(np.ascontiguousarray(Gs[0::2].T))
+            z2 = pat.to_dev(np.ascontiguousarray(Gs[1::2].T))
+            z3 = dev.empty(ctx, n, k)
+            _lib.call("vl_pred_z3", ctx.h, factor.h, _lib.ptr(state._dev["W"]), k, _lib.ptr(z1), _lib.ptr(z2),
+                      _lib.ptr(z3))
+            u, _ = solve_system(factor, state, z3, cfg, P=P)
+            if n_p:
+                _lib.call("vl_pred_accum", ctx.h, blocks.h, _lib.ptr(u), k, _lib.ptr(acc),
+                          _lib.ptr(cov) if full else None)
+        done += c
+    if comm is not None and comm.world > 1:
+        comm.allreduce_(acc)
+        if full:
+            comm.allreduce_(cov)
+    Dp = blocks.Dp
+    accv = dev.download(acc)[:n_p]
+    if full:
+        covm = dev.download(cov).reshape(n_p, n_p)
+        return Dp + np.diag(covm) / s, np.diag(Dp) + covm / s
+    return Dp + accv / s
+
+
+def latent_var_exact(state, factor, blocks, full=False):
+    """Exact diag(Omega_p) by a dense Cholesky of W + SigmaTilde^-1 on the device
+    (predict.py:53-67; n <= 5000, full only for n_p <= 2000)."""
+    if factor.n > 5000:
+        raise CapacityError("exact predictive variances limited to n <= 5000")
+    if full and blocks.n_p > 2000:
+        raise CapacityError("full predictive covariance limited to n_p <= 2000")
+    T = dev.torch()
+    tdev = factor.ctx.tdev
+    B = T.tensor(factor.B.toarray(), dtype=T.float64, device=tdev)
+    D = T.tensor(factor.D, dtype=T.float64, device=tdev)
+    A = B.T @ (B / D[:, None])
+    A.diagonal().add_(T.tensor(state.W, dtype=T.float64, device=tdev))
+    L = T.linalg.cholesky(A)
+    RT = T.tensor(blocks.rhs_matrix().toarray(), dtype=T.float64, device=tdev)
+    S = T.cholesky_solve(RT, L)
+    Dp = blocks.Dp
+    var = Dp + (RT * S).sum(dim=0).cpu().numpy()
+    if full:
+        return var, np.diag(Dp) + (RT.T @ S).cpu().numpy()
+    return var
+
+
+def predict_latent(state, factor, blocks, F_p, method="simulation", cfg=None, s=2000, seed=0, k=100,
+                   variant="none", full=False, comm=None):
+    """Latent predictive distribution with the chosen variance method
+    (predict.py:269-300)."""
+    omega = latent_mean(state, blocks, F_p)
+    cov = None
+    if method == "exact":
+        if full:
+            var, cov = latent_var_exact(state, factor, blocks, full=True)
+        else:
+            var = latent_var_exact(state, factor, blocks)
+        params = {}
+    elif method == "simulation":
+        if full:
+            var, cov = latent_var_sim(state, factor, blocks, s=s, seed=seed, cfg=cfg, full=True, comm=comm)
+        else:
+            var = latent_var_sim(state, factor, blocks, s=s, seed=seed, cfg=cfg, comm=comm)
+        params = {"s": s, "seed": seed}
+    elif method == "lanczos":
+        raise CapabilityError("the Lanczos variance variants are not available on the device backend")
+    else:
+        raise ConfigError(f"unknown variance method {method!r}")
+    return PredictiveDistribution(omega, var, method, params, cov=cov)
+
+
+def response_moments(pred, lik, method="simulation", n_s=2000, seed=0):
+    """Response-scale predictive moments (predict.py:185-213)."""
+    if method == "closed-form":
+        if lik.name != "gamma":
+            raise CapabilityError(f"closed-form response moments unavailable for {lik.name}")
+        pred.response_mean = np.exp(pred.omega + pred.var / 2.0)
+        return pred
+    if method != "simulation":
+        raise ConfigError(f"unknown response-moment method {method!r}")
+    if n_s < 2:
+        raise ConfigError("simulation needs n_s >= 2")
+    rng = np.random.default_rng(seed)
+    sd = np.sqrt(np.maximum(pred.var, 0.0))
+    mu_draws = pred.omega[None, :] + sd[None, :] * rng.standard_normal((n_s, pred.n_p))
+    samples = lik.sample(mu_draws, rng)
+    pred.response_mean = samples.mean(axis=0)
+    pred.response_var = samples.var(axis=0, ddof=1)
+    pred.response_samples = samples
+    return pred
+
+
+def rmse(estimate, truth):
+    estimate = np.asarray(estimate, dtype=float)
+    truth = np.asarray(truth, dtype=float)
+    return float(np.sqrt(np.mean((estimate - truth) ** 2)))
+
+
+def gaussian_log_score(omega, var, truth):
+    """-sum_i log N(truth_i; omega_i, var_i)."""
+    var = np.asarray(var, dtype=float)
+    if np.any(var <= 0):
+        raise NumericalError("non-positive predictive variance: Gaussian log score undefined")
+    omega = np.asarray(omega, dtype=float)
+    truth = np.asarray(truth, dtype=float)
+    return float(np.sum(0.5 * np.log(2.0 * np.pi * var) + (truth - omega) ** 2 / (2.0 * var)))
+
+
+def crps_from_samples(samples, truth):
+    """Mean CRPS from predictive samples (probability-weighted moments)."""
+    samples = np.asarray(samples, dtype=float)
+    truth = np.asarray(truth, dtype=float)
+    m = samples.shape[0]
+    if m < 2:
+        raise ConfigError("CRPS needs at least two samples per point")
+    xs = np.sort(samples, axis=0)
+    term_abs = np.abs(samples - truth[None, :]).mean(axis=0)
+    beta0 = samples.mean(axis=0)
+    weights = np.arange(m, dtype=float)
+    beta1 = (weights[:, None] * xs).sum(axis=0) / (m * (m - 1.0))
+    return float(np.mean(term_abs + beta0 - 2.0 * beta1))
+
+
+def scores(pred, truth, kind):
+    """Scoring rules against held-out truth (predict.py:249-266)."""
+    if kind == "rmse":
+        return rmse(pred.omega, truth)
+    if kind == "log-score":
+        return gaussian_log_score(pred.omega, pred.var, truth)
+    if kind == "crps":
+        if pred.response_samples is None:
+            raise ConfigError("crps needs simulated response samples")
+        return crps_from_samples(pred.response_samples, truth)
+    raise ConfigError(f"unknown score {kind!r}; choose rmse, log-score or crps")
+
+
+__all__ = ["PredictionBlocks", "PredictiveDistribution", "prediction_blocks", "latent_mean", "latent_var_sim",
+           "latent_var_exact", "predict_latent", "response_moments", "rmse", "gaussian_log_score",
+           "crps_from_samples", "scores"]

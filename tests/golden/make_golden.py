@@ -109,6 +109,75 @@ def laplace_case(name, n, seed, rho, m, t, precond="vadu", family="bernoulli-log
     print(f"{name}: n={n} nll={val:.12g} dtheta={grad['dtheta']} newton={st.newton_iters}")
 
 
+def register_poisson():
+    """Test-only Poisson (log link) family registered into the REFERENCE so the
+    rest of its pipeline runs unmodified (config 4 has no
+    reference family)."""
+    import vlgp.likelihoods as L
+    from scipy.special import gammaln
+
+    if "poisson" in L._FAMILIES:
+        return
+
+    class Poisson(L.Likelihood):
+        name = "poisson"
+
+        def validate(self, y):
+            return np.asarray(y, dtype=float)
+
+        def log_density(self, y, mu):
+            return y * mu - np.exp(mu) - gammaln(y + 1.0)
+
+        def derivs(self, y, mu):
+            e = np.exp(mu)
+            return float(self.log_density(y, mu).sum()), y - e, -e, -e
+
+        def sample(self, mu, rng):
+            return rng.poisson(np.exp(mu)).astype(float)
+
+    L._FAMILIES["poisson"] = Poisson
+
+
+def predict_case(name, n, n_p, seed, rho, m, family="poisson", s=24, sim_seed=11, nu=1.5, ordering_seed=7):
+    """Prediction path (config-4 shaped, scaled down): prediction_blocks,
+    latent_mean, latent_var_sim (diag + full) and latent_var_exact."""
+    from vlgp.covariance import CovarianceSpec, cov_matrix
+    from vlgp.laplace import BackendConfig, find_mode
+    from vlgp.likelihoods import get_likelihood
+    from vlgp.predict import latent_mean, latent_var_exact, latent_var_sim
+    from vlgp.vecchia import build_factor, find_neighbors, order_random, prediction_blocks
+
+    register_poisson()
+    rng = np.random.default_rng(seed)
+    allc = rng.uniform(size=(n + n_p, 2))
+    spec = CovarianceSpec(1.0, rho, nu)
+    ball = np.linalg.cholesky(cov_matrix(spec, allc)) @ rng.standard_normal(n + n_p)
+    coords, pcoords = allc[:n], allc[n:]
+    lik = get_likelihood(family)
+    y = lik.sample(ball[:n], rng)
+    perm = order_random(n, ordering_seed)
+    nb = find_neighbors(coords, perm, m)
+    f = build_factor(coords, spec, nb, perm)
+    cfg = BackendConfig(preconditioner="vadu", t=8, probe_seed=3)
+    st = find_mode(f, lik, y[perm], np.zeros(n), cfg)
+    blocks = prediction_blocks(f, pcoords)
+    Fp = np.zeros(n_p)
+    omega = latent_mean(st, blocks, Fp)
+    var_sim, cov_sim = latent_var_sim(st, f, blocks, s=s, seed=sim_seed, cfg=cfg, full=True)
+    var_exact = latent_var_exact(st, f, blocks)
+    nbr = np.full((n, m), -1, dtype=np.int64)
+    for i, q in enumerate(nb):
+        nbr[i, : len(q)] = q
+    out = dict(n=n, n_p=n_p, m=m, seed=seed, rho=rho, nu=nu, sigma2=1.0, family=family, shape=1.0,
+               precond="vadu", t=8, probe_seed=3, cg_tol=cfg.cg_tol, coords=coords, pcoords=pcoords, y=y,
+               F=np.zeros(n), perm=perm, nbr=nbr, b=st.b, W=st.W, newton_iters=st.newton_iters,
+               pred_nbr=np.stack(blocks.neighbors).astype(np.int64), Bpo_vals=blocks.Bpo.data.reshape(n_p, -1),
+               Dp=blocks.Dp, omega=omega, s=s, sim_seed=sim_seed, var_sim=var_sim, cov_sim=cov_sim,
+               var_exact=var_exact, truth=ball[n:])
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(f"{name}: n={n} n_p={n_p} newton={st.newton_iters} var_sim[:3]={var_sim[:3]}")
+
+
 def knn_case(name, n, m, seed, ordering_seed):
     from vlgp.vecchia import find_neighbors, order_random
 
@@ -137,6 +206,9 @@ def main():
     laplace_case("gamma_lrac_cov_n300", 300, seed=17, rho=0.1, m=8, t=6, precond="lrac", rank=25,
                  family="gamma", shape=1.5, nu=2.5, p=2)
     knn_case("knn_n6000_m12", 6000, 12, seed=21, ordering_seed=22)
+    register_poisson()
+    laplace_case("poisson_vadu_n300", 300, seed=18, rho=0.1, m=8, t=6, family="poisson")
+    predict_case("poisson_pred_n500", 500, 60, seed=19, rho=0.1, m=10)
 
 
 if __name__ == "__main__":

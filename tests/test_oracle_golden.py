@@ -88,3 +88,21 @@ def test_matern_anchors():
     r = 0.2
     assert O.matern(r, 1.0, r, 1.5) == pytest.approx((1 + np.sqrt(3)) * np.exp(-np.sqrt(3)), rel=1e-14)
     assert O.matern_drho(r, 1.0, r, 1.5) == pytest.approx(3 * np.exp(-np.sqrt(3)) / r, rel=1e-14)
+
+
+def test_prediction_oracle_matches_reference():
+    g = load("poisson_pred_n500")
+    perm = g["perm"]
+    xy = g["coords"][perm]
+    s2, rho, nu = scal(g, "sigma2"), scal(g, "rho"), scal(g, "nu")
+    nbr, vals, Dp = O.prediction_blocks(xy, g["pcoords"], int(g["m"]), s2, rho, nu)
+    np.testing.assert_array_equal(nbr, g["pred_nbr"])
+    np.testing.assert_allclose(vals, g["Bpo_vals"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(Dp, g["Dp"], rtol=1e-12)
+    omega = O.latent_mean(g["b"], nbr, vals, np.zeros(len(Dp)))
+    np.testing.assert_allclose(omega, g["omega"], rtol=1e-12, atol=1e-14)
+    f = O.vecchia_factor(xy, g["nbr"], s2, rho, nu)
+    var, cov = O.latent_var_sim(f, g["W"], nbr, vals, Dp, int(g["s"]), int(g["sim_seed"]), float(g["cg_tol"]),
+                                full=True)
+    np.testing.assert_allclose(var, g["var_sim"], rtol=1e-9)
+    np.testing.assert_allclose(cov, g["cov_sim"], rtol=1e-9, atol=1e-13)
