@@ -147,20 +147,24 @@ def latent_mean(state, blocks, F_p):
     return dev.download(out)
 
 
-def latent_var_sim(state, factor, blocks, s=2000, seed=0, cfg=None, full=False, chunk=64, comm=None):
+def latent_var_sim(state, factor, blocks, s=2000, seed=0, cfg=None, full=False, chunk=64, comm=None, rng="numpy"):
     """Unbiased simulation estimator of diag(Omega_p) (and the full matrix when
     ``full``), predict.py:70-101: per sample z1, z2 ~ N(0, I) drawn in that
     order from default_rng(seed), z3 = W^1/2 z1 + B^T D^-1/2 z2,
     u = (W + SigmaTilde^-1)^-1 z3 at cfg.cg_tol, z4 = Bpo u.  ``chunk``
     samples run as the columns of one multi-RHS solve; with ``comm`` the
     samples are split contiguously across ranks (each rank replays the shared
-    stream) and the accumulators are summed."""
+    stream) and the accumulators are summed.  ``rng="device"`` draws the
+    normals on the GPU instead (Philox; statistically equivalent, not the
+    reference's stream), which removes the host generation cost at large n*s."""
     from .laplace import BackendConfig, build_preconditioner, solve_system
 
     if s < 2:
         raise ConfigError("simulation needs s >= 2")
     cfg = BackendConfig() if cfg is None else cfg
-    rng = np.random.default_rng(seed)
+    if rng not in ("numpy", "device"):
+        raise ConfigError("rng must be 'numpy' or 'device'")
+    host_rng = np.random.default_rng(seed) if rng == "numpy" else None
     n, n_p = factor.n, blocks.n_p
     ctx, pat = factor.ctx, factor.pattern
     P = build_preconditioner(factor, state._dev["W"], cfg) if cfg.preconditioner == "lrac" else None
@@ -173,14 +177,20 @@ def latent_var_sim(state, factor, blocks, s=2000, seed=0, cfg=None, full=False, 
     done = 0
     while done < s:
         c = min(chunk, s - done)
-        G = rng.standard_normal((2 * c, n))  # z1_0, z2_0, z1_1, z2_1, ... (the reference's draw order)
+        G = host_rng.standard_normal((2 * c, n)) if host_rng is not None else None  # z1_0, z2_0, z1_1, ...
         a, b = max(lo, done), min(hi, done + c)
         if a < b:
-            sel = slice(2 * (a - done), 2 * (b - done))
-            Gs = G[sel]
             k = b - a
-            z1 = pat.to_dev(np.ascontiguousarray(Gs[0::2].T))
-            z2 = pat.to_dev(np.ascontiguousarray(Gs[1::2].T))
+            if G is not None:
+                Gs = G[2 * (a - done):2 * (b - done)]
+                z1 = pat.to_dev(np.ascontiguousarray(Gs[0::2].T))
+                z2 = pat.to_dev(np.ascontiguousarray(Gs[1::2].T))
+            else:
+                T = dev.torch()
+                gen = T.Generator(device=ctx.tdev)
+                gen.manual_seed(int(seed) * 1000003 + a)
+                z1 = T.randn((n, k), generator=gen, dtype=T.float64, device=ctx.tdev)
+                z2 = T.randn((n, k), generator=gen, dtype=T.float64, device=ctx.tdev)
             z3 = dev.empty(ctx, n, k)
             _lib.call("vl_pred_z3", ctx.h, factor.h, _lib.ptr(state._dev["W"]), k, _lib.ptr(z1), _lib.ptr(z2),
                       _lib.ptr(z3))
