@@ -45,3 +45,4 @@ from .predict import (
     rmse,
     scores,
 )
+from .estimate import FitConfig, FitResult, fit, glm_initial_beta, initial_parameters, profile_xi

@@ -178,6 +178,26 @@ def predict_case(name, n, n_p, seed, rho, m, family="poisson", s=24, sim_seed=11
     print(f"{name}: n={n} n_p={n_p} newton={st.newton_iters} var_sim[:3]={var_sim[:3]}")
 
 
+def fit_case(name, n, seed, rho, m, t, family="bernoulli-logit", p=2, max_iters=6, shape=2.0):
+    """The reference's fit() driver (Nesterov + backtracking) on a small problem."""
+    from vlgp.estimate import FitConfig, fit
+    from vlgp.laplace import BackendConfig
+
+    rng_x = np.random.default_rng(seed + 99)
+    X = np.column_stack([np.ones(n)] + [rng_x.standard_normal(n) for _ in range(p - 1)])
+    F = X @ np.linspace(0.2, -0.3, p)
+    coords, y, lik = simulate(n, seed, rho, family=family, shape=shape, F=F)
+    cfg = FitConfig(m=m, ordering_seed=4, max_iters=max_iters,
+                    backend=BackendConfig(preconditioner="vadu", t=t, probe_seed=9, cg_tol=1e-6))
+    res = fit(y, X, coords, lik, cfg)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), n=n, m=m, t=t, family=family, shape=shape, coords=coords,
+                        y=y, X=X, max_iters=max_iters, theta=res.theta, beta=res.beta, xi=res.xi,
+                        objective=res.objective, trace_obj=np.array([r["objective"] for r in res.trace]),
+                        trace_lr=np.array([r["lr"] for r in res.trace]), n_evaluations=res.n_evaluations,
+                        iterations=res.iterations, converged=res.converged)
+    print(f"{name}: theta={res.theta} beta={res.beta} obj={res.objective:.10g} evals={res.n_evaluations}")
+
+
 def knn_case(name, n, m, seed, ordering_seed):
     from vlgp.vecchia import find_neighbors, order_random
 
@@ -209,6 +229,8 @@ def main():
     register_poisson()
     laplace_case("poisson_vadu_n300", 300, seed=18, rho=0.1, m=8, t=6, family="poisson")
     predict_case("poisson_pred_n500", 500, 60, seed=19, rho=0.1, m=10)
+    fit_case("fit_logit_n400", 400, seed=23, rho=0.1, m=10, t=8)
+    fit_case("fit_gamma_n300", 300, seed=24, rho=0.1, m=8, t=6, family="gamma", max_iters=4)
 
 
 if __name__ == "__main__":
