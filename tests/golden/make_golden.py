@@ -198,6 +198,43 @@ def fit_case(name, n, seed, rho, m, t, family="bernoulli-logit", p=2, max_iters=
     print(f"{name}: theta={res.theta} beta={res.beta} obj={res.objective:.10g} evals={res.n_evaluations}")
 
 
+def cli_case(name):
+    """The reference's own file formats end to end: cmd_simulate -> cmd_fit
+    (model JSON) -> cmd_predict (predictions CSV), committed as fixtures."""
+    import json
+
+    from vlgp.cli import cmd_fit, cmd_predict, cmd_simulate
+
+    d = os.path.join(HERE, name)
+    os.makedirs(d, exist_ok=True)
+    from vlgp.cli import _read_csv, _write_csv
+
+    sim = {"n": 300, "d": 2, "likelihood": {"family": "bernoulli-logit"},
+           "covariance": {"sigma2": 1.0, "rho": 0.1, "nu": 1.5},
+           "fixed_effects": {"beta": [0.3], "design": "intercept"}, "seeds": {"simulation": 31}}
+    full = os.path.join(d, "all.csv")
+    cmd_simulate(sim, full)
+    h, a = _read_csv(full)
+    _, tr = _read_csv(os.path.join(d, "all.truth.csv"))
+    data = os.path.join(d, "train.csv")
+    pred_in = os.path.join(d, "pred.csv")
+    _write_csv(data, h, a[:260].tolist())
+    _write_csv(pred_in, h + ["b"], np.column_stack([a[260:], tr[260:, 0]]).tolist())
+    os.remove(full)
+    os.remove(os.path.join(d, "all.truth.csv"))
+    fitcfg = {"likelihood": {"family": "bernoulli-logit"}, "m": 10, "nu": 1.5,
+              "backend": {"preconditioner": "vadu", "t": 8, "cg_tol": 1e-6},
+              "optimizer": {"max_iters": 4}, "seeds": {"ordering": 5, "probes": 6}}
+    with open(os.path.join(d, "fit.json"), "w") as fh:
+        json.dump(fitcfg, fh)
+    cmd_fit(data, fitcfg, os.path.join(d, "model.json"))
+    predcfg = {"prediction": {"method": "exact"}, "scores": ["rmse", "log-score"]}
+    with open(os.path.join(d, "predict.json"), "w") as fh:
+        json.dump(predcfg, fh)
+    cmd_predict(os.path.join(d, "model.json"), data, pred_in, predcfg, os.path.join(d, "predictions.csv"))
+    print(f"{name}: written to {d}")
+
+
 def knn_case(name, n, m, seed, ordering_seed):
     from vlgp.vecchia import find_neighbors, order_random
 
@@ -231,6 +268,7 @@ def main():
     predict_case("poisson_pred_n500", 500, 60, seed=19, rho=0.1, m=10)
     fit_case("fit_logit_n400", 400, seed=23, rho=0.1, m=10, t=8)
     fit_case("fit_gamma_n300", 300, seed=24, rho=0.1, m=8, t=6, family="gamma", max_iters=4)
+    cli_case("cli_logit")
 
 
 if __name__ == "__main__":
