@@ -119,14 +119,32 @@ VL_D void grid_finalize(const double* partials, unsigned* counter, int t, const 
   __syncthreads();
   if (s_ticket != (unsigned)nb - 1) return;
   __threadfence();
-  for (int idx = threadIdx.x; idx < NR * t; idx += blockDim.x) {
+  // one warp per output: lane l folds slots l, l+32, ... in order, then a
+  // fixed xor tree -> deterministic, and ~nb/32 independent loads per lane
+  // instead of one thread walking nb dependent-latency loads
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int idx = threadIdx.x >> 5; idx < NR * t; idx += nw) {
     const int r = idx / t;
+    const bool mx = (MAXMASK >> r) & 1;
     double s = 0.0;
-    for (int b = 0; b < nb; ++b) {
-      double v = __ldcg(partials + (size_t)b * NR * t + idx);
-      s = ((MAXMASK >> r) & 1) ? fmax(s, v) : s + v;
+    int b = lane;
+    for (; b + 96 < nb; b += 128) {
+      const double v0 = __ldcg(partials + (size_t)b * NR * t + idx);
+      const double v1 = __ldcg(partials + (size_t)(b + 32) * NR * t + idx);
+      const double v2 = __ldcg(partials + (size_t)(b + 64) * NR * t + idx);
+      const double v3 = __ldcg(partials + (size_t)(b + 96) * NR * t + idx);
+      s = mx ? fmax(fmax(fmax(fmax(s, v0), v1), v2), v3) : (((s + v0) + v1) + v2) + v3;
     }
-    sh[idx] = s;
+    for (; b < nb; b += 32) {
+      const double v = __ldcg(partials + (size_t)b * NR * t + idx);
+      s = mx ? fmax(s, v) : s + v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double other = __shfl_xor_sync(0xffffffffu, s, o);
+      s = mx ? fmax(s, other) : s + other;
+    }
+    if (lane == 0) sh[idx] = s;
   }
   __syncthreads();
   fin(sh, t);
