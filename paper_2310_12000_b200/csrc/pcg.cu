@@ -117,6 +117,26 @@ struct K3Rhs {
   }
   VL_D void out(int64_t, int, double, double&) const {}
 };
+// t > 1: the update stays fused into the solve's rhs (the solve is gather-
+// bound there, and deferring would add a pass over r, u, v per iteration)
+struct K3RhsFused {
+  double* r;
+  double* u;
+  const double* v;
+  const double* h;
+  const double* alpha;
+  int ld;
+  VL_D double rhs(int64_t s, int c, double& acc) const {
+    const int64_t o = s * ld + c;
+    const double al = alpha[c];  // 0 for frozen columns
+    const double rn = fma(-al, v[o], r[o]);
+    r[o] = rn;
+    u[o] = fma(al, h[o], u[o]);
+    acc += rn * rn;
+    return rn;
+  }
+  VL_D void out(int64_t, int, double, double&) const {}
+};
 // ---- deferred update: r -= alpha v, u += alpha h; then h = z + beta h -------
 template <bool HUPD>
 struct DeferBody {
@@ -193,6 +213,7 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
 
   dispatch_cols(t, ld, [&](auto g, auto nu, auto uu) {
     constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
+    constexpr bool DEFER = (G == 1 && NU == 1 && U == 1);  // single RHS: r/u updates deferred
     // init
     ProfScope ps_init(C, t == 1 ? "cg1_init" : "cgT_init", 0.0);
     launch_rows<G, NU, U, 1, 0>(C, n, t, InitBody{b, r.as<double>(), u, hb[0], ld}, InitFin{K, tol});
@@ -210,10 +231,13 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
         double* hn = hb[0];
         {
           ProfScope ps(C, t == 1 ? "cg1_hupd" : "cgT_hupd", 24.0 * n * t);
-          launch_rows<G, NU, U, 0, 0>(C, n, t,
-                                      DeferBody<true>{z.as<double>(), hn, r.as<double>(), u, v.as<double>(),
-                                                      K.alpha, K.beta, ld},
-                                      Fin0<0>{}, gate);
+          if constexpr (DEFER)
+            launch_rows<G, NU, U, 0, 0>(C, n, t,
+                                        DeferBody<true>{z.as<double>(), hn, r.as<double>(), u, v.as<double>(),
+                                                        K.alpha, K.beta, ld},
+                                        Fin0<0>{}, gate);
+          else
+            launch_rows<G, NU, U, 0, 0>(C, n, t, HUpdBody{z.as<double>(), hn, K.beta, ld}, Fin0<0>{}, gate);
         }
         {
           ProfScope ps(C, t == 1 ? "cg1_spmm_B" : "cgT_spmm_B", bapply_bytes(P, t, 1));
@@ -226,15 +250,19 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
         }
         {
           ProfScope ps(C, t == 1 ? "cg1_trsv_Bt" : "cgT_trsv_Bt", bapply_bytes(P, t, 0));
-          launch_trsv<G, NU, U, 1>(C, F, false, t, ld, dbw, w.as<double>(),
-                                   K3Rhs{r.as<double>(), v.as<double>(), K.alpha, ld},
-                                   K3Fin{K, l}, gate);
+          if constexpr (DEFER)
+            launch_trsv<G, NU, U, 1>(C, F, false, t, ld, dbw, w.as<double>(),
+                                     K3Rhs{r.as<double>(), v.as<double>(), K.alpha, ld}, K3Fin{K, l}, gate);
+          else
+            launch_trsv<G, NU, U, 1>(C, F, false, t, ld, dbw, w.as<double>(),
+                                     K3RhsFused{r.as<double>(), u, v.as<double>(), hn, K.alpha, ld}, K3Fin{K, l},
+                                     gate);
         }
         {
           ProfScope ps(C, t == 1 ? "cg1_trsv_B" : "cgT_trsv_B", bapply_bytes(P, t, 1));
           launch_trsv<G, NU, U, 1>(C, F, true, t, ld, dfw, z.as<double>(),
-                                   RhsScaleDot<true>{w.as<double>(), S.dinv, r.as<double>(), v.as<double>(),
-                                                     K.alpha, ld},
+                                   RhsScaleDot<DEFER>{w.as<double>(), S.dinv, r.as<double>(), v.as<double>(),
+                                                      K.alpha, ld},
                                    K4Fin{K, l, cap}, gate);
         }
       }
@@ -244,10 +272,11 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
       chunk = std::min(chunk * 2, 16);
     }
     // flush the last deferred update (alpha = 0 when nothing is pending)
-    launch_rows<G, NU, U, 0, 0>(C, n, t,
-                                DeferBody<false>{nullptr, hb[0], r.as<double>(), u, v.as<double>(), K.alpha, nullptr,
-                                                 ld},
-                                Fin0<0>{});
+    if constexpr (DEFER)
+      launch_rows<G, NU, U, 0, 0>(C, n, t,
+                                  DeferBody<false>{nullptr, hb[0], r.as<double>(), u, v.as<double>(), K.alpha,
+                                                   nullptr, ld},
+                                  Fin0<0>{});
     if (status[1] != 0) {
       double ev = 0;
       VL_CUDA(cudaMemcpy(&ev, K.errval, sizeof(double), cudaMemcpyDeviceToHost));
