@@ -57,6 +57,7 @@ VL_D void ld_cg_unit(const double* p, double* out) {
     out[1] = b;
   } else {
     double a;
+    // (ld.relaxed.gpu / ld.cv / ld.volatile measured identical on B200)
     asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(a) : "l"(p));
     out[0] = a;
   }
