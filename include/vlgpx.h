@@ -131,6 +131,7 @@ typedef struct {
   int newton_max_iter;
   double newton_grad_tol;
   double newton_obj_tol;
+  int precond; /* eq6 preconditioner of the Newton systems: 0 vadu, 1 l1, 2 lva, 3 diag, 4 identity */
 } vl_newton_cfg;
 
 /* Damped-Newton mode b* (replaces laplace.py:204-287 find_mode).  Device
@@ -169,7 +170,24 @@ int vl_factor_sums(vl_ctx* ctx, const vl_factor* f, const double* W_dev, double*
  * [h_xi | r_xi] (laplace.py:543-576). */
 int vl_grad_probe_pass(vl_ctx* ctx, const vl_factor* f, const double* W_dev, const double* d3_dev, const double* U_dev,
                        const double* V_dev, int64_t t, double* s_dev, double* cols4_host, const double* md3x_dev,
-                       double* xicols2_host);
+                       double* xicols2_host, int plain);
+/* plain != 0: preconditioners without a control variate (laplace.py:433-436):
+ * s = 0.5 md3 mean_t(U o V) and only the h columns are meaningful. */
+
+/* ---- other eq6 preconditioners (preconditioners.py:338-387) -------------------
+ * variant 0 vadu, 1 l1 (P = B^T diag(W + 1/D) B), 2 lva (B^T diag(1/D) B),
+ * 3 diag (diag(W + diag(B^T D^-1 B))), 4 identity.  vl_precond_dinv writes 1/d
+ * of the sandwich / diagonal; pkind = 0 for variants 0-2 (sandwich), 1 for 3-4
+ * (diagonal).  vl_pcg_eq6 / vl_probes_eq6 are vl_pcg_vadu / vl_probes_vadu for
+ * any variant (sample_block + solve of the chosen P); vl_sum_log returns
+ * sum_i log x_i (log det P = -sum log dinv). */
+int vl_precond_dinv(vl_ctx* ctx, const vl_factor* f, int variant, const double* W_dev, double* dinv_dev);
+int vl_pcg_eq6(vl_ctx* ctx, const vl_factor* f, const double* W_dev, const double* dinv_dev, int pkind, int64_t t,
+               const double* b_dev, double* u_dev, double tol, int max_iter, int capture, int32_t* iters_host,
+               int32_t* converged_host, double* res_host, double* alpha_host, double* beta_host, int hist_cap);
+int vl_probes_eq6(vl_ctx* ctx, const vl_factor* f, const double* dinv_dev, int pkind, int64_t t, const double* G_dev,
+                  double* Z_dev, double* V_dev, double* w_host);
+int vl_sum_log(vl_ctx* ctx, int64_t n, const double* x_dev, double* out_host);
 
 /* ---- LRAC preconditioner and the eq7 system (preconditioners.py:167-214,
  * 249-320; laplace.py:118-182) ------------------------------------------------ */
@@ -226,7 +244,7 @@ int vl_lrac_grad(vl_ctx* ctx, const vl_lracw* w, int64_t t, const double* U_dev,
 int vl_grad_probe_pass_split(vl_ctx* ctx, const vl_factor* f, int mode, const double* W_dev, const double* d3_dev,
                              const double* U_dev, const double* V_dev, int64_t t, int64_t t_glob, double* rowA_dev,
                              double* rowB_dev, double* s_dev, double* cols4_host, const double* md3x_dev,
-                             double* xicols2_host);
+                             double* xicols2_host, int plain);
 
 /* out4 = [b^T dQ_s2 b, tvec^T dQ_s2 b, b^T dQ_rho b, tvec^T dQ_rho b]
  * (vecchia.py:357-361 quad_dprecision; laplace.py:537-541) */

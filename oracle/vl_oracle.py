@@ -504,6 +504,42 @@ class Vadu:
         return self.f.B.T @ self._cs(G, self.sd)
 
 
+class Sandwich(Vadu):
+    """P = B^T diag(d) B with d = 1/D (lva, preconditioners.py:351-352)."""
+
+    def __init__(self, f, d, name):
+        self.f = f
+        self.d = d
+        self.sd = np.sqrt(d)
+        self.name = name
+
+
+class Diagonal:
+    """P = diag(d): diag (W + diag(B^T D^-1 B), preconditioners.py:134-158,
+    353-354; _precision_diag 240-246) and identity (d = 1)."""
+
+    def __init__(self, d, name):
+        self.d = d
+        self.sd = np.sqrt(d)
+        self.name = name
+
+    def solve(self, b):
+        return b / self.d if b.ndim == 1 else b / self.d[:, None]
+
+    def logdet(self):
+        return float(np.log(self.d).sum())
+
+    def sample(self, G):
+        return G * self.sd[:, None]
+
+
+def precision_diag(f):
+    """diag(B^T D^-1 B) (PrecisionAccessor.diag, preconditioners.py:228-240)."""
+    B = f.B.tocsr()
+    rows = np.repeat(np.arange(f.n), np.diff(B.indptr))
+    return np.bincount(B.indices, weights=B.data ** 2 / f.D[rows], minlength=f.n)
+
+
 def pchol_sigma(xy, sigma2, rho, nu, k, tol=0.0):
     """Greedy pivoted Cholesky of the exact covariance (preconditioners.py:288-320)."""
     n = xy.shape[0]
@@ -611,9 +647,15 @@ class Mode:
 
 
 def make_precond(f, W, cfg):
-    """laplace.py:118-153 for vadu / lrac."""
-    if cfg.preconditioner == "vadu":
+    """laplace.py:118-153 -> preconditioners.build (338-387)."""
+    if cfg.preconditioner in ("vadu", "l1"):
         return Vadu(f, W)
+    if cfg.preconditioner == "lva":
+        return Sandwich(f, 1.0 / f.D, "lva")
+    if cfg.preconditioner == "diag":
+        return Diagonal(W + precision_diag(f), "diag")
+    if cfg.preconditioner == "identity":
+        return Diagonal(np.ones(f.n), "identity")
     if cfg.preconditioner == "lrac":
         if np.any(W <= 0):
             raise ValueError("lrac needs W > 0")
@@ -729,7 +771,7 @@ def make_probes(f, st, cfg, Z=None):
     if Z is not None:
         return Probes(np.asarray(Z, dtype=float)), P
     rng = np.random.default_rng(cfg.probe_seed)
-    if cfg.preconditioner == "vadu":
+    if cfg.preconditioner != "lrac":
         G = rng.standard_normal((f.n, cfg.t))
         return Probes(P.sample(G), G=G), P
     Gn = rng.standard_normal((f.n, cfg.t))
@@ -854,11 +896,18 @@ def gradient(f, st, lik, X, cfg, pr, P, details=None):
     t = pr.t
     eq7 = cfg.split == "eq7"
     # d logdet / d mu (laplace.py:389-436)
-    if cfg.preconditioner == "vadu":
+    plain = cfg.preconditioner not in ("vadu", "l1", "lrac")
+    if cfg.preconditioner in ("vadu", "l1"):
         H = U * V
         R = (f.B @ V) ** 2
         c = _cv_rows(H, R, t)
         dmu = md3 * (c / (W + 1.0 / f.D) + (H - c[:, None] * R).mean(axis=1))
+    elif plain:                                       # laplace.py:433-436
+        c = np.zeros(f.n)
+        if eq7:
+            dmu = md3 * (1.0 / W - (U * V / W[:, None] ** 2).mean(axis=1))
+        else:
+            dmu = md3 * (U * V).mean(axis=1)
     else:
         H = U * V / W[:, None] ** 2
         R = (V / W[:, None]) ** 2
@@ -883,7 +932,9 @@ def gradient(f, st, lik, X, cfg, pr, P, details=None):
 
             def dA_op(Vv, g=g):
                 return dprec_apply(f, g, Vv)
-        if cfg.preconditioner == "vadu":
+        if plain:
+            dPt, dP_op = 0.0, None
+        elif cfg.preconditioner in ("vadu", "l1"):
             dPt = -float((dD / (f.D * (f.D * W + 1.0))).sum())
 
             def dP_op(Vv, g=g):
@@ -915,7 +966,9 @@ def gradient(f, st, lik, X, cfg, pr, P, details=None):
 
             def dA_op(Vv, m3=m3):
                 return m3[:, None] * Vv
-        if cfg.preconditioner == "vadu":
+        if plain:
+            dPt, dP_op = 0.0, None
+        elif cfg.preconditioner in ("vadu", "l1"):
             dPt = float((m3 / (W + 1.0 / f.D)).sum())
 
             def dP_op(Vv, m3=m3):

@@ -51,7 +51,7 @@ class VlLik(C.Structure):
 
 class VlNewtonCfg(C.Structure):
     _fields_ = [("mode_cg_tol", C.c_double), ("cg_max_iter", C.c_int), ("newton_max_iter", C.c_int),
-                ("newton_grad_tol", C.c_double), ("newton_obj_tol", C.c_double)]
+                ("newton_grad_tol", C.c_double), ("newton_obj_tol", C.c_double), ("precond", C.c_int)]
 
 
 _V = c_void_p
@@ -60,7 +60,11 @@ _SIGS.update({
     "vl_probes_vadu": [_V, _V, _V, c_int64, _V, _V, _V, _V],
     "vl_pcg_vadu": [_V, _V, _V, c_int64, _V, _V, c_double, c_int, c_int, _V, _V, _V, _V, _V, c_int],
     "vl_factor_sums": [_V, _V, _V, _V],
-    "vl_grad_probe_pass": [_V, _V, _V, _V, _V, _V, c_int64, _V, _V, _V, _V],
+    "vl_grad_probe_pass": [_V, _V, _V, _V, _V, _V, c_int64, _V, _V, _V, _V, c_int],
+    "vl_precond_dinv": [_V, _V, c_int, _V, _V],
+    "vl_pcg_eq6": [_V, _V, _V, _V, c_int, c_int64, _V, _V, c_double, c_int, c_int, _V, _V, _V, _V, _V, c_int],
+    "vl_probes_eq6": [_V, _V, _V, c_int, c_int64, _V, _V, _V, _V],
+    "vl_sum_log": [_V, c_int64, _V, _V],
     "vl_grad_scalar_terms": [_V, _V, _V, _V, _V],
     "vl_grad_dbeta": [_V, c_int64, _V, _V, _V, _V, _V, c_int64, _V],
     "vl_gamma_xi_terms": [_V, _V, _V, _V, _V, _V, _V, _V, _V],
@@ -121,7 +125,7 @@ EXPORTED = sorted(_SIGS)
 
 _SIGS.update({
     "vl_grad_probe_pass_split": [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
-                                 c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+                                 c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int],
 })
 EXPORTED = sorted(_SIGS)
 

@@ -507,7 +507,8 @@ int vl_find_mode(vl_ctx* h, const vl_factor* f, const vl_lik* lik, const vl_newt
   return guard([&] {
     if (!h || !f || !lik || !cfg || !out) fail(kEConfig, "null argument");
     LikSpec L{lik->family, lik->shape};
-    NewtonCfg nc{cfg->mode_cg_tol, cfg->cg_max_iter, cfg->newton_max_iter, cfg->newton_grad_tol, cfg->newton_obj_tol};
+    NewtonCfg nc{cfg->mode_cg_tol, cfg->cg_max_iter, cfg->newton_max_iter, cfg->newton_grad_tol, cfg->newton_obj_tol,
+                 cfg->precond};
     NewtonOut no;
     auto fill = [&] {
       out[0] = no.logp;
@@ -645,7 +646,8 @@ int vl_find_mode_lrac(vl_ctx* h, const vl_factor* f, const vl_lrac* l, const vl_
                       int32_t* cg_iters, int cg_iters_cap) {
   return guard([&] {
     LikSpec L{lik->family, lik->shape};
-    NewtonCfg nc{cfg->mode_cg_tol, cfg->cg_max_iter, cfg->newton_max_iter, cfg->newton_grad_tol, cfg->newton_obj_tol};
+    NewtonCfg nc{cfg->mode_cg_tol, cfg->cg_max_iter, cfg->newton_max_iter, cfg->newton_grad_tol, cfg->newton_obj_tol,
+                 cfg->precond};
     NewtonOut no;
     auto fill = [&] {
       out[0] = no.logp;
@@ -710,20 +712,67 @@ int vl_factor_sums(vl_ctx* h, const vl_factor* f, const double* W, double* out6)
 }
 
 int vl_grad_probe_pass(vl_ctx* h, const vl_factor* f, const double* W, const double* d3, const double* U,
-                       const double* V, int64_t t, double* s_out, double* cols4, const double* md3x, double* xicols2) {
+                       const double* V, int64_t t, double* s_out, double* cols4, const double* md3x, double* xicols2,
+                       int plain) {
   return guard([&] {
     if (t < 1 || t > 128) fail(kECapacity, "probe count per call must be in [1, 128]");
-    grad_probe_pass(h->c, f->f, W, d3, U, V, (int)t, (int)t, s_out, cols4, md3x, xicols2);
+    grad_probe_pass(h->c, f->f, W, d3, U, V, (int)t, (int)t, s_out, cols4, md3x, xicols2, plain);
   });
+}
+
+int vl_precond_dinv(vl_ctx* h, const vl_factor* f, int variant, const double* W, double* dinv) {
+  return guard([&] { precond_dinv(h->c, f->f, variant, W, dinv); });
+}
+
+int vl_pcg_eq6(vl_ctx* h, const vl_factor* f, const double* W, const double* dinv, int pkind, int64_t t,
+               const double* bm, double* u, double tol, int max_iter, int capture, int32_t* iters, int32_t* conv,
+               double* res, double* alpha, double* beta, int hist_cap) {
+  return guard([&] {
+    if (t < 1 || t > 128) fail(kECapacity, "right-hand sides per call must be in [1, 128]");
+    if (pkind != 0 && pkind != 1) fail(kEConfig, "pkind must be 0 (sandwich) or 1 (diagonal)");
+    const Factor& F = f->f;
+    const int64_t n = F.pat->n;
+    DevBuf Dinv, tmp;
+    Dinv.alloc(sizeof(double) * n);
+    tmp.alloc(sizeof(double) * n);
+    vadu_diags(h->c, F, W, Dinv.as<double>(), tmp.as<double>());
+    SysVadu S{&F, W, Dinv.as<double>(), dinv, pkind};
+    PcgResult pr;
+    pcg_vadu(h->c, S, (int)t, (int)t, bm, u, tol, max_iter, capture != 0, &pr);
+    for (int c = 0; c < t; ++c) {
+      if (iters) iters[c] = pr.iters[c];
+      if (conv) conv[c] = pr.converged[c];
+      if (res) res[c] = pr.res[c];
+    }
+    if (capture && alpha && beta) {
+      for (int l = 0; l < std::min(pr.max_iters, hist_cap); ++l)
+        for (int c = 0; c < t; ++c) {
+          alpha[(size_t)l * t + c] = pr.alpha[(size_t)l * t + c];
+          beta[(size_t)l * t + c] = pr.beta[(size_t)l * t + c];
+        }
+    }
+  });
+}
+
+int vl_probes_eq6(vl_ctx* h, const vl_factor* f, const double* dinv, int pkind, int64_t t, const double* G, double* Z,
+                  double* V, double* w_host) {
+  return guard([&] {
+    if (t < 1 || t > 128) fail(kECapacity, "probe count per call must be in [1, 128]");
+    probes_eq6(h->c, f->f, dinv, pkind, (int)t, (int)t, G, Z, V, w_host);
+  });
+}
+
+int vl_sum_log(vl_ctx* h, int64_t n, const double* x, double* out) {
+  return guard([&] { *out = sum_log(h->c, n, x); });
 }
 
 int vl_grad_probe_pass_split(vl_ctx* h, const vl_factor* f, int mode, const double* W, const double* d3,
                              const double* U, const double* V, int64_t t, int64_t t_glob, double* rowA, double* rowB,
-                             double* s_out, double* cols4, const double* md3x, double* xicols2) {
+                             double* s_out, double* cols4, const double* md3x, double* xicols2, int plain) {
   return guard([&] {
     if (mode != 3 && (t < 1 || t > 128)) fail(kECapacity, "probe shard width must be in [1, 128]");
     grad_probe_pass_split(h->c, f->f, mode, W, d3, U, V, (int)t, (int)t, (int)t_glob, rowA, rowB, s_out, cols4, md3x,
-                          xicols2);
+                          xicols2, plain);
   });
 }
 

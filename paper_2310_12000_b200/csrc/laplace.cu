@@ -207,6 +207,61 @@ static void read_sums(Ctx& C, const double* dev, double* host, int cnt) {
   VL_CUDA(cudaStreamSynchronize(C.stream));
 }
 
+namespace {
+// 1/d of the eq6 preconditioner variants (preconditioners.py:338-387):
+// 0 vadu / 1 l1: d = W + 1/D ; 2 lva: d = 1/D ; 3 diag: d = W + diag(B^T D^-1 B) ; 4 identity: d = 1
+struct PrecDinvBody {
+  int variant;
+  BView B;
+  const double* D;
+  const double* W;
+  double* dinv;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int, int, double (&)[NR][NU * U]) const {
+    if (!valid) return;
+    double v;
+    if (variant <= 1) {
+      v = 1.0 / (W[s] + 1.0 / D[s]);
+    } else if (variant == 2) {
+      v = D[s];
+    } else if (variant == 3) {
+      // column s of B: the unit diagonal (row s) and the children rows
+      double q = 1.0 / D[s];
+      for (int32_t e = B.tptr[s]; e < B.tptr[s + 1]; ++e) {
+        const double b = B.valT[e];
+        q += b * b / D[B.tidx[e]];
+      }
+      v = 1.0 / (W[s] + q);
+    } else {
+      v = 1.0;
+    }
+    dinv[s] = v;
+  }
+};
+struct SumLogBody {
+  const double* x;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int, int, double (&acc)[NR][NU * U]) const {
+    if (valid) acc[0][0] += log(x[s]);
+  }
+};
+}  // namespace
+
+void precond_dinv(Ctx& C, const Factor& F, int variant, const double* W, double* dinv) {
+  if (variant < 0 || variant > 4) fail(kEConfig, "unknown eq6 preconditioner variant");
+  launch_rows<1, 1, 1, 0, 0>(C, F.pat->n, 1, PrecDinvBody{variant, bview(F, false), F.D.as<double>(), W, dinv},
+                             Fin0<0>{});
+}
+
+double sum_log(Ctx& C, int64_t n, const double* x) {
+  double* sums = C.dev_scalars.as<double>();
+  launch_rows<1, 1, 1, 1, 0>(C, n, 1, SumLogBody{x}, CopySums<1>{sums});
+  double h;
+  VL_CUDA(cudaMemcpyAsync(&h, sums, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+  return h;
+}
+
 void vadu_diags(Ctx& C, const Factor& F, const double* W, double* Dinv, double* dinv) {
   launch_rows<1, 1, 1, 0, 0>(C, F.pat->n, 1, DiagsBody{F.D.as<double>(), W, Dinv, dinv}, Fin0<0>{});
 }
@@ -264,7 +319,7 @@ void newton_mode(Ctx& C, const Factor& F, const LikSpec& LS, const NewtonCfg& cf
   bool converged = false;
   int iters = 0;
   double safety = 1.0;
-  SysVadu S{&F, W, Dinv.as<double>(), dinv.as<double>()};
+  SysVadu S{&F, W, Dinv.as<double>(), dinv.as<double>(), precond_pkind(cfg.precond)};
   out->cg_iters.clear();
   int it;
   for (it = 1; it <= cfg.max_iter; ++it) {
@@ -273,6 +328,7 @@ void newton_mode(Ctx& C, const Factor& F, const LikSpec& LS, const NewtonCfg& cf
     double tol = cfg.mode_cg_tol;
     if (rn > 0.0) tol = std::min(tol, std::max(safety * 0.25 * gnorm / rn, 1e-14));
     vadu_diags(C, F, W, Dinv.as<double>(), dinv.as<double>());
+    if (cfg.precond > 1) precond_dinv(C, F, cfg.precond, W, dinv.as<double>());
     PcgResult pr;
     if (lrac == nullptr) {
       pcg_vadu(C, S, 1, 1, rhs.as<double>(), bnew.as<double>(), tol, cfg.cg_max_iter, false, &pr);
@@ -413,6 +469,72 @@ struct FactorSumsBody {
 
 }  // namespace
 
+namespace {
+struct SqrtInvBody {  // sd = 1/sqrt(dinv) = sqrt(d)
+  const double* dinv;
+  double* sd;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int, int, double (&)[NR][NU * U]) const {
+    if (valid) sd[s] = 1.0 / sqrt(dinv[s]);
+  }
+};
+// diagonal P: Z = sqrt(d) o G, V = P^-1 Z = Z / d, w_c = z_c . v_c
+struct ProbeDiagBody {
+  const double* G;
+  const double* sd;
+  double* Z;
+  double* V;
+  int ld;
+  template <int G_, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    if (!valid) return;
+    double g[NU * U], z[NU * U], v[NU * U];
+    load_row<G_, NU, U>(G, ld, s, gl, t, g);
+    const double f = sd[s];
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) {
+      z[i] = f * g[i];
+      v[i] = z[i] / (f * f);
+      acc[0][i] += z[i] * v[i];
+    }
+    store_row<G_, NU, U>(Z, ld, s, gl, t, z);
+    store_row<G_, NU, U>(V, ld, s, gl, t, v);
+  }
+};
+}  // namespace
+
+void probes_eq6(Ctx& C, const Factor& F, const double* dinv, int pkind, int t, int ld, const double* G, double* Z,
+                double* V, double* w_host) {
+  const Pattern& P = *F.pat;
+  const int64_t n = P.n;
+  DevBuf sd;
+  sd.alloc(sizeof(double) * n);
+  launch_rows<1, 1, 1, 0, 0>(C, n, 1, SqrtInvBody{dinv, sd.as<double>()}, Fin0<0>{});
+  double* sums = C.dev_scalars.as<double>();
+  if (t > 256) fail(kECapacity, "too many probe columns per call");
+  if (pkind == 1) {
+    dispatch_cols(t, ld, [&](auto g, auto nu, auto uu) {
+      constexpr int G_ = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
+      ProfScope ps(C, "probe_Z", 0.0);
+      launch_rows<G_, NU, U, 1, 0>(C, n, t, ProbeDiagBody{G, sd.as<double>(), Z, V, ld}, CopySums<1>{sums});
+    });
+    read_sums(C, sums, w_host, t);
+    return;
+  }
+  BView B = bview(F, false);
+  DepsEll dfw{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
+  dispatch_cols(t, ld, [&](auto g, auto nu, auto uu) {
+    constexpr int G_ = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
+    {
+      ProfScope ps(C, "probe_Z", bapply_bytes(P, t, 1));
+      launch_rows<G_, NU, U, 0, 0>(C, n, t, ProbeZBody{B, G, sd.as<double>(), Z, ld}, Fin0<0>{});
+    }
+    ProfScope ps(C, "probe_V", bapply_bytes(P, t, 1) + 8.0 * n * t);
+    launch_trsv<G_, NU, U, 1>(C, F, true, t, ld, dfw, V, PsolveRhs{G, sd.as<double>(), Z, ld}, CopySums<1>{sums});
+  });
+  read_sums(C, sums, w_host, t);
+}
+
 void probes_vadu(Ctx& C, const Factor& F, const double* W, int t, int ld, const double* G, double* Z, double* V,
                  double* w_host) {
   const Pattern& P = *F.pat;
@@ -480,6 +602,7 @@ struct GradProbeBody {
   const double* md3x;
   double* s_out;
   int ld;
+  int plain;  // preconditioners without a control variate (laplace.py:433-436): c = 0
   template <int G, int NU, int U, int NR>
   VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
     constexpr int NC = NU * U;
@@ -539,7 +662,7 @@ struct GradProbeBody {
     svr = gsum<G>(svr);
     scv = gsum<G>(scv);
     double cw = 0.0;
-    if (t >= 2) {
+    if (t >= 2 && !plain) {
       const double vr = svr / (t - 1), cv = scv / (t - 1);
       cw = (vr >= 1e-300) ? cv / vr : 0.0;
     }
@@ -688,11 +811,12 @@ struct GradSplitFinishBody {
   const double* d3;
   double* s_out;
   int tg;
+  int plain;
   template <int G, int NU, int U, int NR>
   VL_D void run(int64_t s, bool valid, int, int, double (&)[NR][NU * U]) const {
     if (!valid) return;
     double cw = 0.0;
-    if (tg >= 2) {
+    if (tg >= 2 && !plain) {
       const double vr = rowB[2 * s + 1] / (tg - 1), cv = rowB[2 * s] / (tg - 1);
       cw = (vr >= 1e-300) ? cv / vr : 0.0;
     }
@@ -774,7 +898,8 @@ struct GammaXiBody {
 }  // namespace
 
 void grad_probe_pass(Ctx& C, const Factor& F, const double* W, const double* d3, const double* U, const double* V,
-                     int t, int ld, double* s_out, double* cols_host, const double* xi_md3, double* xi_cols_host) {
+                     int t, int ld, double* s_out, double* cols_host, const double* xi_md3, double* xi_cols_host,
+                     int plain) {
   if (!F.has_grad) fail(kEConfig, "factor was built without gradient");
   const Pattern& P = *F.pat;
   BView B = bview(F, false);
@@ -788,13 +913,13 @@ void grad_probe_pass(Ctx& C, const Factor& F, const double* W, const double* d3,
       launch_rows<G, NU, U_, 4, 0>(C, P.n, t,
                                    GradProbeBody<false>{B, F.dval.as<double>(), U, V, F.D.as<double>(),
                                                         F.dD_sig.as<double>(), F.dD_rho.as<double>(), W, d3, nullptr,
-                                                        s_out, ld},
+                                                        s_out, ld, plain},
                                    CopySums<4>{sums});
     } else {
       launch_rows<G, NU, U_, 6, 0>(C, P.n, t,
                                    GradProbeBody<true>{B, F.dval.as<double>(), U, V, F.D.as<double>(),
                                                        F.dD_sig.as<double>(), F.dD_rho.as<double>(), W, d3, xi_md3,
-                                                       s_out, ld},
+                                                       s_out, ld, plain},
                                    CopySums<6>{sums});
     }
   });
@@ -804,7 +929,7 @@ void grad_probe_pass(Ctx& C, const Factor& F, const double* W, const double* d3,
 
 void grad_probe_pass_split(Ctx& C, const Factor& F, int mode, const double* W, const double* d3, const double* U,
                            const double* V, int t, int ld, int t_glob, double* rowA, double* rowB, double* s_out,
-                           double* cols_host, const double* xi_md3, double* xi_cols_host) {
+                           double* cols_host, const double* xi_md3, double* xi_cols_host, int plain) {
   if (!F.has_grad) fail(kEConfig, "factor was built without gradient");
   const Pattern& P = *F.pat;
   BView B = bview(F, false);
@@ -812,7 +937,8 @@ void grad_probe_pass_split(Ctx& C, const Factor& F, int mode, const double* W, c
   ProfScope ps(C, "grad_pass_split", 0.0);
   if (mode == 3) {
     launch_rows<1, 1, 1, 0, 0>(C, P.n, 1,
-                               GradSplitFinishBody{rowA, rowB, F.D.as<double>(), W, d3, s_out, t_glob}, Fin0<0>{});
+                               GradSplitFinishBody{rowA, rowB, F.D.as<double>(), W, d3, s_out, t_glob, plain},
+                               Fin0<0>{});
     return;
   }
   if (t < 1 || 6 * t > 8192) fail(kECapacity, "invalid probe shard width");

@@ -20,6 +20,7 @@ struct NewtonCfg {
   int max_iter;
   double grad_tol;
   double obj_tol;
+  int precond = 0;  // eq6 variant (precond_dinv); ignored with lrac
 };
 
 struct NewtonOut {
@@ -44,6 +45,19 @@ double count_nonpos(Ctx& C, int64_t n, const double* W);
 // 1/D and 1/(W + 1/D) (VADU diagonal)
 void vadu_diags(Ctx& C, const Factor& F, const double* W, double* Dinv, double* dinv);
 
+// eq6 preconditioner variants (preconditioners.py:338-387):
+//   0 vadu, 1 l1   P = B^T diag(W + 1/D) B          (sandwich)
+//   2 lva          P = B^T diag(1/D) B              (sandwich)
+//   3 diag         P = diag(W + diag(B^T D^-1 B))   (diagonal)
+//   4 identity     P = I                            (diagonal)
+// dinv = 1/d of the sandwich / diagonal; pkind 0 sandwich, 1 diagonal.
+void precond_dinv(Ctx& C, const Factor& F, int variant, const double* W, double* dinv);
+inline int precond_pkind(int variant) { return variant <= 2 ? 0 : 1; }
+double sum_log(Ctx& C, int64_t n, const double* x);
+// Z ~ N(0, P) from base normals G, V = P^-1 Z, w_c = z_c . v_c for either kind
+void probes_eq6(Ctx& C, const Factor& F, const double* dinv, int pkind, int t, int ld, const double* G, double* Z,
+                double* V, double* w_host);
+
 // Z = B^T (sqrt(d) o G), V = B^-1 (G / sqrt(d)) = P^-1 Z, w_c = z_c . v_c
 // (preconditioners.py:121-122, iterative.py:268-271).  G, Z, V: n x ld.
 void probes_vadu(Ctx& C, const Factor& F, const double* W, int t, int ld, const double* G, double* Z, double* V,
@@ -59,13 +73,14 @@ void factor_sums(Ctx& C, const Factor& F, const double* W, double* out_host);
 //   cols (host, 4 x t): h_sigma2, r_sigma2, h_rho, r_rho per probe
 //   plus (if xi_md3 != null) 2 x t: h_xi, r_xi with md3x = xi_md3.
 void grad_probe_pass(Ctx& C, const Factor& F, const double* W, const double* d3, const double* U, const double* V,
-                     int t, int ld, double* s_out, double* cols_host, const double* xi_md3, double* xi_cols_host);
+                     int t, int ld, double* s_out, double* cols_host, const double* xi_md3, double* xi_cols_host,
+                     int plain = 0);
 
 // Probe-sharded split of grad_probe_pass (modes 1, 2, 3; see laplace.cu).
 // rowA/rowB: n x 2 device; between modes the caller allreduces them.
 void grad_probe_pass_split(Ctx& C, const Factor& F, int mode, const double* W, const double* d3, const double* U,
                            const double* V, int t, int ld, int t_glob, double* rowA, double* rowB, double* s_out,
-                           double* cols_host, const double* xi_md3, double* xi_cols_host);
+                           double* cols_host, const double* xi_md3, double* xi_cols_host, int plain = 0);
 
 // Scalar gradient terms with b and tvec (host out, 4 values):
 // [quad_sigma2(b), tvec.dQ_sigma2 b, quad_rho(b), tvec.dQ_rho b]

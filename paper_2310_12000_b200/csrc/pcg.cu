@@ -137,6 +137,57 @@ struct K3RhsFused {
   }
   VL_D void out(int64_t, int, double, double&) const {}
 };
+// ---- diagonal preconditioners (diag / identity): elementwise P^-1 -----------
+struct DiagInitBody {  // z = r / d ; acc += r . z
+  const double* r;
+  const double* dinv;
+  double* z;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    if (!valid) return;
+    double a[NU * U];
+    load_row<G, NU, U>(r, ld, s, gl, t, a);
+    const double di = dinv[s];
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) {
+      const double zz = a[i] * di;
+      acc[0][i] += a[i] * zz;
+      a[i] = zz;
+    }
+    store_row<G, NU, U>(z, ld, s, gl, t, a);
+  }
+};
+template <bool STORE>  // false: ||r - alpha v||^2 (K3) ; true: z = (r - alpha v)/d, (r - alpha v).z (K4)
+struct DiagStepBody {
+  const double* r;
+  const double* v;
+  const double* alpha;
+  const double* dinv;
+  double* z;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    if (!valid) return;
+    constexpr int NC = NU * U;
+    double rs[NC], vs[NC];
+    load_row<G, NU, U>(r, ld, s, gl, t, rs);
+    load_row<G, NU, U>(v, ld, s, gl, t, vs);
+    const double di = STORE ? dinv[s] : 0.0;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int c = vl::Cols<G, NU, U>::col(gl, i);
+      const double rn = fma(-(c < t ? alpha[c] : 0.0), vs[i], rs[i]);
+      if (STORE) {
+        rs[i] = rn * di;
+        acc[0][i] += rn * rs[i];
+      } else {
+        acc[0][i] += rn * rn;
+      }
+    }
+    if (STORE) store_row<G, NU, U>(z, ld, s, gl, t, rs);
+  }
+};
 // ---- deferred update: r -= alpha v, u += alpha h; then h = z + beta h -------
 template <bool HUPD>
 struct DeferBody {
@@ -214,14 +265,20 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
   dispatch_cols(t, ld, [&](auto g, auto nu, auto uu) {
     constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
     constexpr bool DEFER = (G == 1 && NU == 1 && U == 1);  // single RHS: r/u updates deferred
+    const bool diagp = S.pkind == 1;  // diagonal preconditioner: elementwise P^-1, updates deferred
     // init
     ProfScope ps_init(C, t == 1 ? "cg1_init" : "cgT_init", 0.0);
     launch_rows<G, NU, U, 1, 0>(C, n, t, InitBody{b, r.as<double>(), u, hb[0], ld}, InitFin{K, tol});
-    launch_trsv<G, NU, U, 0>(C, F, false, t, ld, dbw, w.as<double>(),
-                             RhsPlainActive{r.as<double>(), ld}, Fin0<0>{}, gate);
-    launch_trsv<G, NU, U, 1>(C, F, true, t, ld, dfw, z.as<double>(),
-                             RhsScaleDot<false>{w.as<double>(), S.dinv, r.as<double>(), nullptr, nullptr, ld},
-                             RzInitFin{K}, gate);
+    if (diagp) {
+      launch_rows<G, NU, U, 1, 0>(C, n, t, DiagInitBody{r.as<double>(), S.dinv, z.as<double>(), ld}, RzInitFin{K},
+                                  gate);
+    } else {
+      launch_trsv<G, NU, U, 0>(C, F, false, t, ld, dbw, w.as<double>(),
+                               RhsPlainActive{r.as<double>(), ld}, Fin0<0>{}, gate);
+      launch_trsv<G, NU, U, 1>(C, F, true, t, ld, dfw, z.as<double>(),
+                               RhsScaleDot<false>{w.as<double>(), S.dinv, r.as<double>(), nullptr, nullptr, ld},
+                               RzInitFin{K}, gate);
+    }
     int status[3] = {0, 0, 0};
     int l = 0;
     int chunk = 4;
@@ -231,7 +288,7 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
         double* hn = hb[0];
         {
           ProfScope ps(C, t == 1 ? "cg1_hupd" : "cgT_hupd", 24.0 * n * t);
-          if constexpr (DEFER)
+          if (DEFER || diagp)
             launch_rows<G, NU, U, 0, 0>(C, n, t,
                                         DeferBody<true>{z.as<double>(), hn, r.as<double>(), u, v.as<double>(),
                                                         K.alpha, K.beta, ld},
@@ -250,7 +307,12 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
         }
         {
           ProfScope ps(C, t == 1 ? "cg1_trsv_Bt" : "cgT_trsv_Bt", bapply_bytes(P, t, 0));
-          if constexpr (DEFER)
+          if (diagp)
+            launch_rows<G, NU, U, 1, 0>(C, n, t,
+                                        DiagStepBody<false>{r.as<double>(), v.as<double>(), K.alpha, nullptr,
+                                                            nullptr, ld},
+                                        K3Fin{K, l}, gate);
+          else if constexpr (DEFER)
             launch_trsv<G, NU, U, 1>(C, F, false, t, ld, dbw, w.as<double>(),
                                      K3Rhs{r.as<double>(), v.as<double>(), K.alpha, ld}, K3Fin{K, l}, gate);
           else
@@ -260,10 +322,16 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
         }
         {
           ProfScope ps(C, t == 1 ? "cg1_trsv_B" : "cgT_trsv_B", bapply_bytes(P, t, 1));
-          launch_trsv<G, NU, U, 1>(C, F, true, t, ld, dfw, z.as<double>(),
-                                   RhsScaleDot<DEFER>{w.as<double>(), S.dinv, r.as<double>(), v.as<double>(),
-                                                      K.alpha, ld},
-                                   K4Fin{K, l, cap}, gate);
+          if (diagp)
+            launch_rows<G, NU, U, 1, 0>(C, n, t,
+                                        DiagStepBody<true>{r.as<double>(), v.as<double>(), K.alpha, S.dinv,
+                                                           z.as<double>(), ld},
+                                        K4Fin{K, l, cap}, gate);
+          else
+            launch_trsv<G, NU, U, 1>(C, F, true, t, ld, dfw, z.as<double>(),
+                                     RhsScaleDot<DEFER>{w.as<double>(), S.dinv, r.as<double>(), v.as<double>(),
+                                                        K.alpha, ld},
+                                     K4Fin{K, l, cap}, gate);
         }
       }
       VL_CUDA(cudaMemcpyAsync(status, K.status, sizeof(status), cudaMemcpyDeviceToHost, C.stream));
@@ -272,7 +340,7 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
       chunk = std::min(chunk * 2, 16);
     }
     // flush the last deferred update (alpha = 0 when nothing is pending)
-    if constexpr (DEFER)
+    if (DEFER || diagp)
       launch_rows<G, NU, U, 0, 0>(C, n, t,
                                   DeferBody<false>{nullptr, hb[0], r.as<double>(), u, v.as<double>(), K.alpha,
                                                    nullptr, ld},

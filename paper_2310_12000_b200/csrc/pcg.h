@@ -12,7 +12,8 @@ struct SysVadu {
   const Factor* F;
   const double* W;     // n
   const double* Dinv;  // n   1/D
-  const double* dinv;  // n   1/(W + 1/D)
+  const double* dinv;  // n   1/d of the preconditioner (vadu: 1/(W + 1/D))
+  int pkind = 0;       // 0: P = B^T diag(d) B (K3/K4 triangular solves); 1: P = diag(d)
 };
 
 struct PcgResult {

@@ -58,7 +58,7 @@ class ProbeComm:
         self.dist.all_reduce(tensor, group=self.group)
         return tensor
 
-    def grad_probe_pass(self, factor, state, probes, md3x):
+    def grad_probe_pass(self, factor, state, probes, md3x, plain=0):
         """Sharded gradient probe pass: local row sums -> allreduce -> centred
         sums -> allreduce -> s; STE (h, r) per probe gathered in probe order."""
         from . import _lib
@@ -77,11 +77,12 @@ class ProbeComm:
         common = (_lib.ptr(dv["W"]), _lib.ptr(dv["d3"]), _lib.ptr(probes.solves_dev), _lib.ptr(probes.psolves_dev),
                   t, t_glob, _lib.ptr(rowA), _lib.ptr(rowB), _lib.ptr(s))
         _lib.call("vl_grad_probe_pass_split", *args, 1, *common, _lib.ptr(cols),
-                  _lib.ptr(md3x) if gamma else None, _lib.ptr(xicols) if gamma else None)
+                  _lib.ptr(md3x) if gamma else None, _lib.ptr(xicols) if gamma else None, int(plain))
         self.allreduce_(rowA)
-        _lib.call("vl_grad_probe_pass_split", *args, 2, *common, None, None, None)
-        self.allreduce_(rowB)
-        _lib.call("vl_grad_probe_pass_split", *args, 3, *common, None, None, None)
+        if not plain:  # the centred sums only feed the control-variate weights
+            _lib.call("vl_grad_probe_pass_split", *args, 2, *common, None, None, None, 0)
+            self.allreduce_(rowB)
+        _lib.call("vl_grad_probe_pass_split", *args, 3, *common, None, None, None, int(plain))
         full = np.stack([self.allgather_cols(cols[k], probes.shard) for k in range(4)])
         xfull = np.stack([self.allgather_cols(xicols[k], probes.shard) for k in range(2)]) if gamma else np.zeros((2, t_glob))
         return s, full, xfull

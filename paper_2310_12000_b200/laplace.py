@@ -25,7 +25,10 @@ from .iterative import (CG_MAX_ITER_DEFAULT, CG_TOL_DEFAULT, ProbeSet, slq_from_
 
 MODE_CG_TOL_CAP = 1e-4
 EQ5_VARIANTS = ("lrac", "l2")
-SUPPORTED_PRECONDITIONERS = ("vadu", "l1", "lrac")
+SUPPORTED_PRECONDITIONERS = ("vadu", "l1", "lva", "diag", "identity", "lrac")
+# eq6 variants on the device (csrc/laplace.cu precond_dinv): sandwich B^T diag(d) B or diagonal diag(d)
+EQ6_VARIANT_ID = {"vadu": 0, "l1": 1, "lva": 2, "diag": 3, "identity": 4}
+CV_VARIANTS = ("vadu", "l1", "lrac")  # variants with a control variate in the gradient (laplace.py:414-431)
 
 
 def default_rank(n):
@@ -199,7 +202,8 @@ def find_mode(factor, lik, y, F, cfg, trace=None):
     b, W, d1, d3 = (dev.empty(ctx, n, 1) for _ in range(4))
     lk = _lib.VlLik(lik.family_id, float(lik.shape_param))
     nc = _lib.VlNewtonCfg(float(cfg.mode_cg_tol), int(cfg.cg_max_iter), int(cfg.newton_max_iter),
-                          float(cfg.newton_grad_tol), float(cfg.newton_obj_tol))
+                          float(cfg.newton_grad_tol), float(cfg.newton_obj_tol),
+                          EQ6_VARIANT_ID.get(cfg.preconditioner, 0))
     out = (C.c_double * 8)()
     cg_its = np.zeros(max(cfg.newton_max_iter, 1), dtype=np.int32)
     if cfg.preconditioner == "lrac":
@@ -222,16 +226,22 @@ def find_mode(factor, lik, y, F, cfg, trace=None):
     return state
 
 
-class VaduPreconditioner:
-    """P = B^T diag(W + 1/D) B on the device (preconditioners.py:101-132)."""
-
-    name = "vadu"
+class Eq6Preconditioner:
+    """The eq6 preconditioners on the device (preconditioners.py:101-158,
+    338-387): vadu / l1 (B^T diag(W + 1/D) B), lva (B^T diag(1/D) B), diag
+    (diag(W + diag(B^T D^-1 B))) and identity.  ``dinv`` (device) holds 1/d
+    of the sandwich or diagonal; ``pkind`` 0 = sandwich, 1 = diagonal."""
 
     def __init__(self, factor, W_dev, name="vadu"):
         self.factor = factor
         self.W_dev = W_dev
         self.name = name
+        self.variant = EQ6_VARIANT_ID[name]
+        self.pkind = 0 if self.variant <= 2 else 1
+        self.dinv = dev.empty(factor.ctx, factor.n, 1)
+        _lib.call("vl_precond_dinv", factor.ctx.h, factor.h, self.variant, _lib.ptr(W_dev), _lib.ptr(self.dinv))
         self._sums = None
+        self._logdet = None
 
     def sums(self):
         if self._sums is None:
@@ -241,7 +251,14 @@ class VaduPreconditioner:
         return self._sums
 
     def logdet(self):
-        return float(self.sums()[1])
+        if self._logdet is None:
+            out = np.zeros(1)
+            _lib.call("vl_sum_log", self.factor.ctx.h, self.factor.n, _lib.ptr(self.dinv), _lib.ptr(out))
+            self._logdet = -float(out[0])
+        return self._logdet
+
+
+VaduPreconditioner = Eq6Preconditioner
 
 
 class LracPreconditioner:
@@ -297,7 +314,7 @@ def build_preconditioner(factor, W_dev, cfg):
     _check_supported(cfg)
     if cfg.preconditioner == "lrac":
         return LracPreconditioner(factor, W_dev, lrac_factor(factor, cfg))
-    return VaduPreconditioner(factor, W_dev, cfg.preconditioner)
+    return Eq6Preconditioner(factor, W_dev, cfg.preconditioner)
 
 
 _G_CACHE = []  # (pattern, seed, t, cols, tensor) -- SAA: same probes every evaluation
@@ -360,7 +377,7 @@ def make_probes(factor, state, cfg, cols=None):
     Z = dev.empty(factor.ctx, factor.n, t)
     V = dev.empty(factor.ctx, factor.n, t)
     w = np.zeros(t)
-    _lib.call("vl_probes_vadu", factor.ctx.h, factor.h, _lib.ptr(state._dev["W"]), t, _lib.ptr(G), _lib.ptr(Z),
+    _lib.call("vl_probes_eq6", factor.ctx.h, factor.h, _lib.ptr(P.dinv), P.pkind, t, _lib.ptr(G), _lib.ptr(Z),
               _lib.ptr(V), _lib.ptr(w))
     ps = ProbeSet(Z, cfg.probe_seed, P.name, pattern=factor.pattern, psolves_dev=V, weights=w,
                   shard=(0 if cols is None else cols[0], cfg.t))
@@ -374,10 +391,11 @@ def probes_from_Z(factor, state, cfg, Z):
     Z = np.asarray(Z, dtype=float)
     Zd = factor.pattern.to_dev(Z)
     n, t = Z.shape
-    # P^-1 Z = B^-1 (B^-T Z / d) ; d = W + 1/D
-    x = factor.solve_B(Z, transpose=True)
-    d = state.W + 1.0 / factor.D
-    V = factor.solve_B(x / d[:, None])
+    dinv = factor.pattern.from_dev(P.dinv)  # factor order, (n, 1)
+    if P.pkind == 0:  # P^-1 Z = B^-1 (B^-T Z / d)
+        V = factor.solve_B(factor.solve_B(Z, transpose=True) * dinv)
+    else:
+        V = Z * dinv
     Vd = factor.pattern.to_dev(V)
     w = np.einsum("it,it->t", Z, V)
     return ProbeSet(Zd, cfg.probe_seed, P.name, pattern=factor.pattern, psolves_dev=Vd, weights=w), P
@@ -400,9 +418,9 @@ def _run_probe_solves(factor, state, P, cfg, probes):
                   int(cfg.cg_max_iter), 1, _lib.ptr(its), _lib.ptr(conv), _lib.ptr(res), _lib.ptr(al), _lib.ptr(be),
                   max(cap, 1))
     else:
-        _lib.call("vl_pcg_vadu", factor.ctx.h, factor.h, _lib.ptr(state._dev["W"]), t, _lib.ptr(probes.Z_dev),
-                  _lib.ptr(U), float(cfg.mode_cg_tol), int(cfg.cg_max_iter), 1, _lib.ptr(its), _lib.ptr(conv),
-                  _lib.ptr(res), _lib.ptr(al), _lib.ptr(be), max(cap, 1))
+        _lib.call("vl_pcg_eq6", factor.ctx.h, factor.h, _lib.ptr(state._dev["W"]), _lib.ptr(P.dinv), P.pkind, t,
+                  _lib.ptr(probes.Z_dev), _lib.ptr(U), float(cfg.mode_cg_tol), int(cfg.cg_max_iter), 1,
+                  _lib.ptr(its), _lib.ptr(conv), _lib.ptr(res), _lib.ptr(al), _lib.ptr(be), max(cap, 1))
     probes.solves_dev = U
     probes.iters = its
     probes.tridiags = [tridiag_from_cg(al[:, c], be[:, c], int(its[c])) for c in range(t)]
@@ -422,8 +440,10 @@ def solve_system(factor, state, rhs_dev, cfg, tol=None, P=None):
         return u, its
     conv = np.zeros(k, dtype=np.int32)
     res = np.zeros(k)
-    _lib.call("vl_pcg_vadu", factor.ctx.h, factor.h, _lib.ptr(state._dev["W"]), k, _lib.ptr(rhs_dev), _lib.ptr(u),
-              float(tol), int(cfg.cg_max_iter), 0, _lib.ptr(its), _lib.ptr(conv), _lib.ptr(res), None, None, 1)
+    P = P if P is not None else build_preconditioner(factor, state._dev["W"], cfg)
+    _lib.call("vl_pcg_eq6", factor.ctx.h, factor.h, _lib.ptr(state._dev["W"]), _lib.ptr(P.dinv), P.pkind, k,
+              _lib.ptr(rhs_dev), _lib.ptr(u), float(tol), int(cfg.cg_max_iter), 0, _lib.ptr(its), _lib.ptr(conv),
+              _lib.ptr(res), None, None, 1)
     return u, its
 
 
@@ -451,7 +471,7 @@ def logdet_system(factor, state, cfg, probes=None, P=None, comm=None):
     if cfg.resolved_split() == "eq7":
         return P.sumlogW + P.logdet() + slq
     sums = P.sums()
-    return float(sums[0]) + float(sums[1]) + slq
+    return float(sums[0]) + P.logdet() + slq
 
 
 def neg_marginal_loglik(state, factor, cfg, probes=None, P=None, comm=None):
@@ -487,13 +507,14 @@ def gradient(state, factor, lik, X, cfg, probes=None, P=None, comm=None):
     xicols = np.zeros((2, t))
     if cfg.preconditioner == "lrac":
         return _gradient_lrac(state, factor, lik, X, cfg, probes, P, comm, md3x, s)
+    plain = 0 if cfg.preconditioner in CV_VARIANTS else 1
     if comm is not None and (comm.world > 1 or getattr(comm, "force_split", False)):
-        s, cols, xicols = comm.grad_probe_pass(factor, state, probes, md3x)
+        s, cols, xicols = comm.grad_probe_pass(factor, state, probes, md3x, plain=plain)
     else:
         _lib.call("vl_grad_probe_pass", ctx.h, factor.h, _lib.ptr(dv["W"]), _lib.ptr(dv["d3"]),
                   _lib.ptr(probes.solves_dev), _lib.ptr(probes.psolves_dev), t, _lib.ptr(s), _lib.ptr(cols),
-                  _lib.ptr(md3x) if gamma else None, _lib.ptr(xicols) if gamma else None)
-    tvec, _ = solve_system(factor, state, s, cfg, tol=cfg.mode_cg_tol)
+                  _lib.ptr(md3x) if gamma else None, _lib.ptr(xicols) if gamma else None, plain)
+    tvec, _ = solve_system(factor, state, s, cfg, tol=cfg.mode_cg_tol, P=P)
     terms = np.zeros(4)
     _lib.call("vl_grad_scalar_terms", ctx.h, factor.h, _lib.ptr(dv["b"]), _lib.ptr(tvec), _lib.ptr(terms))
     sums = P.sums()
@@ -502,7 +523,7 @@ def gradient(state, factor, lik, X, cfg, probes=None, P=None, comm=None):
         ex = float(sums[2 + k])
         dPt = float(sums[4 + k])
         h, r = cols[2 * k], cols[2 * k + 1]
-        ste = ste_combine(h, r, dPt)
+        ste = ste_combine(h, None if plain else r, dPt)  # plain STE for variants without dP (laplace.py:509-536)
         dtheta[k] = 0.5 * terms[2 * k] + 0.5 * (ex + ste) - terms[2 * k + 1]
     dxi = np.empty(lik.n_xi)
     if gamma:
@@ -511,7 +532,7 @@ def gradient(state, factor, lik, X, cfg, probes=None, P=None, comm=None):
                   _lib.ptr(dv["W"]), _lib.ptr(tvec), _lib.ptr(md3x), _lib.ptr(g3))
         a = lik.shape
         dlogp = n * (np.log(a) + 1.0 - digamma(a)) + g3[0]
-        ste = ste_combine(xicols[0], xicols[1], float(g3[2]))
+        ste = ste_combine(xicols[0], None if plain else xicols[1], float(g3[2]))
         dxi[0] = -dlogp + 0.5 * (0.0 + ste) + g3[1]
     p = X.shape[1]
     dbeta = np.zeros(p)
