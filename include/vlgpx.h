@@ -231,7 +231,32 @@ int vl_find_mode_lrac(vl_ctx* ctx, const vl_factor* f, const vl_lrac* l, const v
  * (gamma only, else NULL): xicols 2 x t (h_xi, r_xi), xis = [sum G2 m3, sum m3/W]. */
 int vl_lrac_grad(vl_ctx* ctx, const vl_lracw* w, int64_t t, const double* U_dev, const double* V_dev,
                  const double* d3_dev, const double* md3x_dev, double* s_dev, double* hcols_host, double* rcols_host,
-                 double* dPt_host, double* xicols_host, double* xis_host);
+                 double* dPt_host, double* xicols_host, double* xis_host, int plain);
+/* plain != 0: the eq7 plain estimator (l2; laplace.py:433-434, no control variate). */
+
+/* ---- other low-rank-plus-diagonal preconditioners ----------------------------
+ * (LowRankPlusDiagonalPreconditioner, preconditioners.py:161-214, 338-387)
+ * vl_lowrank_create: kind 1 pchol-precision (pivoted Cholesky of B^T D^-1 B,
+ * PrecisionAccessor 228-246), kind 2 rowsel (U = B_S^T D_S^-1/2 over the k rows
+ * with the largest sum_j B_ij^2 / D_i, ties to the lower index, 323-335).
+ * vl_lowrank_einv: 1/e for kind 1 (e = W) or kind 2 = l2 (e = diag(SigmaTilde)
+ * + 1/W).  vl_lowrank_prepare: Woodbury core for P = U U^T + diag(e) (l may be
+ * NULL: k = 0, the l2 diagonal) with the eq6 (W + Q) or eq7 (SigmaTilde + 1/W)
+ * system; out2 = [log det M, sum log(1/e)]; the vl_lrac_pcg / _solve_system /
+ * _probes / _apply_inv entry points then work on it.  vl_diag_sigma_tilde:
+ * diag(SigmaTilde) (vecchia.py:198-212), storage order.  vl_find_mode_lowrank:
+ * find_mode with these preconditioners (wb_kind 1 eq6 low rank, 2 l2). */
+int vl_lowrank_create(vl_ctx* ctx, const vl_factor* f, int kind, int k, double tol, vl_lrac** out,
+                      int32_t* pivots_host, int* keff);
+int vl_lowrank_einv(vl_ctx* ctx, int64_t n, int kind, const double* W_dev, const double* diag_st_dev,
+                    double* einv_dev);
+int vl_lowrank_prepare(vl_ctx* ctx, const vl_factor* f, const vl_lrac* l, const double* Wop_dev,
+                       const double* einv_dev, int eq6, vl_lracw** out, double* out2_host);
+int vl_diag_sigma_tilde(vl_ctx* ctx, const vl_factor* f, double* out_dev);
+int vl_find_mode_lowrank(vl_ctx* ctx, const vl_factor* f, const vl_lrac* l, int wb_kind, const double* diag_st_dev,
+                         const vl_lik* lik, const vl_newton_cfg* cfg, const double* y_dev, const double* F_dev,
+                         double* b_dev, double* W_dev, double* d1_dev, double* d3_dev, double* out_host,
+                         int32_t* cg_iters_host, int cg_iters_cap);
 
 /* Probe-sharded split of vl_grad_probe_pass for multi-GPU runs (the per-row
  * control-variate weights need all t_glob probes):

@@ -594,6 +594,71 @@ class Lrac:
         return self._cs(G_n, np.sqrt(self.e)) + self.U @ G_k
 
 
+class LowRank(Lrac):
+    """P = U U^T + diag(e) for pchol-precision / rowsel (e = W) and l2 (k = 0,
+    e = diag(SigmaTilde) + 1/W) (preconditioners.py:161-214, 353-379)."""
+
+    def __init__(self, U, e, name, piv=None):
+        if np.any(e <= 0) or not np.all(np.isfinite(e)):
+            raise OracleFactorizationError(f"{name} diagonal part must be positive and finite")
+        self.U = U
+        self.piv = piv
+        self.e = e
+        self.name = name
+        M = np.eye(U.shape[1]) + U.T @ (U / e[:, None])
+        self.M_cho = cho_factor(M, lower=True) if U.shape[1] else (np.zeros((0, 0)), True)
+        self.logdet_M = 2.0 * float(np.log(np.diag(self.M_cho[0])).sum()) if U.shape[1] else 0.0
+
+    def solve(self, b):
+        if self.U.shape[1] == 0:
+            return self._cs(b, 1.0 / self.e)
+        return super().solve(b)
+
+
+def pchol_precision(f, k, tol=0.0):
+    """Pivoted Cholesky of B^T D^-1 B (PrecisionAccessor, preconditioners.py:228-246, 288-320)."""
+    B = f.B.tocsr()
+    Bc = f.B.tocsc()
+    d = precision_diag(f).copy()
+    n = f.n
+    L = np.zeros((n, k))
+    piv = []
+    for j in range(k):
+        if d.min() < -1e-10:
+            raise OracleFactorizationError("pivoted Cholesky lost PSD")
+        np.clip(d, 0.0, None, out=d)
+        if d.sum() <= tol:
+            return L[:, :j], np.array(piv, dtype=int)
+        p = int(np.argmax(d))
+        if d[p] <= 0.0:
+            return L[:, :j], np.array(piv, dtype=int)
+        col = np.zeros(n)
+        col[Bc.indices[Bc.indptr[p]:Bc.indptr[p + 1]]] = Bc.data[Bc.indptr[p]:Bc.indptr[p + 1]]
+        row = B.T @ (col / f.D)
+        c = (row - L[:, :j] @ L[p, :j]) / np.sqrt(d[p])
+        c[p] = np.sqrt(d[p])
+        L[:, j] = c
+        d -= c ** 2
+        d[p] = 0.0
+        piv.append(p)
+    return L, np.array(piv, dtype=int)
+
+
+def rowsel_U(f, k):
+    """U = B_S^T D_S^-1/2 over the k rows with the largest sum_j B_ij^2 / D_i (preconditioners.py:323-335, 372-379)."""
+    B = f.B.tocsr()
+    scores = np.add.reduceat(B.data ** 2, B.indptr[:-1]) / f.D
+    order = np.lexsort((np.arange(f.n), -scores))
+    S = np.sort(order[:k])
+    return (B[S].T @ sp.diags(1.0 / np.sqrt(f.D[S]))).toarray(), S
+
+
+def diag_sigma_tilde(f):
+    """vecchia.py:198-212"""
+    X = f.solve_B(np.eye(f.n), transpose=True)
+    return np.einsum("j,jc->c", f.D, X ** 2)
+
+
 # --------------------------------------------------------------------------
 # Laplace objective (laplace.py:51-580)
 # --------------------------------------------------------------------------
@@ -656,6 +721,17 @@ def make_precond(f, W, cfg):
         return Diagonal(W + precision_diag(f), "diag")
     if cfg.preconditioner == "identity":
         return Diagonal(np.ones(f.n), "identity")
+    if cfg.preconditioner in ("pchol-precision", "rowsel"):
+        key = (cfg.preconditioner, cfg.k(f.n))
+        if key not in f.cache:
+            f.cache[key] = (pchol_precision(f, cfg.k(f.n)) if cfg.preconditioner == "pchol-precision"
+                            else rowsel_U(f, cfg.k(f.n)))
+        U, piv = f.cache[key]
+        return LowRank(U, W.copy(), cfg.preconditioner, piv)
+    if cfg.preconditioner == "l2":
+        if "diag_st" not in f.cache:
+            f.cache["diag_st"] = diag_sigma_tilde(f)
+        return LowRank(np.zeros((f.n, 0)), f.cache["diag_st"] + 1.0 / W, "l2")
     if cfg.preconditioner == "lrac":
         if np.any(W <= 0):
             raise ValueError("lrac needs W > 0")
@@ -771,7 +847,7 @@ def make_probes(f, st, cfg, Z=None):
     if Z is not None:
         return Probes(np.asarray(Z, dtype=float)), P
     rng = np.random.default_rng(cfg.probe_seed)
-    if cfg.preconditioner != "lrac":
+    if cfg.preconditioner not in ("lrac", "pchol-precision", "rowsel", "l2"):
         G = rng.standard_normal((f.n, cfg.t))
         return Probes(P.sample(G), G=G), P
     Gn = rng.standard_normal((f.n, cfg.t))

@@ -142,7 +142,13 @@ _SIGS.update({
     "vl_apply_sigma_tilde": [c_void_p, c_void_p, c_int64, c_void_p, c_void_p],
     "vl_lrac_probes": [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "vl_lrac_grad": [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                     c_void_p, c_void_p, c_void_p],
+                     c_void_p, c_void_p, c_void_p, c_int],
+    "vl_lowrank_create": [c_void_p, c_void_p, c_int, c_int, c_double, c_void_p, c_void_p, c_void_p],
+    "vl_lowrank_einv": [c_void_p, c_int64, c_int, c_void_p, c_void_p, c_void_p],
+    "vl_lowrank_prepare": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p],
+    "vl_diag_sigma_tilde": [c_void_p, c_void_p, c_void_p],
+    "vl_find_mode_lowrank": [c_void_p, c_void_p, c_void_p, c_int, c_void_p, C.POINTER(VlLik), C.POINTER(VlNewtonCfg),
+                             c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int],
     "vl_pred_create": [c_void_p, c_void_p, c_double, c_double, c_double, c_void_p, c_int64, c_void_p, c_int,
                        c_void_p],
     "vl_pred_destroy": [c_void_p],

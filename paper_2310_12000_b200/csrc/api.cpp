@@ -637,8 +637,85 @@ int vl_lrac_probes(vl_ctx* h, const vl_lracw* w, int64_t t, const double* Gn, co
 
 int vl_lrac_grad(vl_ctx* h, const vl_lracw* w, int64_t t, const double* U, const double* V, const double* d3,
                  const double* md3x, double* s, double* hcols, double* rcols, double* dPt, double* xicols,
-                 double* xis) {
-  return guard([&] { lrac_grad(h->c, w->p, (int)t, U, V, d3, md3x, s, hcols, rcols, dPt, xicols, xis); });
+                 double* xis, int plain) {
+  return guard([&] { lrac_grad(h->c, w->p, (int)t, U, V, d3, md3x, s, hcols, rcols, dPt, xicols, xis, plain); });
+}
+
+int vl_lowrank_create(vl_ctx* h, const vl_factor* f, int kind, int k, double tol, vl_lrac** out, int32_t* piv_host,
+                      int* keff) {
+  return guard([&] {
+    auto* l = new vl_lrac();
+    l->f = f;
+    try {
+      if (kind == 1) pchol_precision(h->c, f->f, l->lf, k, tol);
+      else if (kind == 2) rowsel_factor(h->c, f->f, l->lf, k);
+      else fail(kEConfig, "kind must be 1 (pchol-precision) or 2 (rowsel)");
+    } catch (...) {
+      delete l;
+      throw;
+    }
+    if (keff) *keff = l->lf.keff;
+    if (piv_host)
+      for (int q = 0; q < l->lf.keff; ++q) piv_host[q] = l->lf.piv_f[q];
+    *out = l;
+  });
+}
+
+int vl_lowrank_einv(vl_ctx* h, int64_t n, int kind, const double* W, const double* diag_st, double* einv) {
+  return guard([&] { lowrank_einv(h->c, n, kind, W, diag_st, einv); });
+}
+
+int vl_lowrank_prepare(vl_ctx* h, const vl_factor* f, const vl_lrac* l, const double* Wop, const double* einv,
+                       int eq6, vl_lracw** out, double* out2) {
+  return guard([&] {
+    auto* w = new vl_lracw();
+    try {
+      lowrank_prepare(h->c, f->f, l ? &l->lf : nullptr, Wop, einv, eq6, w->p);
+    } catch (...) {
+      delete w;
+      throw;
+    }
+    if (out2) {
+      out2[0] = w->p.logdetM;
+      out2[1] = w->p.sumlogW;
+    }
+    *out = w;
+  });
+}
+
+int vl_diag_sigma_tilde(vl_ctx* h, const vl_factor* f, double* out) {
+  return guard([&] { diag_sigma_tilde(h->c, f->f, out); });
+}
+
+int vl_find_mode_lowrank(vl_ctx* h, const vl_factor* f, const vl_lrac* l, int wb_kind, const double* diag_st,
+                         const vl_lik* lik, const vl_newton_cfg* cfg, const double* y, const double* Fv, double* b,
+                         double* W, double* d1, double* d3, double* out, int32_t* cg_iters, int cg_iters_cap) {
+  return guard([&] {
+    if (wb_kind != 1 && wb_kind != 2) fail(kEConfig, "wb_kind must be 1 (eq6 low rank) or 2 (l2)");
+    if (wb_kind == 1 && !l) fail(kEConfig, "low-rank factor required");
+    LikSpec L{lik->family, lik->shape};
+    NewtonCfg nc{cfg->mode_cg_tol, cfg->cg_max_iter, cfg->newton_max_iter, cfg->newton_grad_tol, cfg->newton_obj_tol,
+                 0, wb_kind, diag_st};
+    NewtonOut no;
+    auto fill = [&] {
+      out[0] = no.logp;
+      out[1] = no.quad;
+      out[2] = no.objective;
+      out[3] = no.grad_norm;
+      out[4] = no.iters;
+      out[5] = no.converged;
+      out[6] = (double)no.cg_iters.size();
+      if (cg_iters)
+        for (int i = 0; i < (int)no.cg_iters.size() && i < cg_iters_cap; ++i) cg_iters[i] = no.cg_iters[i];
+    };
+    try {
+      newton_mode(h->c, f->f, L, nc, y, Fv, b, W, d1, d3, &no, l ? &l->lf : nullptr);
+    } catch (...) {
+      fill();
+      throw;
+    }
+    fill();
+  });
 }
 
 int vl_find_mode_lrac(vl_ctx* h, const vl_factor* f, const vl_lrac* l, const vl_lik* lik, const vl_newton_cfg* cfg,

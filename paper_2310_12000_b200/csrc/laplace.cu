@@ -276,6 +276,25 @@ struct CountNonPosBody {  // #{W <= 0} (LRAC / eq7 require W > 0)
 };
 }  // namespace
 
+namespace {
+struct EinvBody {
+  int kind;
+  const double* W;
+  const double* dst;
+  double* out;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int, int, double (&)[NR][NU * U]) const {
+    if (valid) out[s] = kind == 1 ? 1.0 / W[s] : 1.0 / (dst[s] + 1.0 / W[s]);
+  }
+};
+}  // namespace
+
+void lowrank_einv(Ctx& C, int64_t n, int kind, const double* W, const double* diag_st, double* einv) {
+  if (kind != 1 && kind != 2) fail(kEConfig, "unknown low-rank preconditioner kind");
+  if (kind == 2 && diag_st == nullptr) fail(kEConfig, "l2 needs diag(SigmaTilde)");
+  launch_rows<1, 1, 1, 0, 0>(C, n, 1, EinvBody{kind, W, diag_st, einv}, Fin0<0>{});
+}
+
 double count_nonpos(Ctx& C, int64_t n, const double* W) {
   double* sums = C.dev_scalars.as<double>();
   launch_rows<1, 1, 1, 1, 0>(C, n, 1, CountNonPosBody{W}, CopySums<1>{sums});
@@ -330,15 +349,24 @@ void newton_mode(Ctx& C, const Factor& F, const LikSpec& LS, const NewtonCfg& cf
     vadu_diags(C, F, W, Dinv.as<double>(), dinv.as<double>());
     if (cfg.precond > 1) precond_dinv(C, F, cfg.precond, W, dinv.as<double>());
     PcgResult pr;
-    if (lrac == nullptr) {
+    if (lrac == nullptr && cfg.wb_kind != 2) {
       pcg_vadu(C, S, 1, 1, rhs.as<double>(), bnew.as<double>(), tol, cfg.cg_max_iter, false, &pr);
     } else {
-      if (count_nonpos(C, n, W) > 0)
+      const bool nonpos = count_nonpos(C, n, W) > 0;
+      if (cfg.wb_kind == 1) {
+        if (nonpos) fail(kEFactorization, "low-rank preconditioner diagonal part must be positive and finite");
+      } else if (nonpos) {
         fail(kECapability,
-             "lrac preconditions SigmaTilde + W^{-1} and needs W > 0 everywhere (eq7 split; log W undefined); "
-             "switch to an eq6 preconditioner such as vadu");
+             "this preconditioner works on SigmaTilde + W^{-1} and needs W > 0 everywhere (eq7 split; log W "
+             "undefined); switch to an eq6 preconditioner such as vadu");
+      }
       LracPrec Pr;
-      lrac_prepare(C, F, *lrac, W, Pr);
+      if (cfg.wb_kind == 0) {
+        lrac_prepare(C, F, *lrac, W, Pr);
+      } else {
+        lowrank_einv(C, n, cfg.wb_kind, W, cfg.diag_st, tmp.as<double>());
+        lowrank_prepare(C, F, cfg.wb_kind == 2 ? nullptr : lrac, W, tmp.as<double>(), cfg.wb_kind == 1 ? 1 : 0, Pr);
+      }
       lrac_solve_system(C, Pr, 1, rhs.as<double>(), bnew.as<double>(), tol, cfg.cg_max_iter, &pr);
     }
     out->cg_iters.push_back(pr.iters[0]);

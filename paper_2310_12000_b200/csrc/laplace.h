@@ -21,6 +21,11 @@ struct NewtonCfg {
   double grad_tol;
   double obj_tol;
   int precond = 0;  // eq6 variant (precond_dinv); ignored with lrac
+  // low-rank-plus-diagonal preconditioners (lrac != nullptr or wb_kind == 2):
+  // 0 lrac (eq7, e = 1/W), 1 pchol-precision / rowsel (eq6, e = W), 2 l2 (eq7, k = 0,
+  // e = diag(SigmaTilde) + 1/W with diag_st = diag(SigmaTilde))
+  int wb_kind = 0;
+  const double* diag_st = nullptr;
 };
 
 struct NewtonOut {
@@ -38,6 +43,9 @@ struct LracFactor;
 void newton_mode(Ctx& C, const Factor& F, const LikSpec& L, const NewtonCfg& cfg, const double* y,
                  const double* Fv, double* b, double* W, double* d1, double* d3, NewtonOut* out,
                  const LracFactor* lrac = nullptr);
+
+// 1/e of the low-rank-plus-diagonal variants: kind 1: 1/W ; kind 2: 1/(diag_st + 1/W)
+void lowrank_einv(Ctx& C, int64_t n, int kind, const double* W, const double* diag_st, double* einv);
 
 // number of entries with W <= 0 (eq7 / LRAC capability check)
 double count_nonpos(Ctx& C, int64_t n, const double* W);

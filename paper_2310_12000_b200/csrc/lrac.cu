@@ -92,7 +92,9 @@ __global__ void __launch_bounds__(kPcThreads) pchol_step_kernel(int64_t n, int d
                                                                int k, double* __restrict__ L, double* __restrict__ d,
                                                                PcState st, double tol, double* __restrict__ part,
                                                                unsigned* __restrict__ counter,
-                                                               int32_t* __restrict__ piv_s) {
+                                                               int32_t* __restrict__ piv_s,
+                                                               const double* __restrict__ qc) {
+  // qc: dense column of the matrix at the pivot (precision accessor) or null (Matern row of Sigma)
   if (((volatile int*)st.i)[1] != 0) return;
   __shared__ double s_min[kPcThreads / 32], s_sum[kPcThreads / 32], s_max[kPcThreads / 32];
   __shared__ int s_arg[kPcThreads / 32];
@@ -114,12 +116,18 @@ __global__ void __launch_bounds__(kPcThreads) pchol_step_kernel(int64_t n, int d
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
     if (lane == 0) {
-      double r2 = 0.0;
-      for (int q = 0; q < dim; ++q) {
-        const double df = xy[i * dim + q] - xp[q];
-        r2 += df * df;
+      double src;
+      if (qc) {
+        src = qc[i];
+      } else {
+        double r2 = 0.0;
+        for (int q = 0; q < dim; ++q) {
+          const double df = xy[i * dim + q] - xp[q];
+          r2 += df * df;
+        }
+        src = K.val(sqrt(r2));
       }
-      double col = (K.val(sqrt(r2)) - dot) / sq;
+      double col = (src - dot) / sq;
       double di = fmax(d[i], 0.0);  // np.clip(d, 0) of this step
       if (i == p) col = sq;
       Li[j] = col;
@@ -337,6 +345,51 @@ struct RhsScaleD {  // trsv rhs = D o w
   VL_D double rhs(int64_t s, int c, double&) const { return w[s * ld + c] * D[s]; }
   VL_D void out(int64_t, int, double, double&) const {}
 };
+struct PrecK1Body {  // tmp = D^-1 (B h)
+  BView B;
+  const double* h;
+  double* tmp;
+  const double* D;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&)[NR][NU * U]) const {
+    double a[NU * U];
+    zero(a);
+    gather_B<G, NU, U>(B, B.val, s, valid, gl, t, LoadU<U>{h, ld}, a);
+    if (!valid) return;
+    double hs[NU * U];
+    load_row<G, NU, U>(h, ld, s, gl, t, hs);
+    const double di = 1.0 / D[s];
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) a[i] = di * (hs[i] + a[i]);
+    store_row<G, NU, U>(tmp, ld, s, gl, t, a);
+  }
+};
+struct PrecK2Body {  // v = W h + B^T tmp ; acc += h . v
+  BView B;
+  const double* h;
+  const double* tmp;
+  double* v;
+  const double* W;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    double a[NU * U];
+    zero(a);
+    gather_Bt<G, NU, U>(B, s, valid, gl, t, LoadU<U>{tmp, ld}, a);
+    if (!valid) return;
+    double ts[NU * U], hs[NU * U];
+    load_row<G, NU, U>(tmp, ld, s, gl, t, ts);
+    load_row<G, NU, U>(h, ld, s, gl, t, hs);
+    const double ws = W[s];
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) {
+      a[i] = ws * hs[i] + (ts[i] + a[i]);
+      acc[0][i] += hs[i] * a[i];
+    }
+    store_row<G, NU, U>(v, ld, s, gl, t, a);
+  }
+};
 struct RzFin {
   cg::CgCols K;
   VL_D void operator()(const double* sums, int t) const {
@@ -379,7 +432,7 @@ void lrac_pchol(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol) {
   for (int j = 0; j < k; ++j) {
     pchol_step_kernel<<<grid, kPcThreads, 0, C.stream>>>(n, P.d, P.xy.as<double>(), P.fidx.as<int32_t>(), K, j, k,
                                                          LF.L.as<double>(), d.as<double>(), S, tol,
-                                                         part.as<double>(), counter, LF.piv_s.as<int32_t>());
+                                                         part.as<double>(), counter, LF.piv_s.as<int32_t>(), nullptr);
     VL_LAUNCH_CHECK();
     C.prof.launches++;
   }
@@ -394,12 +447,22 @@ void lrac_pchol(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol) {
 }
 
 void lrac_prepare(Ctx& C, const Factor& F, const LracFactor& LF, const double* W, LracPrec& Pr) {
+  lowrank_prepare(C, F, &LF, W, nullptr, 0, Pr);
+}
+
+void lowrank_prepare(Ctx& C, const Factor& F, const LracFactor* LFp, const double* Wop, const double* einv, int eq6,
+                     LracPrec& Pr) {
   const Pattern& P = *F.pat;
   const int64_t n = P.n;
-  const int k = LF.keff;
   Pr.F = &F;
-  Pr.LF = &LF;
+  Pr.LF = LFp ? LFp : &Pr.empty;
+  const LracFactor& LF = *Pr.LF;
+  const double* W = einv ? einv : Wop;
+  const int k = LF.keff;
   Pr.W = W;
+  Pr.Wop = Wop;
+  Pr.eq6 = eq6;
+  Pr.sumlogW = lrac_sumlogW(C, n, W);
   if (k == 0) {
     Pr.logdetM = 0.0;
     return;
@@ -531,13 +594,23 @@ void pcg_lrac(Ctx& C, const LracPrec& Pr, int t, const double* b, double* u, dou
       const int lim = std::min(max_iter, l + chunk);
       for (; l < lim; ++l) {
         launch_rows<G, NU, U, 0, 0>(C, n, t, HUpdBody{z.as<double>(), h.as<double>(), K.beta, t}, Fin0<0>{}, gate);
-        // v = SigmaTilde h + h / W
-        launch_trsv<G, NU, U, 0>(C, F, false, t, t, dbw, scr.as<double>(), TrsvPlain{h.as<double>(), t}, Fin0<0>{},
-                                 gate);
-        launch_trsv<G, NU, U, 0>(C, F, true, t, t, dfw, sx.as<double>(), RhsScaleD{scr.as<double>(), F.D.as<double>(), t},
-                                 Fin0<0>{}, gate);
-        launch_rows<G, NU, U, 1, 0>(C, n, t, Eq7FinishBody{Pr.W, sx.as<double>(), h.as<double>(), v.as<double>(), t},
-                                    K2Fin{K, l, cap}, gate);
+        // v = SigmaTilde h + h / W  (eq7)  or  W h + Q h  (eq6)
+        if (Pr.eq6) {  // v = W h + B^T D^-1 B h
+          launch_rows<G, NU, U, 0, 0>(C, n, t, PrecK1Body{bview(F, false), h.as<double>(), sx.as<double>(),
+                                                          F.D.as<double>(), t},
+                                      Fin0<0>{}, gate);
+          launch_rows<G, NU, U, 1, 0>(C, n, t, PrecK2Body{bview(F, false), h.as<double>(), sx.as<double>(),
+                                                          v.as<double>(), Pr.Wop, t},
+                                      K2Fin{K, l, cap}, gate);
+        } else {
+          launch_trsv<G, NU, U, 0>(C, F, false, t, t, dbw, scr.as<double>(), TrsvPlain{h.as<double>(), t},
+                                   Fin0<0>{}, gate);
+          launch_trsv<G, NU, U, 0>(C, F, true, t, t, dfw, sx.as<double>(),
+                                   RhsScaleD{scr.as<double>(), F.D.as<double>(), t}, Fin0<0>{}, gate);
+          launch_rows<G, NU, U, 1, 0>(C, n, t,
+                                      Eq7FinishBody{Pr.Wop, sx.as<double>(), h.as<double>(), v.as<double>(), t},
+                                      K2Fin{K, l, cap}, gate);
+        }
         launch_rows<G, NU, U, 1, 0>(C, n, t,
                                     UpdBody{r.as<double>(), u, v.as<double>(), h.as<double>(), K.alpha, K.active, t},
                                     K3Fin{K, l}, gate);
@@ -758,6 +831,7 @@ struct LracMuBody {
   const double* md3x;
   double* s_out;
   int ld;
+  int plain;  // no control variate (l2, laplace.py:433-434)
   template <int G, int NU, int U, int NR>
   VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
     constexpr int NC = NU * U;
@@ -791,7 +865,7 @@ struct LracMuBody {
     svr = gsum_l<G>(svr);
     scv = gsum_l<G>(scv);
     double cw = 0.0;
-    if (t >= 2) {
+    if (t >= 2 && !plain) {
       const double vr = svr / (t - 1), cv = scv / (t - 1);
       cw = (vr >= 1e-300) ? cv / vr : 0.0;
     }
@@ -869,7 +943,7 @@ struct DQDotBody {
 // dPt (2); with md3x: xih (t), xir (t), xi_scalars [sum G2 m3, sum m3 / W]
 void lrac_grad(Ctx& C, const LracPrec& Pr, int t, const double* U, const double* V, const double* d3,
                const double* md3x, double* s_out, double* hcols, double* rcols, double* dPt, double* xicols,
-               double* xis) {
+               double* xis, int plain) {
   const Factor& F = *Pr.F;
   const Pattern& P = *F.pat;
   const int64_t n = P.n;
@@ -895,10 +969,11 @@ void lrac_grad(Ctx& C, const LracPrec& Pr, int t, const double* U, const double*
   dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
     constexpr int G_ = decltype(g)::value, NU = decltype(nu)::value, U_ = decltype(uu)::value;
     if (md3x)
-      launch_rows<G_, NU, U_, 2, 0>(C, n, t, LracMuBody<true>{U, V, Pr.W, G2.as<double>(), d3, md3x, s_out, t},
+      launch_rows<G_, NU, U_, 2, 0>(C, n, t, LracMuBody<true>{U, V, Pr.Wop, G2.as<double>(), d3, md3x, s_out, t, plain},
                                     CopySumsL<2>{sums});
     else
-      launch_rows<G_, NU, U_, 0, 0>(C, n, t, LracMuBody<false>{U, V, Pr.W, G2.as<double>(), d3, nullptr, s_out, t},
+      launch_rows<G_, NU, U_, 0, 0>(C, n, t, LracMuBody<false>{U, V, Pr.Wop, G2.as<double>(), d3, nullptr, s_out, t,
+                                                               plain},
                                     Fin0<0>{});
   });
   if (md3x) {
@@ -922,6 +997,21 @@ void lrac_grad(Ctx& C, const LracPrec& Pr, int t, const double* U, const double*
   });
   VL_CUDA(cudaMemcpyAsync(hcols, sums, sizeof(double) * 2 * t, cudaMemcpyDeviceToHost, C.stream));
   VL_CUDA(cudaStreamSynchronize(C.stream));
+  if (md3x && xis) {
+    // xi dP_trace pieces: sum G2 m3, sum m3 / W (host sums over device arrays)
+    std::vector<double> g2h(n), mh(n), wh(n);
+    VL_CUDA(cudaMemcpyAsync(g2h.data(), G2.p, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
+    VL_CUDA(cudaMemcpyAsync(mh.data(), md3x, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
+    VL_CUDA(cudaMemcpyAsync(wh.data(), Pr.Wop, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
+    VL_CUDA(cudaStreamSynchronize(C.stream));
+    double a = 0.0, b = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      a += g2h[i] * mh[i];
+      b += mh[i] / wh[i];
+    }
+    xis[0] = a;
+    xis[1] = b;
+  }
   if (k == 0) {
     for (int i = 0; i < 2 * t; ++i) rcols[i] = 0.0;
     dPt[0] = dPt[1] = 0.0;
@@ -1026,21 +1116,6 @@ void lrac_grad(Ctx& C, const LracPrec& Pr, int t, const double* U, const double*
     for (int l = 0; l < k; ++l) s += a1[(size_t)c * k + l] * a2[(size_t)c * k + l];
     rcols[t + c] = 2.0 * s;
   }
-  if (md3x && xis) {
-    // xi dP_trace pieces: sum G2 m3, sum m3 / W (host sums over device arrays)
-    std::vector<double> g2h(n), mh(n), wh(n);
-    VL_CUDA(cudaMemcpyAsync(g2h.data(), G2.p, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
-    VL_CUDA(cudaMemcpyAsync(mh.data(), md3x, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
-    VL_CUDA(cudaMemcpyAsync(wh.data(), Pr.W, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
-    VL_CUDA(cudaStreamSynchronize(C.stream));
-    double a = 0.0, b = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-      a += g2h[i] * mh[i];
-      b += mh[i] / wh[i];
-    }
-    xis[0] = a;
-    xis[1] = b;
-  }
 }
 
 void lrac_solve_system(Ctx& C, const LracPrec& Pr, int t, const double* rhs, double* u, double tol, int max_iter,
@@ -1050,12 +1125,235 @@ void lrac_solve_system(Ctx& C, const LracPrec& Pr, int t, const double* rhs, dou
   srhs.alloc(sizeof(double) * (size_t)n * t);
   scr.alloc(sizeof(double) * (size_t)n * t);
   us.alloc(sizeof(double) * (size_t)n * t);
+  if (Pr.eq6) {  // laplace.py:180-181
+    pcg_lrac(C, Pr, t, rhs, u, tol, max_iter, false, out);
+    return;
+  }
   apply_sigma_tilde(C, *Pr.F, t, rhs, srhs.as<double>(), scr.as<double>());
   pcg_lrac(C, Pr, t, srhs.as<double>(), us.as<double>(), tol, max_iter, false, out);
   dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
     constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
-    launch_rows<G, NU, U, 0, 0>(C, n, t, DivWBody{Pr.W, us.as<double>(), u, t}, Fin0<0>{});
+    launch_rows<G, NU, U, 0, 0>(C, n, t, DivWBody{Pr.Wop, us.as<double>(), u, t}, Fin0<0>{});
   });
+}
+
+
+// ---------------------------------------------------------------------------
+// Other low-rank-plus-diagonal preconditioners (preconditioners.py:161-246,
+// 323-387) and diag(SigmaTilde) for l2 (vecchia.py:198-212).
+// ---------------------------------------------------------------------------
+namespace {
+
+// Column p of Q = B^T D^-1 B into the dense vector qc (sequential, fixed order):
+// Q[i, p] = sum over rows r with B_rp != 0 (r = p and the children of p) of B_ri B_rp / D_r.
+__global__ void qcol_kernel(const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
+                            const double* __restrict__ val, const int32_t* __restrict__ tptr,
+                            const int32_t* __restrict__ tidx, const double* __restrict__ valT,
+                            const double* __restrict__ D, int m, PcState st, double* __restrict__ qc,
+                            int32_t* __restrict__ touched, int* __restrict__ ntouched) {
+  if (threadIdx.x != 0 || ((volatile int*)st.i)[1] != 0) return;
+  const int32_t p = st.i[0];
+  int nt = 0;
+  auto add_row = [&](int32_t r, double brp) {
+    const double w = brp / D[r];
+    qc[r] += w;  // B_rr = 1
+    touched[nt++] = r;
+    for (int e = 0; e < cnt[r]; ++e) {
+      const int32_t i = nbr[(int64_t)r * m + e];
+      qc[i] += val[(int64_t)r * m + e] * w;
+      touched[nt++] = i;
+    }
+  };
+  add_row(p, 1.0);
+  for (int32_t e = tptr[p]; e < tptr[p + 1]; ++e) add_row(tidx[e], valT[e]);
+  *ntouched = nt;
+}
+
+__global__ void qclear_kernel(double* __restrict__ qc, const int32_t* __restrict__ touched,
+                              const int* __restrict__ ntouched) {
+  const int nt = *ntouched;
+  for (int e = threadIdx.x; e < nt; e += blockDim.x) qc[touched[e]] = 0.0;
+}
+
+struct DiagQBody {  // diag(B^T D^-1 B)
+  BView B;
+  const double* D;
+  double* out;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int, int, double (&)[NR][NU * U]) const {
+    if (!valid) return;
+    double q = 1.0 / D[s];
+    for (int32_t e = B.tptr[s]; e < B.tptr[s + 1]; ++e) q += B.valT[e] * B.valT[e] / D[B.tidx[e]];
+    out[s] = q;
+  }
+};
+
+struct RowScoreBody {  // (1 + sum_e B_se^2) / D_s
+  BView B;
+  const double* D;
+  double* out;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int, int, double (&)[NR][NU * U]) const {
+    if (!valid) return;
+    double q = 1.0;
+    for (int e = 0; e < B.cnt[s]; ++e) {
+      const double b = B.val[s * B.m + e];
+      q += b * b;
+    }
+    out[s] = q / D[s];
+  }
+};
+
+// U[:, c] = B_{r_c,:}^T / sqrt(D_{r_c}) into the dense n x kl row-major factor
+__global__ void rowsel_scatter_kernel(int k, int kl, int m, const int32_t* __restrict__ rows,
+                                      const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
+                                      const double* __restrict__ val, const double* __restrict__ D,
+                                      double* __restrict__ L) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) {
+    const int32_t r = rows[c];
+    const double f = 1.0 / sqrt(D[r]);
+    L[(int64_t)r * kl + c] = f;
+    for (int e = 0; e < cnt[r]; ++e) L[(int64_t)nbr[(int64_t)r * m + e] * kl + c] = val[(int64_t)r * m + e] * f;
+  }
+}
+
+__global__ void eye_block_kernel(int64_t n, int a, int w, double* __restrict__ E) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * w; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / w;
+    const int c = (int)(e % w);
+    E[e] = (i == a + c) ? 1.0 : 0.0;
+  }
+}
+
+struct DX2Body {  // acc[c] += D_s X_sc^2
+  const double* D;
+  const double* X;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    if (!valid) return;
+    double a[NU * U];
+    load_row<G, NU, U>(X, ld, s, gl, t, a);
+    const double ds = D[s];
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) acc[0][i] += ds * a[i] * a[i];
+  }
+};
+
+}  // namespace
+
+void pchol_precision(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol) {
+  const Pattern& P = *F.pat;
+  const int64_t n = P.n;
+  if (k < 1 || k > n) fail(kEConfig, "rank k must be in [1, " + std::to_string(n) + "]");
+  LF.k = k;
+  LF.L.alloc(sizeof(double) * (size_t)n * k);
+  VL_CUDA(cudaMemsetAsync(LF.L.p, 0, sizeof(double) * (size_t)n * k, C.stream));
+  LF.piv_s.alloc(sizeof(int32_t) * k);
+  DevBuf d, st, part, qc, touched, nt;
+  d.alloc(sizeof(double) * n);
+  qc.alloc(sizeof(double) * n);
+  VL_CUDA(cudaMemsetAsync(qc.p, 0, sizeof(double) * n, C.stream));
+  const int64_t tmax = (int64_t)(P.max_children + 1) * (P.m + 1);
+  touched.alloc(sizeof(int32_t) * std::max<int64_t>(tmax, 1));
+  nt.alloc(64);
+  st.alloc(64);
+  const int grid = std::min<int64_t>(C.num_sms * 8, (n * 32 + kPcThreads - 1) / kPcThreads);
+  part.alloc(sizeof(double) * 4 * (size_t)grid);
+  BView Bv = bview(F, false);
+  launch_rows<1, 1, 1, 0, 0>(C, n, 1, DiagQBody{Bv, F.D.as<double>(), d.as<double>()}, Fin0<0>{});
+  // first pivot: argmax of diag(Q), ties to the lowest factor index (preconditioners.py:311)
+  std::vector<double> dh(n);
+  VL_CUDA(cudaMemcpyAsync(dh.data(), d.p, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+  int32_t bs = 0;
+  for (int64_t s = 1; s < n; ++s)
+    if (dh[s] > dh[bs] || (dh[s] == dh[bs] && P.sperm[s] < P.sperm[bs])) bs = (int32_t)s;
+  int h_i[4] = {bs, 0, 0, 0};
+  double h_dp = dh[bs];
+  VL_CUDA(cudaMemcpyAsync(st.p, h_i, sizeof(h_i), cudaMemcpyHostToDevice, C.stream));
+  VL_CUDA(cudaMemcpyAsync(st.as<char>() + 32, &h_dp, sizeof(double), cudaMemcpyHostToDevice, C.stream));
+  PcState S{st.as<int>(), reinterpret_cast<double*>(st.as<char>() + 32)};
+  const MaternK K = make_matern(F);
+  unsigned* counter = next_counter(C);
+  ProfScope ps(C, "pchol_precision", 0.0);
+  for (int j = 0; j < k; ++j) {
+    qcol_kernel<<<1, 32, 0, C.stream>>>(P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(),
+                                        P.tptr.as<int32_t>(), P.tidx.as<int32_t>(), F.valT.as<double>(),
+                                        F.D.as<double>(), P.m, S, qc.as<double>(), touched.as<int32_t>(), nt.as<int>());
+    pchol_step_kernel<<<grid, kPcThreads, 0, C.stream>>>(n, P.d, P.xy.as<double>(), P.fidx.as<int32_t>(), K, j, k,
+                                                         LF.L.as<double>(), d.as<double>(), S, tol,
+                                                         part.as<double>(), counter, LF.piv_s.as<int32_t>(),
+                                                         qc.as<double>());
+    qclear_kernel<<<1, 256, 0, C.stream>>>(qc.as<double>(), touched.as<int32_t>(), nt.as<int>());
+    VL_LAUNCH_CHECK();
+    C.prof.launches += 3;
+  }
+  VL_CUDA(cudaMemcpyAsync(h_i, st.p, sizeof(h_i), cudaMemcpyDeviceToHost, C.stream));
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+  if (h_i[2]) fail(kEFactorization, "pivoted Cholesky: diagonal went negative; input not PSD");
+  LF.keff = h_i[3];
+  std::vector<int32_t> ps_(LF.keff);
+  if (LF.keff) VL_CUDA(cudaMemcpy(ps_.data(), LF.piv_s.p, sizeof(int32_t) * LF.keff, cudaMemcpyDeviceToHost));
+  LF.piv_f.resize(LF.keff);
+  for (int q = 0; q < LF.keff; ++q) LF.piv_f[q] = P.sperm[ps_[q]];
+}
+
+void rowsel_factor(Ctx& C, const Factor& F, LracFactor& LF, int k) {
+  const Pattern& P = *F.pat;
+  const int64_t n = P.n;
+  if (k < 1 || k > n) fail(kEConfig, "rank k must be in [1, " + std::to_string(n) + "]");
+  DevBuf sc;
+  sc.alloc(sizeof(double) * n);
+  launch_rows<1, 1, 1, 0, 0>(C, n, 1, RowScoreBody{bview(F, false), F.D.as<double>(), sc.as<double>()}, Fin0<0>{});
+  std::vector<double> sh(n);
+  VL_CUDA(cudaMemcpyAsync(sh.data(), sc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+  // scores in factor order; lexsort((arange, -scores)): descending score, ties to the lower index
+  std::vector<double> sf(n);
+  for (int64_t s = 0; s < n; ++s) sf[P.sperm[s]] = sh[s];
+  std::vector<int32_t> ord(n);
+  for (int64_t i = 0; i < n; ++i) ord[i] = (int32_t)i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return sf[a] > sf[b]; });
+  std::vector<int32_t> sel(ord.begin(), ord.begin() + k);
+  std::sort(sel.begin(), sel.end());  // S_k ascending (preconditioners.py:375)
+  std::vector<int32_t> rows(k);
+  for (int c = 0; c < k; ++c) rows[c] = P.iperm[sel[c]];
+  LF.k = k;
+  LF.keff = k;
+  LF.piv_f = sel;
+  LF.piv_s.alloc(sizeof(int32_t) * k);
+  VL_CUDA(cudaMemcpyAsync(LF.piv_s.p, rows.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice, C.stream));
+  LF.L.alloc(sizeof(double) * (size_t)n * k);
+  VL_CUDA(cudaMemsetAsync(LF.L.p, 0, sizeof(double) * (size_t)n * k, C.stream));
+  rowsel_scatter_kernel<<<std::max(1, (k + 127) / 128), 128, 0, C.stream>>>(
+      k, k, P.m, LF.piv_s.as<int32_t>(), P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(),
+      F.D.as<double>(), LF.L.as<double>());
+  VL_LAUNCH_CHECK();
+  VL_CUDA(cudaStreamSynchronize(C.stream));
+}
+
+void diag_sigma_tilde(Ctx& C, const Factor& F, double* out) {
+  const Pattern& P = *F.pat;
+  const int64_t n = P.n;
+  constexpr int Wd = 64;
+  DevBuf E, X;
+  E.alloc(sizeof(double) * (size_t)n * Wd);
+  X.alloc(sizeof(double) * (size_t)n * Wd);
+  DepsCsr dbw{P.tptr.as<int32_t>(), P.tidx.as<int32_t>(), F.valT.as<double>()};
+  double* sums = C.dev_scalars.as<double>();
+  ProfScope ps(C, "diag_sigma_tilde", 0.0);
+  for (int64_t a = 0; a < n; a += Wd) {
+    const int w = (int)std::min<int64_t>(Wd, n - a);
+    eye_block_kernel<<<C.num_sms * 4, 256, 0, C.stream>>>(n, (int)a, w, E.as<double>());
+    VL_LAUNCH_CHECK();
+    dispatch_cols(w, w, [&](auto g, auto nu, auto uu) {
+      constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
+      launch_trsv<G, NU, U, 0>(C, F, false, w, w, dbw, X.as<double>(), TrsvPlain{E.as<double>(), w}, Fin0<0>{});
+      launch_rows<G, NU, U, 1, 0>(C, n, w, DX2Body{F.D.as<double>(), X.as<double>(), w}, CopySumsL<1>{sums});
+    });
+    VL_CUDA(cudaMemcpyAsync(out + a, sums, sizeof(double) * w, cudaMemcpyDeviceToDevice, C.stream));
+  }
 }
 
 }  // namespace vl

@@ -18,18 +18,36 @@ struct LracFactor {
   DevBuf piv_s;             // pivots, storage order
 };
 
-// Woodbury pieces for one W: M = I + L^T diag(W) L = Lm Lm^T.
+// Low-rank-plus-diagonal preconditioner P = L L^T + diag(e)
+// (LowRankPlusDiagonalPreconditioner, preconditioners.py:161-214) for one W:
+// W here is 1/e (the Woodbury diagonal): lrac e = 1/W, pchol-precision and
+// rowsel e = W, l2 (k = 0) e = diag(SigmaTilde) + 1/W.  Wop is the system's W
+// (operator), eq6 selects the system form W + Q (else SigmaTilde + 1/W).
+// M = I + L^T diag(1/e) L = Lm Lm^T.
 struct LracPrec {
   const Factor* F = nullptr;
   const LracFactor* LF = nullptr;
-  const double* W = nullptr;
+  const double* W = nullptr;    // 1/e
+  const double* Wop = nullptr;  // operator W
+  int eq6 = 0;
   DevBuf Lm;                // k x k column-major lower Cholesky factor of M
+  DevBuf own;               // owned 1/e buffer when computed here
+  LracFactor empty;         // k = 0 factor for the diagonal-only (l2) form
   double logdetM = 0.0;
-  double sumlogW = 0.0;
+  double sumlogW = 0.0;     // sum log(1/e)
 };
 
 void lrac_pchol(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol);
 void lrac_prepare(Ctx& C, const Factor& F, const LracFactor& LF, const double* W, LracPrec& P);
+// general form: LF may be null (k = 0); einv = 1/e (null -> Wop, the lrac case)
+void lowrank_prepare(Ctx& C, const Factor& F, const LracFactor* LF, const double* Wop, const double* einv, int eq6,
+                     LracPrec& P);
+// pivoted Cholesky of the precision B^T D^-1 B (PrecisionAccessor, preconditioners.py:228-246)
+void pchol_precision(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol);
+// rowsel factor U = B_S^T D_S^-1/2 over the k rows of largest sum_j B_ij^2 / D_i (preconditioners.py:323-335, 372-379)
+void rowsel_factor(Ctx& C, const Factor& F, LracFactor& LF, int k);
+// diag(SigmaTilde) (vecchia.py:198-212) by batched B^-T solves of identity columns
+void diag_sigma_tilde(Ctx& C, const Factor& F, double* out);
 // z = P^-1 r for t columns (n x t)
 void lrac_apply_inv(Ctx& C, const LracPrec& P, int t, const double* r, double* z);
 // PCG on (SigmaTilde + W^-1) U = Bm  (iterative.py:104-178 per column)
@@ -47,7 +65,7 @@ void lrac_free_handles();
 // with md3x (gamma): xicols (2 x t: h_xi, r_xi), xis = [sum G2 m3, sum m3 / W].
 void lrac_grad(Ctx& C, const LracPrec& Pr, int t, const double* U, const double* V, const double* d3,
                const double* md3x, double* s_out, double* hcols, double* rcols, double* dPt, double* xicols,
-               double* xis);
+               double* xis, int plain = 0);
 double lrac_sumlogW(Ctx& C, int64_t n, const double* W);
 void lrac_probes(Ctx& C, const LracPrec& Pr, int t, const double* Gn, const double* Gk, double* Z, double* V,
                  double* w_host);

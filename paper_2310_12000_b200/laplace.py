@@ -19,13 +19,15 @@ from scipy.special import digamma
 
 from . import _lib
 from . import device as dev
-from .errors import CapabilityError, ConfigError, ConvergenceError
+from .errors import CapabilityError, ConfigError, ConvergenceError, FactorizationError
 from .iterative import (CG_MAX_ITER_DEFAULT, CG_TOL_DEFAULT, ProbeSet, slq_from_parts, ste_combine,
                         tridiag_from_cg)
 
 MODE_CG_TOL_CAP = 1e-4
 EQ5_VARIANTS = ("lrac", "l2")
-SUPPORTED_PRECONDITIONERS = ("vadu", "l1", "lva", "diag", "identity", "lrac")
+SUPPORTED_PRECONDITIONERS = ("vadu", "l1", "lva", "diag", "identity", "lrac", "pchol-precision", "rowsel", "l2")
+# low-rank-plus-diagonal variants (Woodbury on the device, csrc/lrac.cu)
+LOWRANK_VARIANTS = ("lrac", "pchol-precision", "rowsel", "l2")
 # eq6 variants on the device (csrc/laplace.cu precond_dinv): sandwich B^T diag(d) B or diagonal diag(d)
 EQ6_VARIANT_ID = {"vadu": 0, "l1": 1, "lva": 2, "diag": 3, "identity": 4}
 CV_VARIANTS = ("vadu", "l1", "lrac")  # variants with a control variate in the gradient (laplace.py:414-431)
@@ -77,7 +79,7 @@ def _check_supported(cfg):
     if cfg.preconditioner not in SUPPORTED_PRECONDITIONERS:
         raise CapabilityError(f"preconditioner {cfg.preconditioner!r} is not available on the device backend "
                               f"(supported: {', '.join(SUPPORTED_PRECONDITIONERS)})")
-    want = "eq7" if cfg.preconditioner == "lrac" else "eq6"
+    want = "eq7" if cfg.preconditioner in EQ5_VARIANTS else "eq6"
     if cfg.resolved_split() != want:
         raise CapabilityError(f"the device {cfg.preconditioner} path uses the {want} log-determinant split")
 
@@ -86,14 +88,19 @@ class LracFactorHandle:
     """Rank-k pivoted Cholesky of the exact covariance, cached on the factor
     like the reference's factor.cache[("sigma_pchol", k)] (laplace.py:128-136)."""
 
-    def __init__(self, factor, k, tol=0.0):
+    def __init__(self, factor, k, tol=0.0, kind=0):
+        # kind 0: pivoted Cholesky of Sigma (lrac); 1: of the precision (pchol-precision); 2: rowsel
         self.factor = factor
         self.k = int(k)
         piv = np.zeros(self.k, dtype=np.int32)
         keff = C.c_int(0)
         h = C.c_void_p()
-        _lib.call("vl_lrac_create", factor.ctx.h, factor.h, self.k, float(tol), C.byref(h), _lib.ptr(piv),
-                  C.byref(keff))
+        if kind == 0:
+            _lib.call("vl_lrac_create", factor.ctx.h, factor.h, self.k, float(tol), C.byref(h), _lib.ptr(piv),
+                      C.byref(keff))
+        else:
+            _lib.call("vl_lowrank_create", factor.ctx.h, factor.h, int(kind), self.k, float(tol), C.byref(h),
+                      _lib.ptr(piv), C.byref(keff))
         self.h = h
         self.keff = int(keff.value)
         self.pivots = piv[: self.keff].astype(int)
@@ -116,13 +123,27 @@ class LracFactorHandle:
 
 
 def lrac_factor(factor, cfg):
+    """The theta-only low-rank factor of the variant, cached on the factor
+    (laplace.py:128-136): lrac -> Sigma's pivoted Cholesky, pchol-precision ->
+    the precision's, rowsel -> B_S^T D_S^-1/2."""
     k = cfg.rank if cfg.rank is not None else default_rank(factor.n)
-    key = ("sigma_pchol", int(k))
+    kind = {"lrac": 0, "pchol-precision": 1, "rowsel": 2}[cfg.preconditioner]
+    key = (("sigma_pchol", "prec_pchol", "rowsel")[kind], int(k))
     lf = factor.cache.get(key)
     if lf is None:
-        lf = LracFactorHandle(factor, k)
+        lf = LracFactorHandle(factor, k, kind=kind)
         factor.cache[key] = lf
     return lf
+
+
+def diag_sigma_tilde_dev(factor):
+    """diag(SigmaTilde) on the device (vecchia.py:198-212), cached on the factor."""
+    d = factor.cache.get("diag_sigma_tilde")
+    if d is None:
+        d = dev.empty(factor.ctx, factor.n, 1)
+        _lib.call("vl_diag_sigma_tilde", factor.ctx.h, factor.h, _lib.ptr(d))
+        factor.cache["diag_sigma_tilde"] = d
+    return d
 
 
 class LaplaceState:
@@ -211,6 +232,14 @@ def find_mode(factor, lik, y, F, cfg, trace=None):
         st = _lib.lib().vl_find_mode_lrac(ctx.h, factor.h, lf.h, C.byref(lk), C.byref(nc), _lib.ptr(y_d),
                                           _lib.ptr(F_d), _lib.ptr(b), _lib.ptr(W), _lib.ptr(d1), _lib.ptr(d3), out,
                                           _lib.ptr(cg_its), int(cg_its.size))
+    elif cfg.preconditioner in ("pchol-precision", "rowsel", "l2"):
+        l2 = cfg.preconditioner == "l2"
+        lf = None if l2 else lrac_factor(factor, cfg)
+        dst = diag_sigma_tilde_dev(factor) if l2 else None
+        st = _lib.lib().vl_find_mode_lowrank(ctx.h, factor.h, None if l2 else lf.h, 2 if l2 else 1,
+                                             _lib.ptr(dst) if l2 else None, C.byref(lk), C.byref(nc),
+                                             _lib.ptr(y_d), _lib.ptr(F_d), _lib.ptr(b), _lib.ptr(W), _lib.ptr(d1),
+                                             _lib.ptr(d3), out, _lib.ptr(cg_its), int(cg_its.size))
     else:
         st = _lib.lib().vl_find_mode(ctx.h, factor.h, C.byref(lk), C.byref(nc), _lib.ptr(y_d), _lib.ptr(F_d),
                                      _lib.ptr(b), _lib.ptr(W), _lib.ptr(d1), _lib.ptr(d3), out,
@@ -262,33 +291,62 @@ VaduPreconditioner = Eq6Preconditioner
 
 
 class LracPreconditioner:
-    """P = L L^T + diag(1/W) on the device (preconditioners.py:167-214)."""
+    """P = L L^T + diag(e) on the device (LowRankPlusDiagonalPreconditioner,
+    preconditioners.py:161-214): lrac (L from Sigma, e = 1/W, eq7 system),
+    pchol-precision / rowsel (e = W, eq6) and l2 (k = 0, e = diag(SigmaTilde)
+    + 1/W, eq7; the reference's diagonal 'l2')."""
 
-    name = "lrac"
-
-    def __init__(self, factor, W_dev, lf):
+    def __init__(self, factor, W_dev, lf, name="lrac"):
         self.factor = factor
         self.W_dev = W_dev
         self.lf = lf
+        self.name = name
         out = np.zeros(2)
         h = C.c_void_p()
-        _lib.call("vl_lrac_prepare", factor.ctx.h, lf.h, _lib.ptr(W_dev), C.byref(h), _lib.ptr(out))
+        if name == "lrac":
+            _lib.call("vl_lrac_prepare", factor.ctx.h, lf.h, _lib.ptr(W_dev), C.byref(h), _lib.ptr(out))
+        else:
+            self.einv = dev.empty(factor.ctx, factor.n, 1)
+            kind = 2 if name == "l2" else 1
+            dst = diag_sigma_tilde_dev(factor) if name == "l2" else None
+            if name != "l2":
+                nonpos = np.zeros(1)
+                _lib.call("vl_sum_log", factor.ctx.h, factor.n, _lib.ptr(W_dev), _lib.ptr(nonpos))
+                if not np.isfinite(nonpos[0]):
+                    raise FactorizationError(f"{name} diagonal part must be positive and finite")
+            _lib.call("vl_lowrank_einv", factor.ctx.h, factor.n, kind, _lib.ptr(W_dev),
+                      _lib.ptr(dst) if dst is not None else None, _lib.ptr(self.einv))
+            _lib.call("vl_lowrank_prepare", factor.ctx.h, factor.h, None if lf is None else lf.h, _lib.ptr(W_dev),
+                      _lib.ptr(self.einv), 0 if name == "l2" else 1, C.byref(h), _lib.ptr(out))
         self.h = h
         self.logdet_M = float(out[0])
-        self.sumlogW = float(out[1])
-        self.pivots = lf.pivots
+        self.sumlogW = float(out[1])  # sum log(1/e)
+        self.pivots = lf.pivots if lf is not None else np.zeros(0, dtype=int)
         self._sums = None
+        self._sumlogWop = None
+
+    @property
+    def sumlogWop(self):
+        """sum log W of the system (the eq7 log-det split, laplace.py:335)."""
+        if self._sumlogWop is None:
+            if self.name == "lrac":
+                self._sumlogWop = self.sumlogW
+            else:
+                out = np.zeros(1)
+                _lib.call("vl_sum_log", self.factor.ctx.h, self.factor.n, _lib.ptr(self.W_dev), _lib.ptr(out))
+                self._sumlogWop = float(out[0])
+        return self._sumlogWop
 
     def logdet(self):
         return -self.sumlogW + self.logdet_M
 
     @property
     def k(self):
-        return self.lf.keff
+        return self.lf.keff if self.lf is not None else 0
 
     @property
     def U(self):
-        return self.lf.L()
+        return self.lf.L() if self.lf is not None else np.zeros((self.factor.n, 0))
 
     def sums(self):
         if self._sums is None:
@@ -312,8 +370,9 @@ class LracPreconditioner:
 
 def build_preconditioner(factor, W_dev, cfg):
     _check_supported(cfg)
-    if cfg.preconditioner == "lrac":
-        return LracPreconditioner(factor, W_dev, lrac_factor(factor, cfg))
+    if cfg.preconditioner in LOWRANK_VARIANTS:
+        lf = None if cfg.preconditioner == "l2" else lrac_factor(factor, cfg)
+        return LracPreconditioner(factor, W_dev, lf, cfg.preconditioner)
     return Eq6Preconditioner(factor, W_dev, cfg.preconditioner)
 
 
@@ -352,7 +411,7 @@ def _lrac_normals(factor, seed, t, k, cols=None):
     Gk = rng.standard_normal((k, t))
     if cols is not None:
         Gn, Gk = Gn[:, cols[0]:cols[1]], Gk[:, cols[0]:cols[1]]
-    val = (pat.to_dev(np.ascontiguousarray(Gn)), dev.upload(factor.ctx, np.ascontiguousarray(Gk)))
+    val = (pat.to_dev(np.ascontiguousarray(Gn)), dev.upload(factor.ctx, np.ascontiguousarray(Gk)) if k else None)
     _G_CACHE.append((pat, key, val))
     del _G_CACHE[:-2]
     return val
@@ -361,14 +420,14 @@ def _lrac_normals(factor, seed, t, k, cols=None):
 def make_probes(factor, state, cfg, cols=None):
     """Fresh N(0, P) probes for the current mode, deterministic in the seed."""
     P = build_preconditioner(factor, state._dev["W"], cfg)
-    if cfg.preconditioner == "lrac":
+    if cfg.preconditioner in LOWRANK_VARIANTS:
         Gn, Gk = _lrac_normals(factor, cfg.probe_seed, cfg.t, P.k, cols)
         t = int(Gn.shape[1])
         Z = dev.empty(factor.ctx, factor.n, t)
         V = dev.empty(factor.ctx, factor.n, t)
         w = np.zeros(t)
-        _lib.call("vl_lrac_probes", factor.ctx.h, P.h, t, _lib.ptr(Gn), _lib.ptr(Gk), _lib.ptr(Z), _lib.ptr(V),
-                  _lib.ptr(w))
+        _lib.call("vl_lrac_probes", factor.ctx.h, P.h, t, _lib.ptr(Gn), _lib.ptr(Gk) if P.k else None,
+                  _lib.ptr(Z), _lib.ptr(V), _lib.ptr(w))
         ps = ProbeSet(Z, cfg.probe_seed, P.name, pattern=factor.pattern, psolves_dev=V, weights=w,
                       shard=(0 if cols is None else cols[0], cfg.t))
         return ps, P
@@ -413,7 +472,7 @@ def _run_probe_solves(factor, state, P, cfg, probes):
     res = np.zeros(t)
     al = np.zeros((max(cap, 1), t))
     be = np.zeros((max(cap, 1), t))
-    if cfg.preconditioner == "lrac":
+    if cfg.preconditioner in LOWRANK_VARIANTS:
         _lib.call("vl_lrac_pcg", factor.ctx.h, P.h, t, _lib.ptr(probes.Z_dev), _lib.ptr(U), float(cfg.mode_cg_tol),
                   int(cfg.cg_max_iter), 1, _lib.ptr(its), _lib.ptr(conv), _lib.ptr(res), _lib.ptr(al), _lib.ptr(be),
                   max(cap, 1))
@@ -433,7 +492,7 @@ def solve_system(factor, state, rhs_dev, cfg, tol=None, P=None):
     k = int(rhs_dev.shape[1])
     u = dev.empty(factor.ctx, factor.n, k)
     its = np.zeros(k, dtype=np.int32)
-    if cfg.preconditioner == "lrac":
+    if cfg.preconditioner in LOWRANK_VARIANTS:
         P = P if P is not None else build_preconditioner(factor, state._dev["W"], cfg)
         _lib.call("vl_lrac_solve_system", factor.ctx.h, P.h, k, _lib.ptr(rhs_dev), _lib.ptr(u), float(tol),
                   int(cfg.cg_max_iter), _lib.ptr(its))
@@ -469,7 +528,7 @@ def logdet_system(factor, state, cfg, probes=None, P=None, comm=None):
         parts = comm.allgather_cols(parts, probes.shard)
     slq = float(sum(parts[i] for i in range(len(parts)))) / len(parts)
     if cfg.resolved_split() == "eq7":
-        return P.sumlogW + P.logdet() + slq
+        return P.sumlogWop + P.logdet() + slq
     sums = P.sums()
     return float(sums[0]) + P.logdet() + slq
 
@@ -505,7 +564,7 @@ def gradient(state, factor, lik, X, cfg, probes=None, P=None, comm=None):
     s = dev.empty(ctx, n, 1)
     cols = np.zeros((4, t))
     xicols = np.zeros((2, t))
-    if cfg.preconditioner == "lrac":
+    if cfg.preconditioner in ("lrac", "l2"):
         return _gradient_lrac(state, factor, lik, X, cfg, probes, P, comm, md3x, s)
     plain = 0 if cfg.preconditioner in CV_VARIANTS else 1
     if comm is not None and (comm.world > 1 or getattr(comm, "force_split", False)):
@@ -556,15 +615,16 @@ def _gradient_lrac(state, factor, lik, X, cfg, probes, P, comm, md3x, s):
     dPt = np.zeros(2)
     xicols = np.zeros((2, t))
     xis = np.zeros(2)
+    plain = 0 if cfg.preconditioner == "lrac" else 1
     _lib.call("vl_lrac_grad", ctx.h, P.h, t, _lib.ptr(probes.solves_dev), _lib.ptr(probes.psolves_dev),
               _lib.ptr(dv["d3"]), _lib.ptr(md3x) if gamma else None, _lib.ptr(s), _lib.ptr(hcols),
-              _lib.ptr(rcols), _lib.ptr(dPt), _lib.ptr(xicols), _lib.ptr(xis))
+              _lib.ptr(rcols), _lib.ptr(dPt), _lib.ptr(xicols), _lib.ptr(xis), plain)
     tvec, _ = solve_system(factor, state, s, cfg, tol=cfg.mode_cg_tol, P=P)
     terms = np.zeros(4)
     _lib.call("vl_grad_scalar_terms", ctx.h, factor.h, _lib.ptr(dv["b"]), _lib.ptr(tvec), _lib.ptr(terms))
     dtheta = np.empty(2)
     for k in (0, 1):
-        ste = ste_combine(hcols[k], rcols[k], float(dPt[k]))
+        ste = ste_combine(hcols[k], None if plain else rcols[k], float(dPt[k]))
         dtheta[k] = 0.5 * terms[2 * k] + 0.5 * (0.0 + ste) - terms[2 * k + 1]
     dxi = np.empty(lik.n_xi)
     if gamma:
@@ -574,7 +634,7 @@ def _gradient_lrac(state, factor, lik, X, cfg, probes, P, comm, md3x, s):
         a = lik.shape
         dlogp = n * (np.log(a) + 1.0 - digamma(a)) + g3[0]
         ex = float(xis[1])
-        ste = ste_combine(xicols[0], xicols[1], float(xis[0] - xis[1]))
+        ste = ste_combine(xicols[0], None if plain else xicols[1], float(xis[0] - xis[1]))
         dxi[0] = -dlogp + 0.5 * (ex + ste) + g3[1]
     X = np.asarray(X, dtype=float)
     if X.ndim == 1:

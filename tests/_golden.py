@@ -10,7 +10,7 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 LAPLACE_CASES = ["logit_vadu_n400", "logit_vadu_n1500", "logit_vadu_cov_n300",
                  "probit_vadu_n300", "gamma_vadu_n300", "logit_lrac_n300",
                  "gamma_lrac_cov_n300", "poisson_vadu_n300", "logit_lva_n300", "logit_diag_n300",
-                 "logit_identity_n300"]
+                 "logit_identity_n300", "logit_pcholprec_n300", "logit_rowsel_n300", "gamma_l2_n300"]
 
 
 def load(name):

@@ -267,6 +267,9 @@ def main():
     laplace_case("poisson_vadu_n300", 300, seed=18, rho=0.1, m=8, t=6, family="poisson")
     for pc, sd in (("lva", 25), ("diag", 26), ("identity", 27)):
         laplace_case(f"logit_{pc}_n300", 300, seed=sd, rho=0.1, m=8, t=6, precond=pc)
+    laplace_case("logit_pcholprec_n300", 300, seed=28, rho=0.1, m=8, t=6, precond="pchol-precision", rank=40)
+    laplace_case("logit_rowsel_n300", 300, seed=29, rho=0.1, m=8, t=6, precond="rowsel", rank=40)
+    laplace_case("gamma_l2_n300", 300, seed=30, rho=0.1, m=8, t=6, precond="l2", family="gamma", shape=2.0)
     predict_case("poisson_pred_n500", 500, 60, seed=19, rho=0.1, m=10)
     fit_case("fit_logit_n400", 400, seed=23, rho=0.1, m=10, t=8)
     fit_case("fit_gamma_n300", 300, seed=24, rho=0.1, m=8, t=6, family="gamma", max_iters=4)
