@@ -38,6 +38,7 @@ from .predict import (
     gaussian_log_score,
     latent_mean,
     latent_var_exact,
+    latent_var_lanczos,
     latent_var_sim,
     predict_latent,
     prediction_blocks,

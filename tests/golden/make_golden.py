@@ -165,6 +165,12 @@ def predict_case(name, n, n_p, seed, rho, m, family="poisson", s=24, sim_seed=11
     omega = latent_mean(st, blocks, Fp)
     var_sim, cov_sim = latent_var_sim(st, f, blocks, s=s, seed=sim_seed, cfg=cfg, full=True)
     var_exact = latent_var_exact(st, f, blocks)
+    from vlgp.predict import latent_var_lanczos
+    lz = {}
+    for variant in ("none", "l1", "l2"):
+        v, order = latent_var_lanczos(st, f, blocks, 20, variant=variant, cfg=cfg)
+        lz[f"var_lz_{variant}"] = v
+        lz[f"order_lz_{variant}"] = order
     nbr = np.full((n, m), -1, dtype=np.int64)
     for i, q in enumerate(nb):
         nbr[i, : len(q)] = q
@@ -173,7 +179,7 @@ def predict_case(name, n, n_p, seed, rho, m, family="poisson", s=24, sim_seed=11
                F=np.zeros(n), perm=perm, nbr=nbr, b=st.b, W=st.W, newton_iters=st.newton_iters,
                pred_nbr=np.stack(blocks.neighbors).astype(np.int64), Bpo_vals=blocks.Bpo.data.reshape(n_p, -1),
                Dp=blocks.Dp, omega=omega, s=s, sim_seed=sim_seed, var_sim=var_sim, cov_sim=cov_sim,
-               var_exact=var_exact, truth=ball[n:])
+               var_exact=var_exact, truth=ball[n:], **lz)
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
     print(f"{name}: n={n} n_p={n_p} newton={st.newton_iters} var_sim[:3]={var_sim[:3]}")
 

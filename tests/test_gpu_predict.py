@@ -69,3 +69,11 @@ def test_duplicate_prediction_point_rejected(case):
     vg, g, f, st, cfg, blocks = case
     with pytest.raises(vg.DataError):
         vg.prediction_blocks(f, g["coords"][:3])
+
+
+@pytest.mark.parametrize("variant", ["none", "l1", "l2"])
+def test_latent_var_lanczos(case, variant):
+    vg, g, f, st, cfg, blocks = case
+    var, order = vg.latent_var_lanczos(st, f, blocks, 20, variant=variant, cfg=cfg)
+    assert order == int(g[f"order_lz_{variant}"])
+    np.testing.assert_allclose(var, g[f"var_lz_{variant}"], rtol=1e-7)
