@@ -68,6 +68,13 @@ struct Ctx {
   // dense head block of the solves (see head.cuh) and its scratch
   bool use_slabs = true;  // coalesced dependency slabs for the single-RHS solves
   bool use_head = true;
+  // sandwich-PCG product mode (pcg.cu) for t == 1 / t > 1:
+  //   0: B h + B^T tmp passes, 1: B^T(om o y) fused into the backward solve,
+  //   2: B^T(om o y) as a side-stream pass concurrent with the forward solve
+  int pmode1 = 0;
+  int pmodeT = 1;
+  cudaStream_t side = nullptr;  // created on first use
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DevBuf head_Y, head_Xh;
   // debug: per-row completion timestamps of the next triangular solves (n entries)
   long long* debug_tstamp = nullptr;

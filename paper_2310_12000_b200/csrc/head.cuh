@@ -59,7 +59,11 @@ __global__ void __launch_bounds__(kRowsThreads) head_rhs_kernel(int H, int t, in
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if (lane == 0) Y[h] = body.rhs(s, 0, acc[0][0]) - part;
+      if (lane == 0) {
+        const double rv = body.rhs(s, 0, acc[0][0]);
+        if constexpr (PsumOf<Body>::value) body.keep_rhs(s, 0, rv);
+        Y[h] = rv - part;
+      }
     }
   } else
   for (int64_t h0 = gwarp * GPW; h0 < H; h0 += nwarps * GPW) {
@@ -71,6 +75,8 @@ __global__ void __launch_bounds__(kRowsThreads) head_rhs_kernel(int H, int t, in
     for (int i = 0; i < NC; ++i) {
       const int c = CL::col(gl, i);
       ys[i] = c < t ? body.rhs(s, c, acc[0][i]) : 0.0;
+      if constexpr (PsumOf<Body>::value)
+        if (c < t) body.keep_rhs(s, c, ys[i]);
     }
     if (EXT) {
       // children outside the head (head children are handled by X^T); 8 in flight
@@ -242,14 +248,91 @@ __global__ void __launch_bounds__(kRowsThreads) head_out_kernel(int H, int t, in
       if (c < t) {
         double xv = Xh[h * t + c];
         for (int k = 1; k < ksplit; ++k) xv += Xh[(size_t)k * H * t + h * t + c];
-        body.out(s, c, xv, acc[0][i]);
         __stcg(x + s * ld + c, sanitize(xv));
+        body.out(s, c, xv, acc[0][i]);
       }
     }
   }
   if constexpr (NR > 0) {
     block_reduce_cols<G, NU, U, NR, 0>(acc, t, partials + (size_t)(slot_base + blockIdx.x) * NR * t, rsh);
     grid_finalize<NR, 0>(partials, counter, t, fin, rsh, total_slots);
+  }
+}
+
+// Fused product of a backward solve (PsumOf<Body>) on the head rows, run
+// after head_out when all of y is final:  p_s = om_s y_s + sum_c B_cs om_c y_c
+// over ALL children c (head or not).  Single column: warp per row.
+template <int G, int NU, int U, class Body>
+__global__ void __launch_bounds__(kRowsThreads) head_psum_kernel(int H, int t, int ld,
+                                                                 const int32_t* __restrict__ head_rows,
+                                                                 const int32_t* __restrict__ tptr,
+                                                                 const int32_t* __restrict__ tidx,
+                                                                 const double* __restrict__ valT,
+                                                                 const double* __restrict__ x, Body body,
+                                                                 const int* __restrict__ gate) {
+  if (gate != nullptr && *((volatile const int*)gate) == 0) return;
+  constexpr int GPW = 32 / G;
+  constexpr int NC = NU * U;
+  const int lane = threadIdx.x & 31, gl = lane % G, gi = lane / G;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if constexpr (G == 1 && NU == 1 && U == 1) {
+    for (int64_t h = gwarp; h < H; h += nwarps) {
+      const int64_t s = head_rows[h];
+      const int e0 = tptr[s], e1 = tptr[s + 1];
+      double part = 0.0;
+      for (int e = e0 + lane; e < e1; e += 32) {
+        const int32_t ch = tidx[e];
+        part += (valT[e] * __ldg(body.om + ch)) * __ldcg(x + (int64_t)ch * ld);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane == 0) body.pout[s] = fma(__ldg(body.om + s), __ldcg(x + s), part);
+    }
+  } else {
+    for (int64_t h0 = gwarp * GPW; h0 < H; h0 += nwarps * GPW) {
+      const int64_t h = h0 + gi;
+      if (h >= H) continue;
+      const int64_t s = head_rows[h];
+      const double os = __ldg(body.om + s);
+      double ps[NC];
+#pragma unroll
+      for (int k = 0; k < NU; ++k) {
+        const int c = U * (gl + G * k);
+        double v[U];
+        if (c < t) ld_cg_unit<U>(x + s * ld + c, v);
+        else
+#pragma unroll
+          for (int i = 0; i < U; ++i) v[i] = 0.0;
+#pragma unroll
+        for (int i = 0; i < U; ++i) ps[U * k + i] = os * v[i];
+      }
+      const int e0 = tptr[s], e1 = tptr[s + 1];
+      for (int e = e0; e < e1; ++e) {
+        const int32_t ch = tidx[e];
+        const double wo = valT[e] * __ldg(body.om + ch);
+#pragma unroll
+        for (int k = 0; k < NU; ++k) {
+          const int c = U * (gl + G * k);
+          double v[U];
+          if (c < t) ld_cg_unit<U>(x + (int64_t)ch * ld + c, v);
+          else
+#pragma unroll
+            for (int i = 0; i < U; ++i) v[i] = 0.0;
+#pragma unroll
+          for (int i = 0; i < U; ++i) ps[U * k + i] += wo * v[i];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NU; ++k) {
+        const int c = U * (gl + G * k);
+        if (c < t) {
+          double* dst = body.pout + s * ld + c;
+          if constexpr (U == 2) *reinterpret_cast<double2*>(dst) = make_double2(ps[2 * k], ps[2 * k + 1]);
+          else *dst = ps[k];
+        }
+      }
+    }
   }
 }
 

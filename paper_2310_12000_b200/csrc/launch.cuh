@@ -41,8 +41,8 @@ void dispatch_cols(int t, int ld, F&& f) {
 
 unsigned* next_counter(Ctx& C);
 int coop_grid(Ctx& C, const void* func, size_t smem);
-cudaEvent_t prof_begin(Ctx& C);
-void prof_end(Ctx& C, cudaEvent_t a);
+cudaEvent_t prof_begin(Ctx& C, cudaStream_t st = nullptr);  // nullptr: C.stream
+void prof_end(Ctx& C, cudaEvent_t a, cudaStream_t st = nullptr);
 
 // Tag the kernels launched in a scope (algorithmic bytes per launch).
 struct ProfScope {
@@ -181,7 +181,8 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
   const int hlanes = (t == 1 && !fwd) ? 32 : G;
   const int hgrid = head ? std::max(1, std::min(4 * C.num_sms, (int)((H * hlanes + kRowsThreads - 1) / kRowsThreads))) : 0;
   const int total = main_slots + 2 * hgrid;
-  C.prof.launches += 1 + (single ? 1 : (long long)segs.size()) + (head ? 3 : 0);
+  C.prof.launches += 1 + (single ? 1 : (long long)segs.size()) + (head ? 3 : 0) +
+                     ((head && !fwd && PsumOf<Body>::value) ? 1 : 0);
   cudaEvent_t ev = (C.prof.on && C.prof.tag) ? prof_begin(C) : nullptr;
   VL_CUDA(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)n * ld, C.stream));
   double* partials = C.red_partial.as<double>();
@@ -222,6 +223,15 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
     head_out_kernel<G, NU, U, NR, Body, Fin><<<hgrid, kRowsThreads, hsm, C.stream>>>(
         H, t, ld, hrows, Xh, ksplit, x, body, fin, partials, counter, slot_out, total, gate);
     VL_LAUNCH_CHECK();
+    if constexpr (PsumOf<Body>::value) {
+      if (!fwd) {
+        const int pl = (t == 1) ? 32 : G;
+        const int pg = std::max(1, std::min(4 * C.num_sms, (int)((H * pl + kRowsThreads - 1) / kRowsThreads)));
+        head_psum_kernel<G, NU, U, Body><<<pg, kRowsThreads, 0, C.stream>>>(
+            H, t, ld, hrows, P.tptr.as<int32_t>(), P.tidx.as<int32_t>(), F.valT.as<double>(), x, body, gate);
+        VL_LAUNCH_CHECK();
+      }
+    }
   };
   auto run_main = [&](int slot0) {
     if (single) {

@@ -17,7 +17,7 @@ unsigned* next_counter(Ctx& C) {
   return base + slot;
 }
 
-cudaEvent_t prof_begin(Ctx& C) {
+cudaEvent_t prof_begin(Ctx& C, cudaStream_t st) {
   Prof& P = C.prof;
   auto take = [&]() {
     cudaEvent_t e;
@@ -30,11 +30,11 @@ cudaEvent_t prof_begin(Ctx& C) {
     return e;
   };
   cudaEvent_t a = take();
-  VL_CUDA(cudaEventRecord(a, C.stream));
+  VL_CUDA(cudaEventRecord(a, st ? st : C.stream));
   return a;
 }
 
-void prof_end(Ctx& C, cudaEvent_t a) {
+void prof_end(Ctx& C, cudaEvent_t a, cudaStream_t st) {
   Prof& P = C.prof;
   cudaEvent_t b;
   if (!P.free_events.empty()) {
@@ -43,7 +43,7 @@ void prof_end(Ctx& C, cudaEvent_t a) {
   } else {
     VL_CUDA(cudaEventCreate(&b));
   }
-  VL_CUDA(cudaEventRecord(b, C.stream));
+  VL_CUDA(cudaEventRecord(b, st ? st : C.stream));
   P.pending.push_back({std::string(P.tag), a, b, P.bytes});
 }
 

@@ -23,6 +23,9 @@
 
 #include <cuda_runtime.h>
 
+#include <type_traits>
+#include <utility>
+
 #include "common.cuh"
 
 namespace vl {
@@ -62,6 +65,24 @@ VL_D void ld_cg_unit(const double* p, double* out) {
     out[0] = a;
   }
 }
+
+// Optional fused product of the backward solve (Body::kPsum): alongside
+// y = B^-T rhs the rows also emit p = B^T (om o y), i.e.
+//   p_s = om_s y_s + sum_{e in deps(s)} w_e om_dep(e) y_dep(e),
+// from the same dependency gathers (om = body.om, a per-row weight).  Such a
+// body's rhs() is pure; the row's epilogue calls
+//   body.fin_row(s, c, x, rhs, psum)   (stores p = om_s x + psum and,
+//                                       optionally, the rhs value itself)
+// after x_s is published, and the head path calls body.keep_rhs(s, c, rhs).
+#ifndef VL_PS_NOGATHER
+#define VL_OMLOAD(p) __ldg(p)
+#else  // diagnostic: fused product without the om gathers (wrong values)
+#define VL_OMLOAD(p) 1.0
+#endif
+template <class T, class = void>
+struct PsumOf : std::false_type {};
+template <class T>
+struct PsumOf<T, std::void_t<decltype(T::kPsum)>> : std::bool_constant<T::kPsum> {};
 
 template <int NR>
 struct Fin0 {
@@ -235,6 +256,23 @@ struct DepsCsr {
   VL_D int32_t idx(int64_t b) const { return ind[b]; }
   VL_D double w(int64_t b) const { return val[b]; }
 };
+// children CSR + per-entry folded weights val2[e] = val[e] * om[ind[e]] of a
+// fused backward product (streamed with the values instead of gathered)
+struct DepsCsrW2 {
+  const int32_t* ptr;
+  const int32_t* ind;
+  const double* val;
+  const double* val2;
+  VL_D int count(int64_t s) const { return ptr[s + 1] - ptr[s]; }
+  VL_D int64_t base(int64_t s) const { return ptr[s]; }
+  VL_D int32_t idx(int64_t b) const { return ind[b]; }
+  VL_D double w(int64_t b) const { return val[b]; }
+  VL_D double w2(int64_t b) const { return val2[b]; }
+};
+template <class T, class = void>
+struct HasW2 : std::false_type {};
+template <class T>
+struct HasW2<T, std::void_t<decltype(std::declval<T>().w2(0))>> : std::true_type {};
 
 // One solve row per group: rhs, dependency gather (optionally polling the
 // sentinel), epilogue and store.  Called by every lane of the warp.
@@ -248,27 +286,44 @@ VL_D void trsv_row(int64_t p, int64_t pend_, int t, int ld, const int32_t* __res
 #endif
   constexpr int BATCH = (NC == 1) ? 32 : (NC == 2 ? VL_BATCH2 : 8);
   using CL = Cols<G, NU, U>;
+  constexpr bool PS = PsumOf<Body>::value;
   const int32_t so = (p < pend_) ? order[p] : -1;
   const bool valid = so >= 0;
   const int64_t s = valid ? so : 0;
-  double xs[NC];
+  double xs[NC], ps[NC], rh[NC];
+  auto take_rhs = [&]() {
 #pragma unroll
-  for (int i = 0; i < NC; ++i) {
-    const int c = CL::col(gl, i);
-    xs[i] = (valid && c < t) ? body.rhs(s, c, acc0[i]) : 0.0;
-  }
+    for (int i = 0; i < NC; ++i) {
+      const int c = CL::col(gl, i);
+      xs[i] = (valid && c < t) ? body.rhs(s, c, acc0[i]) : 0.0;
+      rh[i] = xs[i];
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < NC; ++i) ps[i] = 0.0;
+#ifndef VL_RHS_LATE
+  take_rhs();  // (taking it after the first gathers measured slower at t = 50)
+#endif
   const int cs = valid ? deps.count(s) : 0;
   const int64_t b0 = valid ? deps.base(s) : 0;
   const int cmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)cs);
   for (int e0 = 0; e0 < cmax; e0 += BATCH) {
     int32_t j[BATCH];
-    double w[BATCH];
+    double w[BATCH], o[BATCH];
     double v[BATCH][NC];
 #pragma unroll
     for (int q = 0; q < BATCH; ++q) {
       const bool on = e0 + q < cs;
       j[q] = on ? deps.idx(b0 + e0 + q) : 0;
       w[q] = on ? deps.w(b0 + e0 + q) : 0.0;
+    }
+    if constexpr (PS) {
+#pragma unroll
+      for (int q = 0; q < BATCH; ++q) {
+        const bool on = e0 + q < cs;
+        if constexpr (HasW2<Deps>::value) o[q] = on ? deps.w2(b0 + e0 + q) : 0.0;
+        else o[q] = on ? w[q] * VL_OMLOAD(body.om + j[q]) : 0.0;
+      }
     }
 #pragma unroll
     for (int q = 0; q < BATCH; ++q)
@@ -282,6 +337,9 @@ VL_D void trsv_row(int64_t p, int64_t pend_, int t, int ld, const int32_t* __res
           for (int i = 0; i < U; ++i) v[q][U * k + i] = 0.0;
         }
       }
+#ifdef VL_RHS_LATE
+    if (e0 == 0) take_rhs();
+#endif
     if constexpr (POLL) {
       // warp-converged polling: the whole warp re-polls its pending entries together
       unsigned ns = 8;
@@ -310,14 +368,15 @@ VL_D void trsv_row(int64_t p, int64_t pend_, int t, int ld, const int32_t* __res
 #pragma unroll
     for (int q = 0; q < BATCH; ++q)
 #pragma unroll
-      for (int i = 0; i < NC; ++i) xs[i] -= w[q] * v[q][i];
+      for (int i = 0; i < NC; ++i) {
+        xs[i] -= w[q] * v[q][i];
+        if constexpr (PS) ps[i] += o[q] * v[q][i];
+      }
   }
+#ifdef VL_RHS_LATE
+  if (cmax == 0) take_rhs();
+#endif
   if (valid) {
-#pragma unroll
-    for (int i = 0; i < NC; ++i) {
-      const int c = CL::col(gl, i);
-      if (c < t) body.out(s, c, xs[i], acc0[i]);
-    }
 #pragma unroll
     for (int k = 0; k < NU; ++k) {
       const int c = U * (gl + G * k);
@@ -328,6 +387,19 @@ VL_D void trsv_row(int64_t p, int64_t pend_, int t, int ld, const int32_t* __res
         } else {
           __stcg(dst, sanitize(xs[k]));
         }
+      }
+    }
+    // epilogue after the store: its loads are off the dependency chain
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int c = CL::col(gl, i);
+      if (c < t) body.out(s, c, xs[i], acc0[i]);
+    }
+    if constexpr (PS) {
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        const int c = CL::col(gl, i);
+        if (c < t) body.fin_row(s, c, xs[i], rh[i], ps[i]);
       }
     }
     if (tstamp != nullptr && gl == 0) {
@@ -355,7 +427,10 @@ VL_D void trsv_row1(int64_t p, int64_t pend_, const int32_t* __restrict__ order,
   const int32_t so = (p < pend_) ? order[p] : -1;
   const bool valid = so >= 0;
   const int64_t s = valid ? so : 0;
-  double xs = valid ? body.rhs(s, 0, acc0) : 0.0;
+  constexpr bool PS = PsumOf<Body>::value;
+  double xs = 0.0, rh = 0.0;  // rhs taken after the first gathers are issued
+  double ps = 0.0;
+  int plast = -1;  // first entry of the row's last batch (still in registers at the end)
   const int cs = valid ? deps.count(s) : 0;
   const int64_t b0 = valid ? deps.base(s) : 0;
 #ifdef VL_TS_EXT
@@ -380,6 +455,7 @@ VL_D void trsv_row1(int64_t p, int64_t pend_, const int32_t* __restrict__ order,
     if (q < cs) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
     else v[q] = 0.0;
   }
+  if (valid) xs = rh = body.rhs(s, 0, acc0);
   bool done = !valid;
   unsigned ns = 8;
   int pq = -1;
@@ -400,10 +476,12 @@ VL_D void trsv_row1(int64_t p, int64_t pend_, const int32_t* __restrict__ order,
       if (!pend) {
 #pragma unroll
         for (int q = 0; q < B; ++q) xs -= w[q] * v[q];
+        const int eb = e0;
         e0 += B;
         if (e0 >= cs) {
-          body.out(s, 0, xs, acc0);
           __stcg(x + s, sanitize(xs));
+          body.out(s, 0, xs, acc0);
+          if constexpr (PS) plast = eb;
           if (tstamp != nullptr) {
             long long g;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
@@ -411,6 +489,11 @@ VL_D void trsv_row1(int64_t p, int64_t pend_, const int32_t* __restrict__ order,
           }
           done = true;
         } else {
+          if constexpr (PS) {
+#pragma unroll
+            for (int q = 0; q < B; ++q)
+              if (eb + q < cs) ps += (w[q] * VL_OMLOAD(body.om + j[q])) * v[q];
+          }
 #pragma unroll
           for (int q = 0; q < B; ++q) {
             const bool on = e0 + q < cs;
@@ -461,6 +544,16 @@ VL_D void trsv_row1(int64_t p, int64_t pend_, const int32_t* __restrict__ order,
 #endif
     }
   }
+  if constexpr (PS) {
+    // fused B^T(om o y) of the row: once per item, after the warp's poll loop,
+    // so the om gathers never stall lanes that are still waiting
+    if (valid && plast >= 0) {
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+        if (plast + q < cs) ps += (w[q] * VL_OMLOAD(body.om + j[q])) * v[q];
+    }
+    if (valid) body.fin_row(s, 0, xs, rh, ps);
+  }
 }
 
 // Coalesced dependency slab of the light single-RHS items (Pattern::Slabs).
@@ -483,7 +576,10 @@ VL_D void trsv_row1s(int64_t p, int64_t pend_, const int32_t* __restrict__ order
   const int32_t so = (p < pend_) ? order[p] : -1;
   const bool valid = so >= 0;
   const int64_t s = valid ? so : 0;
-  double xs = valid ? body.rhs(s, 0, acc0) : 0.0;
+  constexpr bool PS = PsumOf<Body>::value;
+  double xs = 0.0, rh = 0.0;  // rhs taken after the first gathers are issued
+  double ps = 0.0;
+  int plast = -1;  // first entry of the row's last batch (still in registers at the end)
 #ifdef VL_TS_EXT
   long long rounds = 0;
   if (tstamp != nullptr && valid) {
@@ -508,6 +604,7 @@ VL_D void trsv_row1s(int64_t p, int64_t pend_, const int32_t* __restrict__ order
     if (j[q] >= 0) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
     else v[q] = 0.0;
   }
+  if (valid) xs = rh = body.rhs(s, 0, acc0);
   bool done = !valid;
   unsigned ns = 8;
   for (;;) {
@@ -527,10 +624,12 @@ VL_D void trsv_row1s(int64_t p, int64_t pend_, const int32_t* __restrict__ order
       if (!pend) {
 #pragma unroll
         for (int q = 0; q < B; ++q) xs -= w[q] * v[q];
+        const int eb = e0;
         e0 += B;
         if (e0 >= wk) {
-          body.out(s, 0, xs, acc0);
           __stcg(x + s, sanitize(xs));
+          body.out(s, 0, xs, acc0);
+          if constexpr (PS) plast = eb;
           if (tstamp != nullptr) {
             long long g;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
@@ -538,6 +637,11 @@ VL_D void trsv_row1s(int64_t p, int64_t pend_, const int32_t* __restrict__ order
           }
           done = true;
         } else {
+          if constexpr (PS) {
+#pragma unroll
+            for (int q = 0; q < B; ++q)
+              if (j[q] >= 0) ps += (w[q] * VL_OMLOAD(body.om + j[q])) * v[q];
+          }
 #pragma unroll
           for (int q = 0; q < B; ++q) {
             const bool on = e0 + q < wk;
@@ -563,6 +667,16 @@ VL_D void trsv_row1s(int64_t p, int64_t pend_, const int32_t* __restrict__ order
         if (is_sentinel(v[q])) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
     }
   }
+  if constexpr (PS) {
+    // fused B^T(om o y) of the row: once per item, after the warp's poll loop,
+    // so the om gathers never stall lanes that are still waiting
+    if (valid && plast >= 0) {
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+        if (j[q] >= 0) ps += (w[q] * VL_OMLOAD(body.om + j[q])) * v[q];
+    }
+    if (valid) body.fin_row(s, 0, xs, rh, ps);
+  }
 }
 
 struct TrsvLaunch {
@@ -573,8 +687,15 @@ struct TrsvLaunch {
 };
 
 // Thick segment: grid-wide sync-free over positions [p0, p1).
+#ifndef VL_PS_MINB
+#define VL_PS_MINB 4
+#endif
+template <int U, class Body>
+constexpr int trsv_min_blocks() {
+  return U == 2 ? (PsumOf<Body>::value ? VL_PS_MINB : 4) : 1;
+}
 template <int G, int NU, int U, int NR, class Deps, class Body, class Fin>
-__global__ void __launch_bounds__(kRowsThreads) trsv_kernel(TrsvLaunch L, int t, int ld,
+__global__ void __launch_bounds__(kRowsThreads, (trsv_min_blocks<U, Body>())) trsv_kernel(TrsvLaunch L, int t, int ld,
                                                             const int32_t* __restrict__ order, Deps deps,
                                                             double* __restrict__ x, Body body, Fin fin,
                                                             double* __restrict__ partials,
@@ -673,10 +794,11 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
     const int64_t s = so;
     const int cs = deps.count(s);
     const int64_t b0 = deps.base(s);
-    double part = 0.0;
+    constexpr bool PS = PsumOf<Body>::value;
+    double part = 0.0, part2 = 0.0, rv = 0.0;
     for (int e0 = 0; e0 < cs; e0 += 32 * HB) {
       int32_t j[HB];
-      double w[HB], v[HB];
+      double w[HB], v[HB], o[HB];
 #pragma unroll
       for (int q = 0; q < HB; ++q) {
         const int e = e0 + q * 32 + lane;
@@ -685,7 +807,9 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
         w[q] = on ? deps.w(b0 + e) : 0.0;
         if (on) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
         else v[q] = 0.0;
+        if constexpr (PS) o[q] = on ? w[q] * VL_OMLOAD(body.om + j[q]) : 0.0;
       }
+      if (e0 == 0 && lane == 0) rv = body.rhs(s, 0, acc[0][0]);
       unsigned ns = 8;
       for (;;) {
         bool pend = false;
@@ -701,14 +825,23 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
           if (is_sentinel(v[q])) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
       }
 #pragma unroll
-      for (int q = 0; q < HB; ++q) part += w[q] * v[q];
+      for (int q = 0; q < HB; ++q) {
+        part += w[q] * v[q];
+        if constexpr (PS) part2 += o[q] * v[q];
+      }
     }
+    if (cs == 0 && lane == 0) rv = body.rhs(s, 0, acc[0][0]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if constexpr (PS) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part2 += __shfl_xor_sync(0xffffffffu, part2, o);
+    }
     if (lane == 0) {
-      const double xs = body.rhs(s, 0, acc[0][0]) - part;
-      body.out(s, 0, xs, acc[0][0]);
+      const double xs = rv - part;
       __stcg(x + s, sanitize(xs));
+      body.out(s, 0, xs, acc[0][0]);
+      if constexpr (PS) body.fin_row(s, 0, xs, rv, part2);
       if (tstamp != nullptr) {
         long long g;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
