@@ -70,8 +70,9 @@ struct Ctx {
   bool use_head = true;
   // sandwich-PCG product mode (pcg.cu) for t == 1 / t > 1:
   //   0: B h + B^T tmp passes, 1: B^T(om o y) fused into the backward solve,
-  //   2: B^T(om o y) as a side-stream pass concurrent with the forward solve
-  int pmode1 = 0;
+  //   2: B^T(om o y) as a side-stream pass concurrent with the forward solve,
+  //   3: (t == 1) mode 0 with D^-1 B h carried by recurrence (no B h pass)
+  int pmode1 = 3;
   int pmodeT = 1;
   cudaStream_t side = nullptr;  // created on first use
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;

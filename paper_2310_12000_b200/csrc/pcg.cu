@@ -15,6 +15,7 @@
 //        mode 1: p = B^T(om o y) from the same gathers (PsumOf), r stored
 //   Fwd  z = B^-1 (y / d);  (r - alpha (W h + q)).z -> beta
 //        mode 2: p = B^T(om o y) on a side stream, concurrent with Fwd
+// Mode 3 (single RHS): mode 0 with D^-1 B h carried by recurrence (no K1).
 // Mode 0 (and the diagonal preconditioners):
 //   K1  tmp = D^-1 (B h);  K2  v = W h + B^T tmp, h.v -> alpha
 //   K3  ||r - alpha v||;   K4  z = (r - alpha v)/d, r.z -> beta
@@ -194,6 +195,31 @@ struct DeferBody {
       }
       store_row<G, NU, U>(h, ld, s, gl, t, hs);
     }
+  }
+};
+// ---- sandwich form, product mode 3 (single RHS): B h by recurrence ----------
+// D^-1 B h_l = om o y_l + beta D^-1 B h_{l-1}  (B z_l = y_l / d exactly), so
+// the K1 pass becomes part of the deferred elementwise update.
+struct DeferGBody {
+  const double* z;
+  const double* y;
+  const double* om;
+  double* h;
+  double* gt;
+  double* r;
+  double* u;
+  const double* v;
+  const double* alpha;
+  const double* beta;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int, int, double (&)[NR][NU * U]) const {
+    if (!valid) return;
+    const double al = alpha[0], be = beta[0];
+    const double hs = h[s];
+    r[s] = fma(-al, v[s], r[s]);
+    u[s] = fma(al, hs, u[s]);
+    h[s] = z[s] + be * hs;
+    gt[s] = om[s] * y[s] + be * gt[s];
   }
 };
 // ---- sandwich form, product mode 0: B h and B^T tmp passes ----------------
@@ -425,9 +451,9 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
   double* hb[1] = {h0.as<double>()};
 
   const bool diagp = S.pkind == 1;  // diagonal preconditioner: product form, elementwise P^-1
-  const int pmode = diagp ? -1 : (t == 1 ? C.pmode1 : C.pmodeT);
+  const int pmode = diagp ? -1 : (t == 1 ? C.pmode1 : C.pmodeT);  // 3: single RHS only
   DevBuf om, val2;
-  if (pmode >= 1) {
+  if (pmode >= 1) {  // om = D^-1 / d
     const int g = std::max(1, std::min(4 * C.num_sms, (int)((n + 255) / 256)));
     om.alloc(sizeof(double) * (size_t)n);
     omega_kernel<<<g, 256, 0, C.stream>>>(n, S.Dinv, S.dinv, om.as<double>());
@@ -481,7 +507,8 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
     auto fwd_dot1 = [&]() { return RhsScaleDot<false>{Y, S.dinv, R, nullptr, nullptr, ld}; };
     if (diagp) {
       launch_rows<G, NU, U, 1, 0>(C, n, t, DiagInitBody{R, S.dinv, Z, ld}, RzInitFin{K}, gate);
-    } else if (pmode == 0) {
+    } else if (pmode == 0 || pmode == 3) {
+      if (pmode == 3) VL_CUDA(cudaMemsetAsync(Pp, 0, vb, C.stream));  // D^-1 B h_{-1} = 0
       launch_trsv<G, NU, U, 0>(C, F, false, t, ld, dbw, Y, RhsPlainActive{R, ld}, Fin0<0>{}, gate);
       launch_trsv<G, NU, U, 1>(C, F, true, t, ld, dfw, Z, RhsScaleDot<false>{Y, S.dinv, R, nullptr, nullptr, ld},
                                RzInitFin{K}, gate);
@@ -507,7 +534,7 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
     while (l < max_iter) {
       const int lim = std::min(max_iter, l + chunk);
       for (; l < lim; ++l) {
-        if (pmode >= 1) {
+        if (pmode == 1 || pmode == 2) {
           {
             ProfScope ps(C, tg_h, (pmode == 1 ? 8.0 : 10.0) * vbytes + 8.0 * n);
             if (pmode == 1)
@@ -543,6 +570,29 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
           continue;
         }
         double* hn = Hh;
+        if constexpr (DEFER) {
+          if (pmode == 3) {
+            {
+              ProfScope ps(C, tg_h, 8.0 * 12 * n);
+              launch_rows<1, 1, 1, 0, 0>(C, n, 1, DeferGBody{Z, Y, Om, hn, Pp, R, u, Q, K.alpha, K.beta},
+                                         Fin0<0>{}, gate);
+            }
+            {
+              ProfScope ps(C, tg_bt, bapply_bytes(P, t, 1));
+              launch_rows<G, NU, U, 1, 0>(C, n, t, K2Body{B, hn, Pp, Q, S.W, ld}, K2Fin{K, l, cap}, gate);
+            }
+            {
+              ProfScope ps(C, tg_bw, bapply_bytes(P, t, 0));
+              launch_trsv<G, NU, U, 1>(C, F, false, t, ld, dbw, Y, K3Rhs{R, Q, K.alpha, ld}, K3Fin{K, l}, gate);
+            }
+            {
+              ProfScope ps(C, tg_fw, bapply_bytes(P, t, 1));
+              launch_trsv<G, NU, U, 1>(C, F, true, t, ld, dfw, Z, RhsScaleDot<DEFER>{Y, S.dinv, R, Q, K.alpha, ld},
+                                       K4Fin{K, l, cap}, gate);
+            }
+            continue;
+          }
+        }
         {
           ProfScope ps(C, tg_h, 24.0 * n * t);
           if (DEFER || diagp)
@@ -586,7 +636,7 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
       chunk = std::min(chunk * 2, 16);
     }
     // flush the last deferred update (alpha = 0 when nothing is pending)
-    if (pmode >= 1)
+    if (pmode == 1 || pmode == 2)
       launch_rows<G, NU, U, 0, 0>(C, n, t, UFlushBody{Hh, u, K.alpha, ld}, Fin0<0>{});
     else if (DEFER || diagp)
       launch_rows<G, NU, U, 0, 0>(C, n, t, DeferBody<false>{nullptr, Hh, R, u, Q, K.alpha, nullptr, ld}, Fin0<0>{});
