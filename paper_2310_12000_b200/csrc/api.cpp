@@ -188,13 +188,24 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
     }
     return it;
   };
-  auto slabs = [&](const std::vector<int32_t>& order, const std::vector<uint32_t>& its, bool fwd_dir,
+  // Heavy items carry their row, dependency base and count in the item
+  // descriptor (items = row | bit, off = ELL / CSR base, w = count), so the
+  // solve issues their coalesced dependency loads without the order -> row
+  // pointer chain.
+  auto slabs = [&](const std::vector<int32_t>& order, std::vector<uint32_t>& its, bool fwd_dir,
                    Pattern::Slabs& S) {
     std::vector<uint32_t> off(std::max<size_t>(its.size(), 1), 0), w(std::max<size_t>(its.size(), 1), 0);
     int64_t tot = 0;
     auto deg = [&](int32_t s) { return fwd_dir ? cnt[s] : (tptr[s + 1] - tptr[s]); };
     for (size_t k = 0; k < its.size(); ++k) {
-      if (its[k] & 0x80000000u) continue;
+      if (its[k] & 0x80000000u) {
+        const int32_t s = order[its[k] & 0x7fffffffu];
+        const int64_t base = fwd_dir ? (int64_t)s * P.m : (int64_t)tptr[s];
+        if (base > (int64_t)UINT32_MAX) fail(kECapacity, "dependency base exceeds 32 bits");
+        off[k] = (uint32_t)base;
+        w[k] = (uint32_t)deg(s);
+        continue;
+      }
       const int32_t c = (int32_t)its[k];
       int wk = 0;
       for (int32_t p = c; p < c + 32; ++p)
@@ -226,6 +237,8 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
       }
     }
     S.nent = tot * 32;
+    for (auto& it : its)
+      if (it & 0x80000000u) it = (uint32_t)order[it & 0x7fffffffu] | 0x80000000u;
     upload(C, S.off, off);
     upload(C, S.w, w);
     upload(C, S.idx, idx);
@@ -235,8 +248,6 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
   auto bi = items(bwd, P.bwd_level_ptr, false);
   P.fwd_nitems = (int64_t)fi.size();
   P.bwd_nitems = (int64_t)bi.size();
-  upload(C, P.fwd_items, fi);
-  upload(C, P.bwd_items, bi);
   // dense head block + backward schedule without it
   upload(C, P.head_rows, P.head_rows_h);
   upload(C, P.head_pos, P.head_pos_h);
@@ -250,10 +261,12 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
       if ((int64_t)(it & 0x7fffffffu) < P.fwd_level_ptr[P.head_L]) ++P.fwd_items_head_end;
   auto bni = items(P.bwdnh_order_h, P.bwdnh_level_ptr, false);
   P.bwdnh_nitems = (int64_t)bni.size();
-  upload(C, P.bwdnh_items, bni);
   slabs(fwd, fi, true, P.fwd_sl);
   slabs(bwd, bi, false, P.bwd_sl);
   slabs(P.bwdnh_order_h, bni, false, P.bwdnh_sl);
+  upload(C, P.fwd_items, fi);
+  upload(C, P.bwd_items, bi);
+  upload(C, P.bwdnh_items, bni);
   VL_CUDA(cudaStreamSynchronize(C.stream));
 }
 

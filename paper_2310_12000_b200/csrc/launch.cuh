@@ -112,9 +112,9 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
   int64_t nitems, npos;
   Slab sl{nullptr, nullptr, nullptr, nullptr};
   auto pick = [&](const Pattern::Slabs& S, const DevBuf& sv, int64_t skip) {
-    if (!C.use_slabs || S.nent == 0 || sv.p == nullptr) return;
-    sl.off = S.off.as<uint32_t>() + skip;
+    sl.off = S.off.as<uint32_t>() + skip;  // also the heavy items' descriptors
     sl.w = S.w.as<uint32_t>() + skip;
+    if (!C.use_slabs || S.nent == 0 || sv.p == nullptr) return;
     sl.idx = S.idx.as<int32_t>();
     sl.val = sv.as<double>();
   };

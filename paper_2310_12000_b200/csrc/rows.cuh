@@ -246,6 +246,8 @@ struct DepsEll {
   VL_D int64_t base(int64_t s) const { return s * m; }
   VL_D int32_t idx(int64_t b) const { return nbr[b]; }
   VL_D double w(int64_t b) const { return val[b]; }
+  VL_D const void* iaddr(int64_t b) const { return nbr + b; }
+  VL_D const void* vaddr(int64_t b) const { return val + b; }
 };
 struct DepsCsr {
   const int32_t* ptr;
@@ -255,6 +257,8 @@ struct DepsCsr {
   VL_D int64_t base(int64_t s) const { return ptr[s]; }
   VL_D int32_t idx(int64_t b) const { return ind[b]; }
   VL_D double w(int64_t b) const { return val[b]; }
+  VL_D const void* iaddr(int64_t b) const { return ind + b; }
+  VL_D const void* vaddr(int64_t b) const { return val + b; }
 };
 // children CSR + per-entry folded weights val2[e] = val[e] * om[ind[e]] of a
 // fused backward product (streamed with the values instead of gathered)
@@ -268,6 +272,8 @@ struct DepsCsrW2 {
   VL_D int32_t idx(int64_t b) const { return ind[b]; }
   VL_D double w(int64_t b) const { return val[b]; }
   VL_D double w2(int64_t b) const { return val2[b]; }
+  VL_D const void* iaddr(int64_t b) const { return ind + b; }
+  VL_D const void* vaddr(int64_t b) const { return val + b; }
 };
 template <class T, class = void>
 struct HasW2 : std::false_type {};
@@ -733,6 +739,9 @@ constexpr uint32_t kHeavyBit = 0x80000000u;
 #ifndef VL_PREFETCH
 #define VL_PREFETCH 1
 #endif
+#ifndef VL_HPREFETCH
+#define VL_HPREFETCH 0
+#endif
 
 template <int NR, class Deps, class Body, class Fin>
 __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int64_t npos,
@@ -758,11 +767,13 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
   // item i + 2W are in flight and the structure of item i + W (its order
   // entries and slab lines) is prefetched into L2, so a warp reaching its next
   // item finds the dependent-load chain mostly in L2 instead of HBM.
+  // light item: d = first position, (o, w) = slab columns; heavy item:
+  // d = row | kHeavyBit, o = base of its dependencies, w = their count
   auto desc = [&](int64_t i, uint32_t& d, uint32_t& o, uint32_t& w) {
     if (i < nitems) {
       d = __ldg(items + i);
-      o = sl.idx ? __ldg(sl.off + i) : 0u;
-      w = sl.idx ? __ldg(sl.w + i) : 0u;
+      o = __ldg(sl.off + i);
+      w = __ldg(sl.w + i);
     } else {
       d = kHeavyBit; o = 0u; w = 0u;
     }
@@ -773,6 +784,13 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
   for (int64_t it = gwarp; it < nitems; it += nwarps) {
     const uint32_t item = c_d;
     const uint32_t off = c_o, wk = c_w;
+    if (VL_HPREFETCH && it + nwarps < nitems && (n_d & kHeavyBit)) {
+      // next heavy item: its first round of dependency indices / values
+      const int64_t nb = n_o;
+      const int ne = (int)min(n_w, (uint32_t)(32 * HB));
+      if (lane * 32 < ne) asm volatile("prefetch.global.L2 [%0];" ::"l"(deps.iaddr(nb + lane * 32)));
+      if (lane * 16 < ne) asm volatile("prefetch.global.L2 [%0];" ::"l"(deps.vaddr(nb + lane * 16)));
+    }
     if (VL_PREFETCH && sl.idx != nullptr && it + nwarps < nitems && !(n_d & kHeavyBit)) {
       asm volatile("prefetch.global.L2 [%0];" ::"l"(order + n_d + lane));
       for (uint32_t l = lane; l < 3 * n_w; l += 32) {
@@ -790,10 +808,9 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
         trsv_row1((int64_t)item + lane, npos, order, deps, x, body, smax, tstamp, acc[0][0]);
       continue;
     }
-    const int32_t so = order[item & ~kHeavyBit];
-    const int64_t s = so;
-    const int cs = deps.count(s);
-    const int64_t b0 = deps.base(s);
+    const int64_t s = (int64_t)(item & ~kHeavyBit);
+    const int cs = (int)wk;
+    const int64_t b0 = (int64_t)off;
     constexpr bool PS = PsumOf<Body>::value;
     double part = 0.0, part2 = 0.0, rv = 0.0;
     for (int e0 = 0; e0 < cs; e0 += 32 * HB) {
