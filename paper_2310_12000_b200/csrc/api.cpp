@@ -299,6 +299,7 @@ int vl_ctx_create(int device, void* stream, vl_ctx** out) {
     if (const char* e = std::getenv("VL_MIN_THICK")) C.min_thick_levels = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("VL_USE_HEAD")) C.use_head = std::atoi(e) != 0;
     if (const char* e = std::getenv("VL_USE_SLABS")) C.use_slabs = std::atoi(e) != 0;
+    if (const char* e = std::getenv("VL_USE_LOCAL")) C.use_local = std::atoi(e) != 0;
     if (const char* e = std::getenv("VL_PMODE1")) C.pmode1 = std::max(0, std::min(3, std::atoi(e)));
     if (const char* e = std::getenv("VL_PMODET")) C.pmodeT = std::max(0, std::min(1, std::atoi(e)));
     try {

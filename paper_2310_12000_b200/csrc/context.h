@@ -67,6 +67,7 @@ struct Ctx {
   int min_thick_levels = 4;
   // dense head block of the solves (see head.cuh) and its scratch
   bool use_slabs = true;  // coalesced dependency slabs for the single-RHS solves
+  bool use_local = true;  // SM-local sweeps for multi-column gather passes (rows_local_kernel)
   bool use_head = true;
   // sandwich-PCG product mode (pcg.cu) for t == 1 / t > 1:
   //   0: B h + B^T tmp passes, 1: B^T(om o y) fused into the backward solve,

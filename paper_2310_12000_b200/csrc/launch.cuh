@@ -67,7 +67,8 @@ inline double bapply_bytes(const Pattern& P, int t, int diag_vectors) {
 }
 
 template <int G, int NU, int U, int NR, int MAXMASK, class Body, class Fin>
-void launch_rows(Ctx& C, int64_t n, int t, const Body& body, const Fin& fin, const int* gate = nullptr) {
+void launch_rows(Ctx& C, int64_t n, int t, const Body& body, const Fin& fin, const int* gate = nullptr,
+                 const int32_t* wptr = nullptr) {
   auto kern = rows_kernel<G, NU, U, NR, MAXMASK, Body, Fin>;
   const size_t smem = red_smem_bytes<G, NU, U, NR>(kRowsThreads, t);
   int64_t need = (n * G + kRowsThreads - 1) / kRowsThreads;
@@ -75,7 +76,35 @@ void launch_rows(Ctx& C, int64_t n, int t, const Body& body, const Fin& fin, con
   int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
   C.prof.launches++;
   cudaEvent_t ev = (C.prof.on && C.prof.tag) ? prof_begin(C) : nullptr;
-  kern<<<blocks, kRowsThreads, smem, C.stream>>>(n, t, body, fin, C.red_partial.as<double>(), next_counter(C), gate);
+  kern<<<blocks, kRowsThreads, smem, C.stream>>>(n, t, body, fin, C.red_partial.as<double>(), next_counter(C), gate,
+                                                 wptr);
+  VL_LAUNCH_CHECK();
+  if (ev) prof_end(C, ev);
+}
+
+// SM-local sweep (rows_local_kernel) for gather bodies over a spatially
+// ordered pattern; falls back to launch_rows when it does not apply.
+template <int G, int NU, int U, int NR, int MAXMASK, class Body, class Fin>
+void launch_rows_local(Ctx& C, const Pattern& P, int64_t n, int t, const Body& body, const Fin& fin,
+                       const int* gate = nullptr, const int32_t* wptr = nullptr) {
+  // wptr (B^T products): work-balanced runs in either kernel
+  if (!(C.use_local && P.order_kind != 0 && (G > 1 || U > 1) && n >= (int64_t)C.num_sms * 64)) {
+    launch_rows<G, NU, U, NR, MAXMASK>(C, n, t, body, fin, gate, wptr);
+    return;
+  }
+  auto kern = rows_local_kernel<G, NU, U, NR, MAXMASK, Body, Fin>;
+  const size_t smem = red_smem_bytes<G, NU, U, NR>(kLocalThreads, t);
+  static bool carve = false;  // prefer L1 over shared memory (per instantiation)
+  if (!carve) {
+    VL_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    if (smem > 48 * 1024)
+      VL_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    carve = true;
+  }
+  C.prof.launches++;
+  cudaEvent_t ev = (C.prof.on && C.prof.tag) ? prof_begin(C) : nullptr;
+  kern<<<C.num_sms, kLocalThreads, smem, C.stream>>>(n, t, body, fin, C.red_partial.as<double>(), next_counter(C),
+                                                     gate, wptr);
   VL_LAUNCH_CHECK();
   if (ev) prof_end(C, ev);
 }

@@ -126,9 +126,11 @@ void op_spmm(Ctx& C, const Factor& F, int op, int t, int ld, const double* x, do
   BView B = bview(F, false);
   dispatch_cols(t, ld, [&](auto g, auto nu, auto u) {
     constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(u)::value;
-    if (op == 0) launch_rows<G, NU, U, 0, 0>(C, P.n, t, BodyBx{B, F.val.as<double>(), x, y, ld, 1}, Fin0<0>{});
-    else if (op == 1) launch_rows<G, NU, U, 0, 0>(C, P.n, t, BodyBtx{B, x, y, ld}, Fin0<0>{});
-    else if (op == 2) launch_rows<G, NU, U, 0, 0>(C, P.n, t, BodyBx{B, F.dval.as<double>(), x, y, ld, 0}, Fin0<0>{});
+    if (op == 0) launch_rows_local<G, NU, U, 0, 0>(C, P, P.n, t, BodyBx{B, F.val.as<double>(), x, y, ld, 1}, Fin0<0>{});
+    else if (op == 1)
+      launch_rows_local<G, NU, U, 0, 0>(C, P, P.n, t, BodyBtx{B, x, y, ld}, Fin0<0>{}, nullptr, P.tptr.as<int32_t>());
+    else if (op == 2)
+      launch_rows_local<G, NU, U, 0, 0>(C, P, P.n, t, BodyBx{B, F.dval.as<double>(), x, y, ld, 0}, Fin0<0>{});
     else fail(kEConfig, "unknown product op");
   });
 }

@@ -188,11 +188,42 @@ constexpr size_t red_smem_bytes(int threads, int t) {
 // run() is called by every lane of the warp (valid == false for tail rows)
 // so bodies may use warp shuffles.
 // ---------------------------------------------------------------------------
+// Row run [r0, r1) of CTA b of `grid`: contiguous equal-row chunks (multiple
+// of GPW), or, with a weight pointer wptr (n + 1, nondecreasing; the children
+// CSR pointer of a B^T pass), equal shares of the weight wptr[s] + s so rows
+// with hundreds of children (the first points of a random order) do not pile
+// up in one CTA.
+template <int GPW>
+VL_D void row_run(int64_t n, const int32_t* __restrict__ wptr, int64_t b, int64_t grid, int64_t& r0, int64_t& r1) {
+  if (wptr != nullptr) {
+    const int64_t W = (int64_t)wptr[n] + n;
+    auto first_row = [&](int64_t target) {  // smallest s with wptr[s] + s >= target
+      int64_t lo = 0, hi = n;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)wptr[mid] + mid < target) lo = mid + 1;
+        else hi = mid;
+      }
+      return lo;
+    };
+    // run boundaries on multiples of GPW (warp-aligned rows for the t = 1 streaming gathers)
+    r0 = first_row(W * b / grid) / GPW * GPW;
+    r1 = b + 1 == grid ? n : first_row(W * (b + 1) / grid) / GPW * GPW;
+  } else {
+    int64_t chunk = (n + grid - 1) / grid;
+    chunk = (chunk + GPW - 1) / GPW * GPW;
+    r0 = b * chunk;
+    r1 = r0 + chunk < n ? r0 + chunk : n;
+    if (r0 > n) r0 = n;
+  }
+}
+
 template <int G, int NU, int U, int NR, int MAXMASK, class Body, class Fin>
 __global__ void __launch_bounds__(kRowsThreads) rows_kernel(int64_t n, int t, Body body, Fin fin,
                                                             double* __restrict__ partials,
                                                             unsigned* __restrict__ counter,
-                                                            const int* __restrict__ gate) {
+                                                            const int* __restrict__ gate,
+                                                            const int32_t* __restrict__ wptr = nullptr) {
   if (gate != nullptr && *((volatile const int*)gate) == 0) return;
   extern __shared__ double rsh[];
   constexpr int GPW = 32 / G;
@@ -204,10 +235,51 @@ __global__ void __launch_bounds__(kRowsThreads) rows_kernel(int64_t n, int t, Bo
   // (a spatial patch in Hilbert order), so neighbour rows gathered by
   // adjacent rows are reused from L1 instead of re-fetched from L2.
   const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-  int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
-  chunk = (chunk + GPW - 1) / GPW * GPW;
-  const int64_t r0 = (int64_t)blockIdx.x * chunk;
-  const int64_t r1 = r0 + chunk < n ? r0 + chunk : n;
+  int64_t r0, r1;
+  row_run<GPW>(n, wptr, blockIdx.x, gridDim.x, r0, r1);
+  double acc[NRR][NU * U];
+#pragma unroll
+  for (int r = 0; r < NRR; ++r)
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) acc[r][i] = 0.0;
+  for (int64_t s0 = r0 + (int64_t)wib * GPW; s0 < r1; s0 += (int64_t)wpb * GPW) {
+    const int64_t s = s0 + gi;
+    body.template run<G, NU, U, NRR>(s, s < r1, gl, t, acc);
+  }
+  if constexpr (NR > 0) {
+    block_reduce_cols<G, NU, U, NR, MAXMASK>(acc, t, partials + (size_t)blockIdx.x * NR * t, rsh);
+    grid_finalize<NR, MAXMASK>(partials, counter, t, fin, rsh);
+  }
+}
+
+// SM-local variant for gather bodies over spatially ordered rows (t > 1):
+// ONE CTA of kLocalThreads per SM sweeps one contiguous run of storage rows
+// (a spatial patch) with its warps interleaved row by row, so the whole SM
+// works on one narrow window of rows at a time and the neighbour rows its
+// gathers touch are L1 hits (the window's rows were just read or are read by
+// the neighbouring warps).  With 8 independent CTAs per SM each SM juggles 8
+// windows whose union overflows L1 (and, across the chip, L2): measured on
+// the kNN factor at t = 64, X was re-read 2x (B x) to 10x (B^T x) from HBM.
+// Used for the plain products (vl_spmm): B X at t = 16 0.30 -> 0.22 ms; the
+// reducing probe / gradient passes measured slower with it (their reduction
+// scratch at 1024 threads eats the L1 carve-out) and keep rows_kernel.
+constexpr int kLocalThreads = 1024;
+template <int G, int NU, int U, int NR, int MAXMASK, class Body, class Fin>
+__global__ void __launch_bounds__(kLocalThreads, 1) rows_local_kernel(int64_t n, int t, Body body, Fin fin,
+                                                                      double* __restrict__ partials,
+                                                                      unsigned* __restrict__ counter,
+                                                                      const int* __restrict__ gate,
+                                                                      const int32_t* __restrict__ wptr) {
+  if (gate != nullptr && *((volatile const int*)gate) == 0) return;
+  extern __shared__ double rsh[];
+  constexpr int GPW = 32 / G;
+  constexpr int NRR = NR > 0 ? NR : 1;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % G;
+  const int gi = lane / G;
+  const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  int64_t r0, r1;
+  row_run<GPW>(n, wptr, blockIdx.x, gridDim.x, r0, r1);
   double acc[NRR][NU * U];
 #pragma unroll
   for (int r = 0; r < NRR; ++r)

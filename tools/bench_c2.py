@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--precs", default="vadu,lrac")
     ap.add_argument("--oracle", default="", help="comma list of preconditioners to also run on the CPU oracle")
+    ap.add_argument("--newton-grad-tol", type=float, default=1e-6,
+                    help="BackendConfig.newton_grad_tol (DESIGN 6: the fp64 noise floor of |d1 - Q b|)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     ns = argparse.Namespace(n=a.n, seed=a.seed)
@@ -45,7 +47,7 @@ def main():
     lines = []
     for prec in a.precs.split(","):
         backend = vg.BackendConfig(preconditioner=prec, t=a.t, cg_tol=1e-3, probe_seed=a.seed + 5,
-                                   rank=a.rank if prec == "lrac" else None)
+                                   rank=a.rank if prec == "lrac" else None, newton_grad_tol=a.newton_grad_tol)
         cfg = FitConfig(m=20, ordering_seed=a.seed + 3, nu=1.5, backend=backend)
         obj = _Objective(y, X, coords, vg.get_likelihood("bernoulli-logit"), cfg)
         val, grad = obj.evaluate(theta, np.zeros(0), np.zeros(0), want_grad=True)  # warm-up
@@ -58,7 +60,7 @@ def main():
         torch.cuda.synchronize()
         s_eval = e0.elapsed_time(e1) / 1e3 / a.steps
         fct, st, pr = obj.last
-        line = {"config": "C2", "n": a.n, "m": 20, "t": a.t, "rho": a.rho, "preconditioner": prec,
+        line = {"config": "C2", "newton_grad_tol": a.newton_grad_tol, "n": a.n, "m": 20, "t": a.t, "rho": a.rho, "preconditioner": prec,
                 "rank": a.rank if prec == "lrac" else None, "s_per_eval": s_eval, "evals_per_s": 1.0 / s_eval,
                 "nll": float(val), "grad_log_theta": [float(g) for g in grad],
                 "newton_steps": int(st.newton_iters), "newton_cg": [int(c) for c in st.cg_iters],
@@ -66,7 +68,7 @@ def main():
         if prec in a.oracle.split(","):
             from oracle import vl_oracle as O
             ocfg = O.Cfg(preconditioner=prec, t=a.t, cg_tol=1e-3, probe_seed=a.seed + 5,
-                         rank=a.rank if prec == "lrac" else None)
+                         rank=a.rank if prec == "lrac" else None, newton_grad_tol=a.newton_grad_tol)
             t0 = time.perf_counter()
             oval, og, oinfo = O.evaluate(obj.xy, obj.nbr.astype(np.int64), obj.y, np.zeros(a.n), obj.X, 1.0, a.rho, 1.5,
                                      O.Lik("bernoulli-logit"), ocfg)
