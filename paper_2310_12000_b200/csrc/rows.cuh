@@ -354,6 +354,9 @@ struct HasW2<T, std::void_t<decltype(std::declval<T>().w2(0))>> : std::true_type
 
 // One solve row per group: rhs, dependency gather (optionally polling the
 // sentinel), epilogue and store.  Called by every lane of the warp.
+#ifndef VL_LANEMETA
+#define VL_LANEMETA 1
+#endif
 template <int G, int NU, int U, bool POLL, class Deps, class Body>
 VL_D void trsv_row(int64_t p, int64_t pend_, int t, int ld, const int32_t* __restrict__ order, const Deps& deps,
                    double* __restrict__ x, const Body& body, unsigned smax, long long* __restrict__ tstamp, int gl,
@@ -385,22 +388,49 @@ VL_D void trsv_row(int64_t p, int64_t pend_, int t, int ld, const int32_t* __res
   const int cs = valid ? deps.count(s) : 0;
   const int64_t b0 = valid ? deps.base(s) : 0;
   const int cmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)cs);
+  // Lane-parallel metadata (VL_LANEMETA): the G lanes of a row load G
+  // consecutive (index, weight) entries in one coalesced round and the batches
+  // take them by shuffle, so a batch's gathers do not wait behind a dependent
+  // index load (one metadata round trip per G entries instead of per batch).
+  constexpr bool LM = VL_LANEMETA && G >= BATCH && (G % BATCH) == 0;
+  int32_t jl = 0;
+  double wl = 0.0, ol = 0.0;
   for (int e0 = 0; e0 < cmax; e0 += BATCH) {
     int32_t j[BATCH];
     double w[BATCH], o[BATCH];
     double v[BATCH][NC];
+    if constexpr (LM) {
+      if (e0 % G == 0) {
+        const int e = e0 + gl;
+        const bool on = e < cs;
+        jl = on ? deps.idx(b0 + e) : 0;
+        wl = on ? deps.w(b0 + e) : 0.0;
+        if constexpr (PS) {
+          if constexpr (HasW2<Deps>::value) ol = on ? deps.w2(b0 + e) : 0.0;
+          else ol = on ? wl * VL_OMLOAD(body.om + jl) : 0.0;
+        }
+      }
 #pragma unroll
-    for (int q = 0; q < BATCH; ++q) {
-      const bool on = e0 + q < cs;
-      j[q] = on ? deps.idx(b0 + e0 + q) : 0;
-      w[q] = on ? deps.w(b0 + e0 + q) : 0.0;
-    }
-    if constexpr (PS) {
+      for (int q = 0; q < BATCH; ++q) {
+        const int src = (e0 + q) % G;
+        j[q] = __shfl_sync(0xffffffffu, jl, src, G);
+        w[q] = __shfl_sync(0xffffffffu, wl, src, G);
+        if constexpr (PS) o[q] = __shfl_sync(0xffffffffu, ol, src, G);
+      }
+    } else {
 #pragma unroll
       for (int q = 0; q < BATCH; ++q) {
         const bool on = e0 + q < cs;
-        if constexpr (HasW2<Deps>::value) o[q] = on ? deps.w2(b0 + e0 + q) : 0.0;
-        else o[q] = on ? w[q] * VL_OMLOAD(body.om + j[q]) : 0.0;
+        j[q] = on ? deps.idx(b0 + e0 + q) : 0;
+        w[q] = on ? deps.w(b0 + e0 + q) : 0.0;
+      }
+      if constexpr (PS) {
+#pragma unroll
+        for (int q = 0; q < BATCH; ++q) {
+          const bool on = e0 + q < cs;
+          if constexpr (HasW2<Deps>::value) o[q] = on ? deps.w2(b0 + e0 + q) : 0.0;
+          else o[q] = on ? w[q] * VL_OMLOAD(body.om + j[q]) : 0.0;
+        }
       }
     }
 #pragma unroll
