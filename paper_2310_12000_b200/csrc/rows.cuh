@@ -347,6 +347,13 @@ struct DepsCsrW2 {
   VL_D const void* iaddr(int64_t b) const { return ind + b; }
   VL_D const void* vaddr(int64_t b) const { return val + b; }
 };
+// Column-unit solves over the children CSR (B^T: heavy-tailed dependency
+// counts) take 8-entry gather batches at 3 CTAs/SM; over the ELL (B, <= m
+// entries) 4-entry batches at 4 CTAs/SM (measured at t = 16 / 50 / 64).
+template <class Deps>
+constexpr bool csr_deps() {
+  return !std::is_same<Deps, DepsEll>::value;
+}
 template <class T, class = void>
 struct HasW2 : std::false_type {};
 template <class T>
@@ -365,7 +372,7 @@ VL_D void trsv_row(int64_t p, int64_t pend_, int t, int ld, const int32_t* __res
 #ifndef VL_BATCH2
 #define VL_BATCH2 4
 #endif
-  constexpr int BATCH = (NC == 1) ? 32 : (NC == 2 ? VL_BATCH2 : 8);
+  constexpr int BATCH = (NC == 1) ? 32 : (NC == 2 ? (csr_deps<Deps>() ? 8 : VL_BATCH2) : 8);
   using CL = Cols<G, NU, U>;
   constexpr bool PS = PsumOf<Body>::value;
   const int32_t so = (p < pend_) ? order[p] : -1;
@@ -798,12 +805,12 @@ struct TrsvLaunch {
 #ifndef VL_PS_MINB
 #define VL_PS_MINB 4
 #endif
-template <int U, class Body>
+template <int U, class Body, class Deps>
 constexpr int trsv_min_blocks() {
-  return U == 2 ? (PsumOf<Body>::value ? VL_PS_MINB : 4) : 1;
+  return U == 2 ? (csr_deps<Deps>() ? 3 : (PsumOf<Body>::value ? VL_PS_MINB : 4)) : 1;
 }
 template <int G, int NU, int U, int NR, class Deps, class Body, class Fin>
-__global__ void __launch_bounds__(kRowsThreads, (trsv_min_blocks<U, Body>())) trsv_kernel(TrsvLaunch L, int t, int ld,
+__global__ void __launch_bounds__(kRowsThreads, (trsv_min_blocks<U, Body, Deps>())) trsv_kernel(TrsvLaunch L, int t, int ld,
                                                             const int32_t* __restrict__ order, Deps deps,
                                                             double* __restrict__ x, Body body, Fin fin,
                                                             double* __restrict__ partials,
