@@ -128,3 +128,30 @@ def test_near_duplicates_raise(vg):
     nb = vg.find_neighbors(coords, np.arange(3), 2)
     with pytest.raises(vg.FactorizationError):
         vg.build_factor(coords, vg.CovarianceSpec(1.0, 0.3, 1.5), nb)
+
+
+def _random_parents(n, m, rng):
+    """Row i: min(i, m) distinct parents uniform on [0, i) (BASELINE config 5)."""
+    nbr = np.full((n, m), -1, dtype=np.int64)
+    for i in range(1, n):
+        k = min(i, m)
+        nbr[i, :k] = rng.choice(i, size=k, replace=False)
+    return nbr.astype(np.int32)
+
+
+@pytest.mark.parametrize("t", [1, 16, 64])
+@pytest.mark.parametrize("order_kind", [0, 1])
+def test_ops_random_parents_vs_oracle(vg, t, order_kind):
+    # config-5 style pattern: the first rows have hundreds of children, so the
+    # B^T products run on work-balanced runs; order_kind 1 also takes the
+    # SM-local product sweep (n >= 64 rows per SM)
+    rng = np.random.default_rng(100 + t)
+    n, m = 30000, 20
+    xy = rng.uniform(size=(n, 2))
+    nbr = _random_parents(n, m, rng)
+    f = vg.vecchia.build_factor(xy, vg.CovarianceSpec(1.0, 0.05, 1.5), nbr, order_kind=order_kind)
+    fo = O.Factor(xy, nbr.astype(np.int64), 1.0, 0.05, 1.5, f.B, f.D)
+    X = rng.standard_normal((n, t))
+    for got, want in [(f.B_matvec(X), fo.Bmul(X)), (f.BT_matvec(X), fo.BTmul(X)),
+                      (f.solve_B(X), fo.solve_B(X)), (f.solve_B(X, True), fo.solve_B(X, True))]:
+        assert np.abs(got - want).max() <= 1e-11 * np.abs(want).max()
