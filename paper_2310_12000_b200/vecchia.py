@@ -141,6 +141,12 @@ class Pattern:
         self.max_children = int(info[6])
         self._sperm_t = None
 
+    def max_count(self):
+        """Largest neighbour count (VecchiaFactor.m), computed once per pattern."""
+        if getattr(self, "_max_count", None) is None:
+            self._max_count = int((self.nbr >= 0).sum(axis=1).max()) if self.m else 0
+        return self._max_count
+
     # factor-order numpy <-> storage-order device tensors
     def to_dev(self, v):
         """Permute to storage order into a pinned staging buffer and copy H2D
@@ -210,8 +216,8 @@ class VecchiaFactor:
         self.coords = coords
         self.spec = spec
         self._neighbors = neighbors
-        self.perm = np.asarray(perm, dtype=int)
-        self.iperm = np.argsort(self.perm)
+        self._perm = None if perm is None else np.asarray(perm, dtype=int)
+        self._iperm = None
         self.pattern = pattern
         self.h = handle
         self.m = m
@@ -225,6 +231,19 @@ class VecchiaFactor:
                 _lib.lib().vl_factor_destroy(self.h)
         except Exception:
             pass
+
+    # perm / iperm (vecchia.py:139-217 attributes), materialised on first use
+    @property
+    def perm(self):
+        if self._perm is None:
+            self._perm = np.arange(self.pattern.n)
+        return self._perm
+
+    @property
+    def iperm(self):
+        if self._iperm is None:
+            self._iperm = np.argsort(self.perm)
+        return self._iperm
 
     @property
     def ctx(self):
@@ -368,15 +387,16 @@ def build_factor(locs, spec, neighbors, perm=None, want_grad=True, order_kind=DE
     definite or D_i < 1e-10 * sigma2 (vecchia.py:220-283).
     """
     coords = _coords(locs)
-    if perm is None:
-        perm = np.arange(coords.shape[0])
-    perm = np.asarray(perm, dtype=int)
-    xy = np.ascontiguousarray(coords[perm])
+    if perm is None:  # identity order: no host copy (the fit loop's per-theta call)
+        xy = coords
+    else:
+        perm = np.asarray(perm, dtype=int)
+        xy = np.ascontiguousarray(coords[perm])
     n = xy.shape[0]
     pat = neighbors if isinstance(neighbors, Pattern) else pattern_for(xy, neighbors, order_kind)
     if pat.n != n:
         raise ConfigError("neighbor sets must have one entry per point")
-    m = int((pat.nbr >= 0).sum(axis=1).max()) if pat.m else 0
+    m = pat.max_count()
     h = C.c_void_p()
     _lib.call("vl_factor_build", pat.ctx.h, pat.h, float(spec.sigma2), float(spec.rho), float(spec.nu),
               1 if want_grad else 0, C.byref(h))
