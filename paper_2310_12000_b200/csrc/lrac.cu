@@ -93,8 +93,12 @@ __global__ void __launch_bounds__(kPcThreads) pchol_step_kernel(int64_t n, int d
                                                                PcState st, double tol, double* __restrict__ part,
                                                                unsigned* __restrict__ counter,
                                                                int32_t* __restrict__ piv_s,
-                                                               const double* __restrict__ qc) {
+                                                               const double* __restrict__ qc,
+                                                               double* __restrict__ LT) {
   // qc: dense column of the matrix at the pivot (precision accessor) or null (Matern row of Sigma)
+  // LT: column-major copy of L (k x n, column c contiguous over rows) for the
+  // thread-per-row dot products (coalesced across the warp; L itself is
+  // row-major for the Woodbury GEMMs)
   if (((volatile int*)st.i)[1] != 0) return;
   __shared__ double s_min[kPcThreads / 32], s_sum[kPcThreads / 32], s_max[kPcThreads / 32];
   __shared__ int s_arg[kPcThreads / 32];
@@ -107,42 +111,61 @@ __global__ void __launch_bounds__(kPcThreads) pchol_step_kernel(int64_t n, int d
   double wmin = 1e300, wsum = 0.0, wmax = -1.0;
   int warg = 0x7fffffff;  // factor index of the best
   int wsrow = -1;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = gw; i < n; i += nw) {
-    double* Li = L + i * k;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    // dot = L[i, :j] . L[p, :j] in column order (Lp[c] is a warp-wide broadcast)
     double dot = 0.0;
-    for (int l = lane; l < j; l += 32) dot += Li[l] * Lp[l];
+    const double* li = LT + i;
+    int c = 0;
+    for (; c + 4 <= j; c += 4) {
+      const double a0 = li[(int64_t)c * n], a1 = li[(int64_t)(c + 1) * n];
+      const double a2 = li[(int64_t)(c + 2) * n], a3 = li[(int64_t)(c + 3) * n];
+      dot = fma(a0, Lp[c], dot);
+      dot = fma(a1, Lp[c + 1], dot);
+      dot = fma(a2, Lp[c + 2], dot);
+      dot = fma(a3, Lp[c + 3], dot);
+    }
+    for (; c < j; ++c) dot = fma(li[(int64_t)c * n], Lp[c], dot);
+    double src;
+    if (qc) {
+      src = qc[i];
+    } else {
+      double r2 = 0.0;
+      for (int q = 0; q < dim; ++q) {
+        const double df = xy[i * dim + q] - xp[q];
+        r2 += df * df;
+      }
+      src = K.val(sqrt(r2));
+    }
+    double col = (src - dot) / sq;
+    double di = fmax(d[i], 0.0);  // np.clip(d, 0) of this step
+    if (i == p) col = sq;
+    L[i * k + j] = col;
+    LT[(int64_t)j * n + i] = col;
+    di = di - col * col;
+    if (i == p) di = 0.0;
+    d[i] = di;
+    wmin = fmin(wmin, di);
+    const double dc = fmax(di, 0.0);
+    wsum += dc;
+    const int fi = fidx[i];
+    if (dc > wmax || (dc == wmax && fi < warg)) {
+      wmax = dc;
+      warg = fi;
+      wsrow = (int)i;
+    }
+  }
+  // warp reduction (fixed xor tree), then lane 0 of each warp holds the warp's values
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-    if (lane == 0) {
-      double src;
-      if (qc) {
-        src = qc[i];
-      } else {
-        double r2 = 0.0;
-        for (int q = 0; q < dim; ++q) {
-          const double df = xy[i * dim + q] - xp[q];
-          r2 += df * df;
-        }
-        src = K.val(sqrt(r2));
-      }
-      double col = (src - dot) / sq;
-      double di = fmax(d[i], 0.0);  // np.clip(d, 0) of this step
-      if (i == p) col = sq;
-      Li[j] = col;
-      di = di - col * col;
-      if (i == p) di = 0.0;
-      d[i] = di;
-      wmin = fmin(wmin, di);
-      const double dc = fmax(di, 0.0);
-      wsum += dc;
-      const int fi = fidx[i];
-      if (dc > wmax || (dc == wmax && fi < warg)) {
-        wmax = dc;
-        warg = fi;
-        wsrow = (int)i;
-      }
+  for (int o = 16; o > 0; o >>= 1) {
+    wmin = fmin(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
+    wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+    const double mx = __shfl_xor_sync(0xffffffffu, wmax, o);
+    const int f = __shfl_xor_sync(0xffffffffu, warg, o);
+    const int row = __shfl_xor_sync(0xffffffffu, wsrow, o);
+    if (row >= 0 && (mx > wmax || (mx == wmax && f < warg))) {
+      wmax = mx;
+      warg = f;
+      wsrow = row;
     }
   }
   // block reduction (lane 0 of each warp holds the warp's values)
@@ -174,41 +197,86 @@ __global__ void __launch_bounds__(kPcThreads) pchol_step_kernel(int64_t n, int d
     pb[2] = bmax;
     pb[3] = (double)brow;
     __threadfence();
-    const unsigned tk = atomicAdd(counter, 1u);
-    if (tk == gridDim.x - 1) {
-      __threadfence();
-      double gmin = 1e300, gsum = 0.0, gmax = -1.0;
-      int grow = -1, gf = 0x7fffffff;
-      for (unsigned b = 0; b < gridDim.x; ++b) {
-        const double* q = part + (size_t)b * 4;
-        gmin = fmin(gmin, __ldcg(q));
-        gsum += __ldcg(q + 1);
-        const int row = (int)__ldcg(q + 3);
-        const double mx = __ldcg(q + 2);
-        if (row >= 0) {
-          const int f = fidx[row];
-          if (mx > gmax || (mx == gmax && f < gf)) {
-            gmax = mx;
-            gf = f;
-            grow = row;
-          }
-        }
+    s_arg[0] = (int)atomicAdd(counter, 1u);
+  }
+  __syncthreads();
+  if (s_arg[0] != (int)gridDim.x - 1) return;
+  // last CTA: all threads fold the per-block partials (thread-strided, then a
+  // fixed shuffle / shared-memory tree: deterministic, and ~gridDim / 256
+  // independent loads per thread instead of one thread walking gridDim
+  // dependent loads).  Ties of the maximum go to the lowest factor index.
+  __threadfence();
+  double gmin = 1e300, gsum = 0.0, gmax = -1.0;
+  int grow = -1, gf = 0x7fffffff;
+  auto better = [&](double mx, int f) { return mx > gmax || (mx == gmax && f < gf); };
+  for (unsigned bq = threadIdx.x; bq < gridDim.x; bq += blockDim.x) {
+    const double* q = part + (size_t)bq * 4;
+    gmin = fmin(gmin, __ldcg(q));
+    gsum += __ldcg(q + 1);
+    const int row = (int)__ldcg(q + 3);
+    const double mx = __ldcg(q + 2);
+    if (row >= 0) {
+      const int f = fidx[row];
+      if (better(mx, f)) {
+        gmax = mx;
+        gf = f;
+        grow = row;
       }
-      piv_s[j] = p;
-      st.i[3] = j + 1;
-      if (j + 1 < k) {
-        if (gmin < -1e-10) {
-          st.i[2] = 1;
-          st.i[1] = 1;
-        } else if (gsum <= tol || !(gmax > 0.0)) {
-          st.i[1] = 1;
-        } else {
-          st.i[0] = grow;
-          *st.dp = gmax;
-        }
-      }
-      *counter = 0u;
     }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    gmin = fmin(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
+    gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
+    const double mx = __shfl_xor_sync(0xffffffffu, gmax, o);
+    const int f = __shfl_xor_sync(0xffffffffu, gf, o);
+    const int row = __shfl_xor_sync(0xffffffffu, grow, o);
+    if (row >= 0 && better(mx, f)) {
+      gmax = mx;
+      gf = f;
+      grow = row;
+    }
+  }
+  __syncthreads();  // s_* reused below
+  if (lane == 0) {
+    s_min[wib] = gmin;
+    s_sum[wib] = gsum;
+    s_max[wib] = gmax;
+    s_arg[wib] = grow;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    gmin = 1e300;
+    gsum = 0.0;
+    gmax = -1.0;
+    grow = -1;
+    gf = 0x7fffffff;
+    for (int w = 0; w < kPcThreads / 32; ++w) {
+      gmin = fmin(gmin, s_min[w]);
+      gsum += s_sum[w];
+      if (s_arg[w] >= 0) {
+        const int f = fidx[s_arg[w]];
+        if (better(s_max[w], f)) {
+          gmax = s_max[w];
+          gf = f;
+          grow = s_arg[w];
+        }
+      }
+    }
+    piv_s[j] = p;
+    st.i[3] = j + 1;
+    if (j + 1 < k) {
+      if (gmin < -1e-10) {
+        st.i[2] = 1;
+        st.i[1] = 1;
+      } else if (gsum <= tol || !(gmax > 0.0)) {
+        st.i[1] = 1;
+      } else {
+        st.i[0] = grow;
+        *st.dp = gmax;
+      }
+    }
+    *counter = 0u;
   }
 }
 
@@ -418,7 +486,9 @@ void lrac_pchol(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol) {
   DevBuf d, st, part;
   d.alloc(sizeof(double) * n);
   st.alloc(64);
-  const int grid = std::min<int64_t>(C.num_sms * 8, (n * 32 + kPcThreads - 1) / kPcThreads);
+  const int grid = std::min<int64_t>(C.num_sms * 8, (n + kPcThreads - 1) / kPcThreads);
+  DevBuf LT;  // column-major copy of L for the step kernel's dot products
+  LT.alloc(sizeof(double) * (size_t)n * k);
   part.alloc(sizeof(double) * 4 * (size_t)grid);
   fill_kernel<<<C.num_sms * 4, 256, 0, C.stream>>>(n, F.sigma2, d.as<double>());
   int h_i[4] = {P.iperm[0], 0, 0, 0};  // first pivot: all d equal -> lowest factor index
@@ -432,7 +502,8 @@ void lrac_pchol(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol) {
   for (int j = 0; j < k; ++j) {
     pchol_step_kernel<<<grid, kPcThreads, 0, C.stream>>>(n, P.d, P.xy.as<double>(), P.fidx.as<int32_t>(), K, j, k,
                                                          LF.L.as<double>(), d.as<double>(), S, tol,
-                                                         part.as<double>(), counter, LF.piv_s.as<int32_t>(), nullptr);
+                                                         part.as<double>(), counter, LF.piv_s.as<int32_t>(), nullptr,
+                                                         LT.as<double>());
     VL_LAUNCH_CHECK();
     C.prof.launches++;
   }
@@ -1258,7 +1329,9 @@ void pchol_precision(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol)
   touched.alloc(sizeof(int32_t) * std::max<int64_t>(tmax, 1));
   nt.alloc(64);
   st.alloc(64);
-  const int grid = std::min<int64_t>(C.num_sms * 8, (n * 32 + kPcThreads - 1) / kPcThreads);
+  const int grid = std::min<int64_t>(C.num_sms * 8, (n + kPcThreads - 1) / kPcThreads);
+  DevBuf LT;  // column-major copy of L for the step kernel's dot products
+  LT.alloc(sizeof(double) * (size_t)n * k);
   part.alloc(sizeof(double) * 4 * (size_t)grid);
   BView Bv = bview(F, false);
   launch_rows<1, 1, 1, 0, 0>(C, n, 1, DiagQBody{Bv, F.D.as<double>(), d.as<double>()}, Fin0<0>{});
@@ -1284,7 +1357,7 @@ void pchol_precision(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol)
     pchol_step_kernel<<<grid, kPcThreads, 0, C.stream>>>(n, P.d, P.xy.as<double>(), P.fidx.as<int32_t>(), K, j, k,
                                                          LF.L.as<double>(), d.as<double>(), S, tol,
                                                          part.as<double>(), counter, LF.piv_s.as<int32_t>(),
-                                                         qc.as<double>());
+                                                         qc.as<double>(), LT.as<double>());
     qclear_kernel<<<1, 256, 0, C.stream>>>(qc.as<double>(), touched.as<int32_t>(), nt.as<int>());
     VL_LAUNCH_CHECK();
     C.prof.launches += 3;

@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--oracle", default="", help="comma list of preconditioners to also run on the CPU oracle")
     ap.add_argument("--newton-grad-tol", type=float, default=1e-6,
                     help="BackendConfig.newton_grad_tol (DESIGN 6: the fp64 noise floor of |d1 - Q b|)")
+    ap.add_argument("--prof", action="store_true", help="per-tag kernel times of the timed evaluations")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     ns = argparse.Namespace(n=a.n, seed=a.seed)
@@ -52,6 +53,14 @@ def main():
         obj = _Objective(y, X, coords, vg.get_likelihood("bernoulli-logit"), cfg)
         val, grad = obj.evaluate(theta, np.zeros(0), np.zeros(0), want_grad=True)  # warm-up
         torch.cuda.synchronize()
+        from paper_2310_12000_b200 import _lib
+        L = _lib.lib()
+        if a.prof:
+            L.vl_prof_enable.argtypes = [_lib.c_void_p, _lib.c_int]
+            L.vl_prof_reset.argtypes = [_lib.c_void_p]
+            L.vl_prof_report.argtypes = [_lib.c_void_p, _lib.C.c_char_p, _lib.c_int, _lib.P_int64]
+            _lib.check(L.vl_prof_reset(obj.pattern.ctx.h))
+            _lib.check(L.vl_prof_enable(obj.pattern.ctx.h, 1))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(a.steps):
@@ -59,12 +68,24 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         s_eval = e0.elapsed_time(e1) / 1e3 / a.steps
+        tags = None
+        if a.prof:
+            buf = _lib.C.create_string_buffer(1 << 16)
+            nl = _lib.C.c_int64(0)
+            _lib.check(L.vl_prof_report(obj.pattern.ctx.h, buf, 1 << 16, _lib.C.byref(nl)))
+            _lib.check(L.vl_prof_enable(obj.pattern.ctx.h, 0))
+            tags = {}
+            for ln in buf.value.decode().splitlines():
+                tg, cnt, tms, _ = ln.split("\t")
+                tags[tg] = {"launches": int(cnt) // a.steps, "ms_per_eval": round(float(tms) / a.steps, 3)}
         fct, st, pr = obj.last
         line = {"config": "C2", "newton_grad_tol": a.newton_grad_tol, "n": a.n, "m": 20, "t": a.t, "rho": a.rho, "preconditioner": prec,
                 "rank": a.rank if prec == "lrac" else None, "s_per_eval": s_eval, "evals_per_s": 1.0 / s_eval,
                 "nll": float(val), "grad_log_theta": [float(g) for g in grad],
                 "newton_steps": int(st.newton_iters), "newton_cg": [int(c) for c in st.cg_iters],
                 "probe_cg_mean": float(np.mean(pr.iters)) if pr.iters is not None else None}
+        if tags is not None:
+            line["kernels"] = tags
         if prec in a.oracle.split(","):
             from oracle import vl_oracle as O
             ocfg = O.Cfg(preconditioner=prec, t=a.t, cg_tol=1e-3, probe_seed=a.seed + 5,
