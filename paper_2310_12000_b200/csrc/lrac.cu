@@ -111,20 +111,38 @@ __global__ void __launch_bounds__(kPcThreads) pchol_step_kernel(int64_t n, int d
   double wmin = 1e300, wsum = 0.0, wmax = -1.0;
   int warg = 0x7fffffff;  // factor index of the best
   int wsrow = -1;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  // two threads per row: half-warp h (lanes 16h..16h+15) covers rows
+  // base..base+15 and columns [h*jh, min(j, (h+1)*jh)); 8 independent loads
+  // in flight per thread (coalesced 128 B per half-warp and column)
+  const int half = lane >> 4;
+  const int jh = (j + 1) >> 1;
+  const int c0 = half * jh, c1 = min(j, c0 + jh);
+  const int64_t rows_per_grid = ((int64_t)gridDim.x * blockDim.x) >> 1;
+  const int64_t r0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 16 + (lane & 15);
+  const int64_t nround = (n + rows_per_grid - 1) / rows_per_grid;
+  for (int64_t rr = 0; rr < nround; ++rr) {
+    const int64_t i = r0 + rr * rows_per_grid;
+    const bool on = i < n;
     // dot = L[i, :j] . L[p, :j] in column order (Lp[c] is a warp-wide broadcast)
-    double dot = 0.0;
-    const double* li = LT + i;
-    int c = 0;
-    for (; c + 4 <= j; c += 4) {
-      const double a0 = li[(int64_t)c * n], a1 = li[(int64_t)(c + 1) * n];
-      const double a2 = li[(int64_t)(c + 2) * n], a3 = li[(int64_t)(c + 3) * n];
-      dot = fma(a0, Lp[c], dot);
-      dot = fma(a1, Lp[c + 1], dot);
-      dot = fma(a2, Lp[c + 2], dot);
-      dot = fma(a3, Lp[c + 3], dot);
+    double da = 0.0, db = 0.0;
+    if (on) {
+      const double* li = LT + i;
+      int c = c0;
+      for (; c + 8 <= c1; c += 8) {
+        double a[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = li[(int64_t)(c + q) * n];
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+          da = fma(a[q], Lp[c + q], da);
+          db = fma(a[q + 1], Lp[c + q + 1], db);
+        }
+      }
+      for (; c < c1; ++c) da = fma(li[(int64_t)c * n], Lp[c], da);
     }
-    for (; c < j; ++c) dot = fma(li[(int64_t)c * n], Lp[c], dot);
+    double dot = da + db;
+    dot += __shfl_xor_sync(0xffffffffu, dot, 16);  // the row's other half
+    if (!on || half) continue;
     double src;
     if (qc) {
       src = qc[i];
@@ -486,7 +504,7 @@ void lrac_pchol(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol) {
   DevBuf d, st, part;
   d.alloc(sizeof(double) * n);
   st.alloc(64);
-  const int grid = std::min<int64_t>(C.num_sms * 8, (n + kPcThreads - 1) / kPcThreads);
+  const int grid = std::min<int64_t>(C.num_sms * 8, (2 * n + kPcThreads - 1) / kPcThreads);
   DevBuf LT;  // column-major copy of L for the step kernel's dot products
   LT.alloc(sizeof(double) * (size_t)n * k);
   part.alloc(sizeof(double) * 4 * (size_t)grid);
@@ -499,6 +517,7 @@ void lrac_pchol(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol) {
   const MaternK K = make_matern(F);
   unsigned* counter = next_counter(C);
   ProfScope ps(C, "lrac_pchol", 0.0);
+  cudaEvent_t pev = C.prof.on ? prof_begin(C) : nullptr;  // the k steps as one timed region
   for (int j = 0; j < k; ++j) {
     pchol_step_kernel<<<grid, kPcThreads, 0, C.stream>>>(n, P.d, P.xy.as<double>(), P.fidx.as<int32_t>(), K, j, k,
                                                          LF.L.as<double>(), d.as<double>(), S, tol,
@@ -507,6 +526,7 @@ void lrac_pchol(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol) {
     VL_LAUNCH_CHECK();
     C.prof.launches++;
   }
+  if (pev) prof_end(C, pev);
   VL_CUDA(cudaMemcpyAsync(h_i, st.p, sizeof(h_i), cudaMemcpyDeviceToHost, C.stream));
   VL_CUDA(cudaStreamSynchronize(C.stream));
   if (h_i[2]) fail(kEFactorization, "pivoted Cholesky: diagonal went negative; input not PSD");
@@ -1329,7 +1349,7 @@ void pchol_precision(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol)
   touched.alloc(sizeof(int32_t) * std::max<int64_t>(tmax, 1));
   nt.alloc(64);
   st.alloc(64);
-  const int grid = std::min<int64_t>(C.num_sms * 8, (n + kPcThreads - 1) / kPcThreads);
+  const int grid = std::min<int64_t>(C.num_sms * 8, (2 * n + kPcThreads - 1) / kPcThreads);
   DevBuf LT;  // column-major copy of L for the step kernel's dot products
   LT.alloc(sizeof(double) * (size_t)n * k);
   part.alloc(sizeof(double) * 4 * (size_t)grid);
