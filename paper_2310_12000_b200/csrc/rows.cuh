@@ -194,7 +194,8 @@ constexpr size_t red_smem_bytes(int threads, int t) {
 // with hundreds of children (the first points of a random order) do not pile
 // up in one CTA.
 template <int GPW>
-VL_D void row_run(int64_t n, const int32_t* __restrict__ wptr, int64_t b, int64_t grid, int64_t& r0, int64_t& r1) {
+VL_D void row_run(int64_t n, const int32_t* __restrict__ wptr, int64_t b, int64_t grid, int64_t& r0, int64_t& r1,
+                  int wpb = 1) {
   if (wptr != nullptr) {
     const int64_t W = (int64_t)wptr[n] + n;
     auto first_row = [&](int64_t target) {  // smallest s with wptr[s] + s >= target
@@ -210,8 +211,11 @@ VL_D void row_run(int64_t n, const int32_t* __restrict__ wptr, int64_t b, int64_
     r0 = first_row(W * b / grid) / GPW * GPW;
     r1 = b + 1 == grid ? n : first_row(W * (b + 1) / grid) / GPW * GPW;
   } else {
+    // a multiple of one row group per warp of the CTA: every warp gets the
+    // same number of groups (no idle warps at the closing block reduction)
+    const int64_t unit = (int64_t)GPW * wpb;
     int64_t chunk = (n + grid - 1) / grid;
-    chunk = (chunk + GPW - 1) / GPW * GPW;
+    chunk = (chunk + unit - 1) / unit * unit;
     r0 = b * chunk;
     r1 = r0 + chunk < n ? r0 + chunk : n;
     if (r0 > n) r0 = n;
@@ -236,7 +240,7 @@ __global__ void __launch_bounds__(kRowsThreads) rows_kernel(int64_t n, int t, Bo
   // adjacent rows are reused from L1 instead of re-fetched from L2.
   const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
   int64_t r0, r1;
-  row_run<GPW>(n, wptr, blockIdx.x, gridDim.x, r0, r1);
+  row_run<GPW>(n, wptr, blockIdx.x, gridDim.x, r0, r1, wpb);
   double acc[NRR][NU * U];
 #pragma unroll
   for (int r = 0; r < NRR; ++r)
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__(kLocalThreads, 1) rows_local_kernel(int64_t n,
   const int gi = lane / G;
   const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
   int64_t r0, r1;
-  row_run<GPW>(n, wptr, blockIdx.x, gridDim.x, r0, r1);
+  row_run<GPW>(n, wptr, blockIdx.x, gridDim.x, r0, r1, wpb);
   double acc[NRR][NU * U];
 #pragma unroll
   for (int r = 0; r < NRR; ++r)
