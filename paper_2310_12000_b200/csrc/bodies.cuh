@@ -87,6 +87,9 @@ constexpr int kStreamWin = 256;
 #ifndef VL_STREAM_ELL
 #define VL_STREAM_ELL 0
 #endif
+#ifndef VL_STREAM_PROD
+#define VL_STREAM_PROD 1
+#endif
 template <class Idx, class Wt, class Load>
 VL_D void stream_rows1(int64_t E0, int64_t E1, int64_t b, int64_t e, const Idx& idx, const Wt& wt, const Load& load,
                        double& acc) {
@@ -111,6 +114,18 @@ VL_D void stream_rows1(int64_t E0, int64_t E1, int64_t b, int64_t e, const Idx& 
       if (w0 + k * 32 + lane < E1) load(j[k], 0, &xv[k]);
       else xv[k] = 0.0;
     }
+#if VL_STREAM_PROD
+    // products formed in parallel (8 per lane), the lane's fold is one shared
+    // load + add per entry of its row (the longest row of the window sets the
+    // warp's fold time)
+#pragma unroll
+    for (int k = 0; k < K; ++k) sw[k * 32 + lane] = wv[k] * xv[k];
+    __syncwarp();
+    const int64_t lo = b > w0 ? b : w0;
+    const int64_t hi = e < w0 + kStreamWin ? e : w0 + kStreamWin;
+    for (int64_t q = lo; q < hi; ++q) acc += sw[q - w0];
+    __syncwarp();
+#else
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       sw[k * 32 + lane] = wv[k];
@@ -121,6 +136,7 @@ VL_D void stream_rows1(int64_t E0, int64_t E1, int64_t b, int64_t e, const Idx& 
     const int64_t hi = e < w0 + kStreamWin ? e : w0 + kStreamWin;
     for (int64_t q = lo; q < hi; ++q) acc = fma(sw[q - w0], sx[q - w0], acc);
     __syncwarp();
+#endif
   }
 }
 
