@@ -117,22 +117,30 @@ __global__ void __launch_bounds__(kRowsThreads) head_rhs_kernel(int H, int t, in
 }
 
 // Single column: Xh[r] = sum_q M[r][q] Y[q] with M row-major (X for the
-// forward solve, X^T for the backward one), one warp per output row, lanes
-// over q (coalesced), fixed-order shuffle reduction.  ksplit = 1.
+// forward solve, X^T for the backward one).  One CTA per output row: its 8
+// warps take 8 contiguous chunks of the row's nonzero range (lanes over q,
+// coalesced), then a fixed-order combine -- deterministic, and the longest
+// rows (~H entries) no longer set the launch time through one warp's serial
+// load chain (warp-per-row: 19 us for H = 3072).  ksplit = 1.
+constexpr int kGemvThreads = 256;
 template <bool TRANS>
-__global__ void __launch_bounds__(256) head_gemv_kernel(int H, const double* __restrict__ M,
-                                                        const double* __restrict__ Y, double* __restrict__ Xh,
-                                                        const int* __restrict__ gate) {
+__global__ void __launch_bounds__(kGemvThreads) head_gemv_kernel(int H, const double* __restrict__ M,
+                                                                 const double* __restrict__ Y,
+                                                                 double* __restrict__ Xh,
+                                                                 const int* __restrict__ gate) {
   if (gate != nullptr && *((volatile const int*)gate) == 0) return;
-  const int lane = threadIdx.x & 31;
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (r >= H) return;
+  __shared__ double sp[kGemvThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r = blockIdx.x;
   const double* row = M + (size_t)r * H;
   // X row r is nonzero for q <= r; X^T row r for q >= r
   const int q0 = TRANS ? r : 0, q1 = TRANS ? H : r + 1;
+  const int len = q1 - q0;
+  const int cw = ((len + 8 * 32 - 1) / (8 * 32)) * 32;  // chunk per warp, whole 32-entry rounds
+  const int a = q0 + w * cw, b = min(q1, a + cw);
   double acc = 0.0;
-  int q = q0 + lane;
-  for (; q + 96 < q1; q += 128) {
+  int q = a + lane;
+  for (; q + 96 < b; q += 128) {
     const double a0 = row[q], a1 = row[q + 32], a2 = row[q + 64], a3 = row[q + 96];
     const double y0 = Y[q], y1 = Y[q + 32], y2 = Y[q + 64], y3 = Y[q + 96];
     acc += a0 * y0;
@@ -140,10 +148,17 @@ __global__ void __launch_bounds__(256) head_gemv_kernel(int H, const double* __r
     acc += a2 * y2;
     acc += a3 * y3;
   }
-  for (; q < q1; q += 32) acc += row[q] * Y[q];
+  for (; q < b; q += 32) acc += row[q] * Y[q];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) Xh[r] = acc;
+  if (lane == 0) sp[w] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < kGemvThreads / 32; ++k) s += sp[k];
+    Xh[r] = s;
+  }
 }
 
 // Xh_k = partial of X Y (TRANS = false) or X^T Y (TRANS = true) over the

@@ -239,9 +239,8 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
           F.valT.as<double>(), x, Y, body, fin, partials, counter, slot_rhs, total, gate);
     VL_LAUNCH_CHECK();
     if (t == 1) {
-      const int gb = (H * 32 + 255) / 256;
-      if (fwd) head_gemv_kernel<false><<<gb, 256, 0, C.stream>>>(H, F.headXr.as<double>(), Y, Xh, gate);
-      else head_gemv_kernel<true><<<gb, 256, 0, C.stream>>>(H, F.headX.as<double>(), Y, Xh, gate);
+      if (fwd) head_gemv_kernel<false><<<H, kGemvThreads, 0, C.stream>>>(H, F.headXr.as<double>(), Y, Xh, gate);
+      else head_gemv_kernel<true><<<H, kGemvThreads, 0, C.stream>>>(H, F.headX.as<double>(), Y, Xh, gate);
     } else {
       const size_t asm_ = sizeof(double) * 32 * (size_t)t;
       const dim3 ga((H + 31) / 32, ksplit);
