@@ -52,10 +52,28 @@ __global__ void __launch_bounds__(kRowsThreads) head_rhs_kernel(int H, int t, in
     for (int64_t h = gwarp; h < H; h += nwarps) {
       const int64_t s = head_rows[h];
       const int e0 = tptr[s], e1 = tptr[s + 1];
+      // 4 entries per lane in flight; the head mask and x load both depend only
+      // on the child index (x of a head child is read but not used) -- the
+      // same per-lane entry order as a plain strided loop
       double part = 0.0;
-      for (int e = e0 + lane; e < e1; e += 32) {
-        const int32_t ch = tidx[e];
-        if (head_pos[ch] < 0) part += valT[e] * __ldcg(x + (int64_t)ch * ld);
+      for (int eb = e0 + lane; eb < e1; eb += 128) {
+        int32_t ch[4];
+        double w[4], xv[4];
+        int hp[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = eb + 32 * q;
+          ch[q] = e < e1 ? tidx[e] : 0;
+          w[q] = e < e1 ? valT[e] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          hp[q] = head_pos[ch[q]];
+          xv[q] = __ldcg(x + (int64_t)ch[q] * ld);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (eb + 32 * q < e1 && hp[q] < 0) part += w[q] * xv[q];
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
