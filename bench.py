@@ -333,7 +333,7 @@ def main():
                 "share_of_step": round(d["ms"] / ms, 4)}
 
     # ---- end-to-end through the public API with host buffers -------------------
-    e2e_steps = a.e2e_steps if a.e2e_steps is not None else max(1, min(a.steps, 3))
+    e2e_steps = a.e2e_steps if a.e2e_steps is not None else max(1, min(a.steps, 5))
     y_host = np.ascontiguousarray(obj.y)
     F_host = np.zeros(a.n)
     state0 = obj.last[1]
