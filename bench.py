@@ -49,6 +49,8 @@ def parse():
     # fp64 resolution of the Newton gradient d1 - Q b is ~eps*||Q||_inf*|b| ~ 6e-6 at
     # n=1e6, rho=0.02 (D_min ~ 3e-10): the reference default 1e-6 is unattainable there
     ap.add_argument("--newton-grad-tol", type=float, default=1e-5)
+    ap.add_argument("--ref-budget-s", type=float, default=1500.0,
+                    help="--impl reference: stop timing further evaluations past this many seconds")
     return ap.parse_args()
 
 
@@ -147,32 +149,78 @@ def measured_peak():
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline (oracle port of the reference path, bounded sample)
+# reference-side pieces (oracle = CPU restatement of vlgp; never the product)
 # ---------------------------------------------------------------------------
 
-def cpu_baseline(xy, nbr, B, D, W, counts, t, sample_rows=20000):
-    """Time the reference algorithm (oracle/vl_oracle.py: the same numpy /
-    SuperLU / sparsetools calls as vlgp) on a bounded sample of the workload
-    and extrapolate one evaluation: factor+gradient build on `sample_rows`
-    rows (x n/sample_rows), SuperLU setup, 3 single-RHS PCG iterations (the
-    reference solves every system and every probe one column at a time) x the
-    evaluation's CG iteration count, plus the gradient's n x t SpMM / solve
-    passes.  Returns (evals/s, details)."""
+C3_FIXTURE = os.path.join(ROOT, "tests", "golden", "c3_reference.json")
+
+
+def _sha(a):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def c3_reference(a):
+    """The reference's own result on this exact dataset (tests/golden/c3_reference.json,
+    produced by running vlgp in the build container), or None if the config differs."""
+    try:
+        ref = json.load(open(C3_FIXTURE))
+    except (OSError, ValueError):
+        return None
+    same = (ref["n"] == a.n and ref["m"] == a.m and ref["t"] == a.t and ref["rho"] == a.rho
+            and ref["seed"] == a.seed and ref["newton_grad_tol"] == a.newton_grad_tol)
+    return ref if same else None
+
+
+def parity_block(a, nll, dtheta, y, counts=None):
+    ref = c3_reference(a)
+    if ref is None:
+        return {"reference": None, "why": "no reference fixture for this config"}
+    out = {"reference": "tests/golden/c3_reference.json (vlgp run on the same seeded inputs)",
+           "y_sha256_match": _sha(np.asarray(y).astype(np.uint8)) == ref["y_sha256"],
+           "nll_rel": abs(nll - ref["nll"]) / abs(ref["nll"]),
+           "grad_rel": max(abs(g - r) / abs(r) for g, r in zip(dtheta, ref["dtheta"])),
+           "ref_nll": ref["nll"], "ref_dtheta": ref["dtheta"]}
+    if counts is not None:
+        out["newton_cg_match"] = counts.get("newton_cg_list") == ref["newton_cg"]
+        out["probe_cg_maxdiff"] = int(np.abs(np.array(counts["probe_cg_per_column"]) - np.array(ref["probe_cg"])).max())
+    return out
+
+
+def cpu_dataset(a):
+    """bench's dataset on the host with the oracle only (no GPU, no product code):
+    same coords, same Vecchia-sampled latent field recipe, same y."""
+    from oracle import vl_oracle as O
+    coords, _ = synth(a)
+    perm_s = np.random.default_rng(a.seed + 1).permutation(a.n)
+    xs = np.ascontiguousarray(coords[perm_s])
+    fs = O.vecchia_factor(xs, O.knn_previous(xs, 30, workers=-1), 1.0, a.rho, 1.5)
+    g = np.random.default_rng(a.seed + 2).standard_normal(a.n)
+    b = np.empty(a.n)
+    b[perm_s] = fs.solve_B(np.sqrt(fs.D) * g)
+    p = 1.0 / (1.0 + np.exp(-b))
+    y = (np.random.default_rng(a.seed + 4).uniform(size=a.n) < p).astype(float)
+    perm = np.random.default_rng(a.seed + 3).permutation(a.n)
+    xy = np.ascontiguousarray(coords[perm])
+    return xy, O.knn_previous(xy, a.m, workers=-1), y, perm
+
+
+def cpu_baseline(xy, nbr, W, counts, t, rho):
+    """Bounded sample (~20-40 s) of the reference algorithm on this evaluation
+    (oracle port: same numpy / SuperLU / sparsetools calls as vlgp): the FULL
+    factor + gradient build, SuperLU setup, 3 single-RHS PCG iterations at this
+    evaluation's mode W, one n x t SpMM and P-solve; scaled by THIS run's CG
+    iteration counts.  --impl reference times complete evaluations instead."""
     from threadpoolctl import threadpool_limits
     from oracle import vl_oracle as O
 
     n = xy.shape[0]
     out = {}
     with threadpool_limits(os.cpu_count()):
-        rows = np.random.default_rng(0).choice(np.arange(64, n), size=min(sample_rows, n - 64), replace=False)
-        nb_s = np.full_like(nbr, -1)
-        nb_s[rows] = nbr[rows]
         t0 = time.perf_counter()
-        f_s = O.vecchia_factor(xy, nb_s, 1.0, 0.02, 1.5)
-        O.vecchia_grads(f_s)
-        out["build_sample_s"] = time.perf_counter() - t0
-        t_build = out["build_sample_s"] * n / rows.size
-        f = O.Factor(xy, nbr, 1.0, 0.02, 1.5, B, D)
+        f = O.vecchia_factor(xy, nbr, 1.0, rho, 1.5)
+        O.vecchia_grads(f)
+        out["build_s"] = time.perf_counter() - t0
         t0 = time.perf_counter()
         _ = f.lu
         out["splu_s"] = time.perf_counter() - t0
@@ -182,7 +230,6 @@ def cpu_baseline(xy, nbr, B, D, W, counts, t, sample_rows=20000):
         t0 = time.perf_counter()
         O.pcg(op, rhs, Pv.solve, 1e-300, max_iter=3)
         out["pcg3_s"] = time.perf_counter() - t0
-        t_iter = out["pcg3_s"] / 3.0
         V = np.random.default_rng(2).standard_normal((n, t))
         t0 = time.perf_counter()
         _ = f.B @ V
@@ -191,56 +238,78 @@ def cpu_baseline(xy, nbr, B, D, W, counts, t, sample_rows=20000):
         _ = Pv.solve(V)
         out["psolve_t_s"] = time.perf_counter() - t0
     its = counts["newton_cg"] + counts["probe_cg"] + counts["tvec_cg"]
-    # gradient: mu-derivative B@V (1), per theta dA_op (5) + dP_op (7) SpMMs, psolves (1 solve pair)
-    t_grad = 25 * out["spmm_t_s"] + out["psolve_t_s"]
-    total = t_build + out["splu_s"] + its * t_iter + t_grad
+    t_iter = out["pcg3_s"] / 3.0
+    t_grad = 25 * out["spmm_t_s"] + out["psolve_t_s"]   # mu-derivative + per-theta dA / dP SpMM passes
+    total = out["build_s"] + out["splu_s"] + its * t_iter + t_grad
     out.update(cg_iterations=its, t_iter_s=t_iter, est_eval_s=total)
     return 1.0 / total, out
 
 
-# ---------------------------------------------------------------------------
-
 def reference_arm(a, rank, world):
-    """--impl reference: the reference algorithm (oracle port) on the host
-    cores, bounded sample per step, same metric/unit/config."""
+    """--impl reference: COMPLETE evaluations of the reference algorithm on the
+    host cores -- the oracle restatement of vlgp (same numpy/scipy calls),
+    factor -> Newton mode -> probes -> SLQ NLL -> STE gradient, on the same
+    seeded dataset, probe columns spread over all host cores.  No product code,
+    no GPU.  Times as many whole evaluations as --steps asks for and the
+    --ref-budget-s allows (at least one) and reports the number timed."""
     if rank != 0:
         return
-    counts_path = os.path.join(ROOT, "profiles", "bench_counts.json")
-    with open(counts_path) as fh:
-        counts = json.load(fh)
-    import paper_2310_12000_b200 as vg  # noqa: F401  (native kNN only; no GPU work)
     from oracle import vl_oracle as O
-    coords, _ = synth(a)
-    perm = np.random.default_rng(a.seed + 3).permutation(a.n)
-    xy = np.ascontiguousarray(coords[perm])
-    from paper_2310_12000_b200.vecchia import neighbor_array
-    nbr = neighbor_array(coords, perm, a.m).astype(np.int64)
+    cores = os.cpu_count()
     t0 = time.perf_counter()
-    f = O.vecchia_factor(xy, nbr, 1.0, a.rho, 1.5)
-    build_full = time.perf_counter() - t0
-    W = np.full(a.n, 0.2)
-    vals = []
-    for _ in range(a.warmup + a.steps):
-        v, det = cpu_baseline(xy, nbr, f.B, f.D, W, counts, a.t)
-        vals.append(v)
-    v = float(np.median(vals[a.warmup:])) if a.steps else float(vals[-1])
-    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "impl": "reference", "config": workload(a),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                             "sample": "oracle port of vlgp (numpy/SuperLU/sparsetools, as the reference): factor+"
-                                       "grad build on 20k rows, SuperLU setup, 3 single-RHS PCG iterations, n x t "
-                                       "SpMM + solve; extrapolated with the evaluation's CG iteration counts "
-                                       f"({counts_path})", "details": det, "full_factor_build_s": build_full},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    xy, nbr, y, perm = cpu_dataset(a)
+    setup_s = time.perf_counter() - t0
+    cfg = O.Cfg(t=a.t, cg_tol=1e-3, probe_seed=a.seed + 5, newton_grad_tol=a.newton_grad_tol, workers=cores)
+    lik = O.Lik("bernoulli-logit")
+    times, val, g, info = [], None, None, None
+    for _ in range(max(1, a.steps)):
+        t0 = time.perf_counter()
+        val, g, info = O.evaluate(xy, nbr, y[perm], np.zeros(a.n), np.zeros((a.n, 0)), 1.0, a.rho, 1.5, lik, cfg)
+        times.append(time.perf_counter() - t0)
+        if sum(times) + times[0] > a.ref_budget_s:
+            break
+    v = len(times) / sum(times)
+    st, pr = info["state"], info["probes"]
+    counts = {"newton_steps": st.newton_iters, "newton_cg": int(sum(st.cg_iters)), "newton_cg_list": list(st.cg_iters),
+              "probe_cg": int(sum(pr.iters)), "probe_cg_per_column": [int(i) for i in pr.iters],
+              "tvec_cg": int(info.get("tvec_iters", 0))}
+    sample = (f"{len(times)} complete evaluation(s) at n={a.n} (factor+dtheta build, damped Newton, probes, "
+              f"{a.t} probe CGs over {cores} forked workers, SLQ, STE gradient); oracle/vl_oracle.py restates vlgp "
+              f"with the same numpy/SuperLU/sparsetools/LAPACK calls; dataset setup {setup_s:.0f}s untimed")
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": len(times),
+            "steps_requested": a.steps, "warmup": 0, "warmup_requested": a.warmup,
+            "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference", "config": dict(workload(a), parallelism="host"),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "eval_s": times, "nll": float(val), "dtheta": [float(x) for x in g["dtheta"]], "iterations": counts,
+            "parity_vs_vlgp": parity_block(a, float(val), g["dtheta"], y, counts)}
     print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(a):
+    """--gpus N without a torchrun environment: re-launch under torch.distributed.run."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
     a = parse()
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        sys.exit(spawn_ranks(a))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
     if a.impl == "reference":
         return reference_arm(a, rank, world)
 
@@ -286,14 +355,29 @@ def main():
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = []
+
+    def on_phase(label):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        marks.append((label, ev))
+
+    obj.on_phase = on_phase
     with Clocks(local) as clk:
         e0.record()
         for _ in range(a.steps):
             val, grad = obj.evaluate(theta, beta, xi, want_grad=True)
         e1.record()
         torch.cuda.synchronize()
+    obj.on_phase = None
     barrier()
     ms = e0.elapsed_time(e1)
+    # per-phase device time (CUDA events at the API phase boundaries): the replicated part
+    # (factor, Newton mode) and the probe-sharded part (probes + NLL, gradient incl. tvec)
+    phase_ms = {}
+    for (lab, ev), (_, nxt) in zip(marks, marks[1:]):
+        if lab != "end":
+            phase_ms[lab] = phase_ms.get(lab, 0.0) + ev.elapsed_time(nxt) / a.steps
     if world > 1:
         tt = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -362,33 +446,34 @@ def main():
     # iteration counts of this evaluation (also used by the reference arm)
     fct, st, pr = obj.last
     counts = {"newton_steps": st.newton_iters, "newton_cg": int(sum(st.cg_iters)),
-              "probe_cg": int(np.sum(pr.iters)), "tvec_cg": int(np.max(pr.iters)) if pr.iters is not None else 0,
+              "newton_cg_list": [int(c) for c in st.cg_iters],
+              "probe_cg": int(np.sum(pr.iters)), "tvec_cg": int(getattr(pr, "tvec_iters", 0)),
               "probe_cg_per_column": [int(i) for i in pr.iters]}
-    # tvec iterations are not returned by the API; use the largest probe count as a proxy upper bound
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         from paper_2310_12000_b200.vecchia import Pattern  # noqa: F401
         try:
-            v_cpu, det = cpu_baseline(obj.xy, obj.nbr.astype(np.int64), fct.B, fct.D, st.W, counts, a.t)
+            v_cpu, det = cpu_baseline(obj.xy, obj.nbr.astype(np.int64), st.W, counts, a.t, a.rho)
             cpu = {"value": v_cpu, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                   "sample": "oracle port of vlgp (numpy/SuperLU/sparsetools as the reference): factor+grad build "
-                             "on 20k rows, SuperLU setup, 3 single-RHS PCG iterations, one n x t SpMM and solve; "
-                             "extrapolated with this evaluation's CG iteration counts", "details": det}
+                   "sample": "oracle port of vlgp (numpy/SuperLU/sparsetools as the reference): full factor+grad "
+                             "build, SuperLU setup, 3 single-RHS PCG iterations at this evaluation's mode W, one n x t "
+                             "SpMM and P-solve; scaled by this evaluation's CG iteration counts (complete CPU "
+                             "evaluations: --impl reference)", "details": det}
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
     if rank == 0:
-        os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-        if world == 1 and a.n == 1_000_000:
-            with open(os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out"))
-                                   else "profiles", "bench_counts.json"), "w") as fh:
-                json.dump(counts, fh)
+        dtheta = [float(gv / th) for gv, th in zip(grad, theta)]
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": dict(workload(a), parallelism=f"probe-shard x{world}"),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches.value),
                 "clocks": clk.summary(), "nll": float(val), "grad_log_theta": [float(x) for x in grad],
+                "parity": parity_block(a, float(val), dtheta, y, counts),
+                "phase_ms": {k: round(v, 3) for k, v in phase_ms.items()},
+                "phases": {"replicated": ["factor", "mode"], "probe_sharded": ["probes_nll", "gradient"],
+                           "note": "gradient includes the replicated single-RHS tvec solve"},
                 "iterations": counts, "kernels": tags}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -83,7 +83,8 @@ int vl_pattern_create(vl_ctx* ctx, int64_t n, int d, int m, const double* xy_hos
 int vl_pattern_destroy(vl_pattern* p);
 /* sperm_host: n int32, storage position -> factor index */
 int vl_pattern_perm(const vl_pattern* p, int32_t* sperm_host);
-/* info: [n, d, m, nnz_off, n_levels_fwd, n_levels_bwd, max_children, order_kind] */
+/* info (10 entries): [n, d, m, nnz_off, n_levels_fwd, n_levels_bwd, max_children, order_kind,
+ *   head_levels, head_rows] -- the last two describe the dense head block of the solves (0 = off) */
 int vl_pattern_info(const vl_pattern* p, int64_t* info);
 
 /* ---- factor (per theta) ------------------------------------------------------
@@ -233,6 +234,19 @@ int vl_lrac_grad(vl_ctx* ctx, const vl_lracw* w, int64_t t, const double* U_dev,
                  const double* d3_dev, const double* md3x_dev, double* s_dev, double* hcols_host, double* rcols_host,
                  double* dPt_host, double* xicols_host, double* xis_host, int plain);
 /* plain != 0: the eq7 plain estimator (l2; laplace.py:433-434, no control variate). */
+
+/* Probe-sharded vl_lrac_grad (multi-GPU; the LRAC mu-derivative of
+ * laplace.py:421-431 needs per-row statistics over all t_glob probes):
+ *   mode 1: rowA = [sum_c H, sum_c R] over the local t columns, plus every
+ *           per-column / scalar output of vl_lrac_grad (hcols, rcols, dPt, xicols, xis);
+ *   -- caller allreduces rowA (n x 2) --
+ *   mode 2: rowB = [sum_c (H - hbar)(R - rbar), sum_c (R - rbar)^2];
+ *   -- caller allreduces rowB --
+ *   mode 3: s from rowA, rowB and diag(L M^-1 L^T). */
+int vl_lrac_grad_split(vl_ctx* ctx, const vl_lracw* w, int mode, int64_t t, int64_t t_glob, const double* U_dev,
+                       const double* V_dev, const double* d3_dev, const double* md3x_dev, double* rowA_dev,
+                       double* rowB_dev, double* s_dev, double* hcols_host, double* rcols_host, double* dPt_host,
+                       double* xicols_host, double* xis_host, int plain);
 
 /* ---- other low-rank-plus-diagonal preconditioners ----------------------------
  * (LowRankPlusDiagonalPreconditioner, preconditioners.py:161-214, 338-387)

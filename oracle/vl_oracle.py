@@ -108,12 +108,13 @@ def _closest_earlier(dist, i, m):
     return cand[np.lexsort((cand, dist[cand]))][:k]
 
 
-def knn_previous(xy, m, brute_max=4096):
+def knn_previous(xy, m, brute_max=4096, workers=1):
     """Nearest-preceding neighbour sets on already-permuted coords.
 
     Returns an (n, m) int64 array padded with -1 (row i holds min(i, m)
     entries, nearest first).  Brute force below ``brute_max`` rows, windowed
-    kd-tree above (vecchia.py:59-98).
+    kd-tree above (vecchia.py:59-98); ``workers`` threads for the tree query
+    (cKDTree's own parallel query; the selection is identical).
     """
     xy = np.atleast_2d(np.asarray(xy, dtype=float))
     n = xy.shape[0]
@@ -131,14 +132,23 @@ def knn_previous(xy, m, brute_max=4096):
         todo = np.arange(nb, n)
         k = min(n, 2 * m + 16)
         while todo.size:
-            dd, ii = tree.query(xy[todo], k=k)
-            ok = ((ii < todo[:, None]).sum(axis=1) >= m) | (k >= n)
-            for row in np.flatnonzero(ok):
-                i = int(todo[row])
-                keep = ii[row] < i
-                c, cd = ii[row][keep], dd[row][keep]
-                sel = c[np.lexsort((c, cd))][: min(i, m)]
-                out[i, : sel.size] = sel
+            dd, ii = tree.query(xy[todo], k=k, workers=workers)
+            earlier = ii < todo[:, None]
+            ok = (earlier.sum(axis=1) >= m) | (k >= n)
+            rows = np.flatnonzero(ok)
+            if rows.size:
+                # vectorised form of the per-row lexsort((cand, dist)) over the
+                # earlier candidates: stable sort by index, then stable by distance
+                ci = np.where(earlier[rows], ii[rows], n)
+                cd = np.where(earlier[rows], dd[rows], np.inf)
+                o = np.argsort(ci, axis=1, kind="stable")
+                ci, cd = np.take_along_axis(ci, o, 1), np.take_along_axis(cd, o, 1)
+                o = np.argsort(cd, axis=1, kind="stable")
+                ci = np.take_along_axis(ci, o, 1)[:, :m]
+                take = np.minimum(todo[rows], m)
+                ci[np.arange(m)[None, :] >= take[:, None]] = -1
+                ci[ci >= n] = -1
+                out[todo[rows]] = ci
             todo = todo[~ok]
             k = min(n, 2 * k)
     return out
@@ -676,6 +686,7 @@ class Cfg:
     newton_max_iter: int = 100
     newton_grad_tol: float = 1e-6
     newton_obj_tol: float = 1e-8
+    workers: int = 1          # host processes for the independent probe solves (not a reference knob)
 
     @property
     def split(self):
@@ -855,14 +866,41 @@ def make_probes(f, st, cfg, Z=None):
     return Probes(P.sample(Gn, Gk), G=Gn, Gk=Gk), P
 
 
-def probe_solves(f, st, P, cfg, pr):
-    """laplace.py:290-309"""
+_PAR = None   # (op, Z, psolve, tol, max_iter) inherited by forked probe workers
+
+
+def _probe_column(i):
+    from threadpoolctl import threadpool_limits
+    op, Z, psolve, tol, max_iter = _PAR
+    with threadpool_limits(1):
+        res = pcg(op, Z[:, i], psolve, tol, max_iter, capture=True)
+    return i, res
+
+
+def probe_solves(f, st, P, cfg, pr, workers=None):
+    """laplace.py:290-309: one capped-tolerance PCG per probe column.  With
+    ``workers`` > 1 the (independent) columns are distributed over forked
+    processes -- the same per-column arithmetic, results placed by column."""
+    global _PAR
     if pr.solves is not None:
         return
+    workers = cfg.workers if workers is None else workers
     op = system_matvec(f, st.W, cfg.split)
     U = np.empty_like(pr.Z)
-    for i in range(pr.t):
-        res = pcg(op, pr.Z[:, i], P.solve, cfg.mode_tol, cfg.cg_max_iter, capture=True)
+    out = [None] * pr.t
+    if workers > 1 and pr.t > 1:
+        import multiprocessing as mp
+        _PAR = (op, pr.Z, P.solve, cfg.mode_tol, cfg.cg_max_iter)
+        try:
+            with mp.get_context("fork").Pool(min(workers, pr.t)) as pool:
+                for i, res in pool.imap_unordered(_probe_column, range(pr.t)):
+                    out[i] = res
+        finally:
+            _PAR = None
+    else:
+        for i in range(pr.t):
+            out[i] = pcg(op, pr.Z[:, i], P.solve, cfg.mode_tol, cfg.cg_max_iter, capture=True)
+    for i, res in enumerate(out):
         U[:, i] = res.u
         pr.tri.append((res.diag, res.off))
         pr.iters.append(res.iters)

@@ -143,6 +143,8 @@ _SIGS.update({
     "vl_lrac_probes": [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "vl_lrac_grad": [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                      c_void_p, c_void_p, c_void_p, c_int],
+    "vl_lrac_grad_split": [c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                           c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int],
     "vl_lowrank_create": [c_void_p, c_void_p, c_int, c_int, c_double, c_void_p, c_void_p, c_void_p],
     "vl_lowrank_einv": [c_void_p, c_int64, c_int, c_void_p, c_void_p, c_void_p],
     "vl_lowrank_prepare": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p],

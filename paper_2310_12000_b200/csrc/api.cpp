@@ -134,6 +134,37 @@ static int guard(F&& f) {
   }
 }
 
+// Every handle-based entry point runs on its context's device and restores
+// the caller's current device on return (contexts on several devices in one
+// process stay independent: the caching pool files blocks by current device).
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int d) {
+    int cur = 0;
+    VL_CUDA(cudaGetDevice(&cur));
+    if (cur != d) {
+      VL_CUDA(cudaSetDevice(d));
+      prev = cur;
+    }
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <class F>
+static int guard_dev(vl_ctx* h, F&& f) {
+  if (h == nullptr) {
+    g_last_error = "null context handle";
+    return kEConfig;
+  }
+  const int device = h->c.device;
+  return guard([&] {
+    DeviceScope ds(device);
+    f();
+  });
+}
+
 template <class T>
 static void upload(Ctx& C, DevBuf& dst, const std::vector<T>& src) {
   dst.alloc(sizeof(T) * std::max<size_t>(src.size(), 1));
@@ -321,7 +352,7 @@ int vl_ctx_create(int device, void* stream, vl_ctx** out) {
 }
 
 int vl_ctx_destroy(vl_ctx* h) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (!h) return;
     cudaSetDevice(h->c.device);
     if (h->c.stream) cudaStreamSynchronize(h->c.stream);
@@ -335,11 +366,11 @@ int vl_ctx_destroy(vl_ctx* h) {
 }
 
 int vl_ctx_sync(vl_ctx* h) {
-  return guard([&] { VL_CUDA(cudaStreamSynchronize(h->c.stream)); });
+  return guard_dev(h, [&] { VL_CUDA(cudaStreamSynchronize(h->c.stream)); });
 }
 
 int vl_ctx_info(vl_ctx* h, int64_t* info) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     info[0] = h->c.device;
     info[1] = h->c.num_sms;
   });
@@ -353,7 +384,7 @@ int vl_knn_previous(const double* xy, int64_t n, int d, int m, int32_t* out, int
 }
 
 int vl_knn_previous_dev(vl_ctx* h, const double* xy, int64_t n, int d, int m, int32_t* out) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (!xy || !out) fail(kEConfig, "null pointer");
     knn_previous_dev(h->c, xy, n, d, m, out);
   });
@@ -361,7 +392,7 @@ int vl_knn_previous_dev(vl_ctx* h, const double* xy, int64_t n, int d, int m, in
 
 int vl_knn_query(vl_ctx* h, const double* train, int64_t n, const double* q, int64_t nq, int d, int m, int32_t* out,
                  double* dmin) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (!train || (nq > 0 && (!q || !out || !dmin))) fail(kEConfig, "null pointer");
     knn_query_dev(h->c, train, n, q, nq, d, m, out, dmin);
   });
@@ -369,7 +400,7 @@ int vl_knn_query(vl_ctx* h, const double* train, int64_t n, const double* q, int
 
 int vl_pattern_create(vl_ctx* h, int64_t n, int d, int m, const double* xy, const int32_t* nbr, int order_kind,
                       vl_pattern** out) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (!h || !out) fail(kEConfig, "null handle");
     if (n < 1 || d < 1 || m < 0) fail(kEConfig, "invalid pattern sizes");
     if (order_kind < 0 || order_kind > 2) fail(kEConfig, "unknown storage order");
@@ -413,12 +444,14 @@ int vl_pattern_info(const vl_pattern* p, int64_t* info) {
     info[5] = P.nlev_bwd;
     info[6] = P.max_children;
     info[7] = P.order_kind;
+    info[8] = P.head_L;
+    info[9] = P.head_H;
   });
 }
 
 int vl_factor_build(vl_ctx* h, const vl_pattern* p, double sigma2, double rho, double nu, int want_grad,
                     vl_factor** out) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (!h || !p || !out) fail(kEConfig, "null handle");
     VL_CUDA(cudaSetDevice(h->c.device));
     auto* f = new vl_factor();
@@ -437,7 +470,7 @@ int vl_factor_destroy(vl_factor* f) {
 }
 
 int vl_factor_get(vl_ctx* h, const vl_factor* f, int which, double* out) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     const Factor& F = f->f;
     const Pattern& P = *F.pat;
     const DevBuf* src = nullptr;
@@ -458,7 +491,7 @@ int vl_factor_get(vl_ctx* h, const vl_factor* f, int which, double* out) {
 }
 
 int vl_factor_set(vl_ctx* h, vl_factor* f, int which, const double* in) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     Factor& F = f->f;
     const Pattern& P = *F.pat;
     DevBuf* dst = nullptr;
@@ -480,14 +513,14 @@ int vl_factor_set(vl_ctx* h, vl_factor* f, int which, const double* in) {
 }
 
 int vl_prof_enable(vl_ctx* h, int on) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     prof_collect(h->c);
     h->c.prof.on = on != 0;
   });
 }
 
 int vl_prof_reset(vl_ctx* h) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     prof_collect(h->c);
     h->c.prof.agg.clear();
     h->c.prof.launches = 0;
@@ -495,7 +528,7 @@ int vl_prof_reset(vl_ctx* h) {
 }
 
 int vl_prof_report(vl_ctx* h, char* buf, int len, int64_t* launches) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     prof_collect(h->c);
     std::string s;
     for (auto& kv : h->c.prof.agg) {
@@ -515,7 +548,7 @@ int vl_prof_report(vl_ctx* h, char* buf, int len, int64_t* launches) {
 // debug hook (not in the public header): record per-row completion times of
 // subsequent triangular solves into a device buffer of n int64 (NULL disables)
 int vl_debug_set_tstamp(vl_ctx* h, void* dev_buf) {
-  return guard([&] { h->c.debug_tstamp = (long long*)dev_buf; });
+  return guard_dev(h, [&] { h->c.debug_tstamp = (long long*)dev_buf; });
 }
 
 // ---- Laplace path -----------------------------------------------------------
@@ -523,7 +556,7 @@ int vl_debug_set_tstamp(vl_ctx* h, void* dev_buf) {
 int vl_find_mode(vl_ctx* h, const vl_factor* f, const vl_lik* lik, const vl_newton_cfg* cfg, const double* y,
                  const double* Fv, double* b, double* W, double* d1, double* d3, double* out, int32_t* cg_iters,
                  int cg_iters_cap) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (!h || !f || !lik || !cfg || !out) fail(kEConfig, "null argument");
     LikSpec L{lik->family, lik->shape};
     NewtonCfg nc{cfg->mode_cg_tol, cfg->cg_max_iter, cfg->newton_max_iter, cfg->newton_grad_tol, cfg->newton_obj_tol,
@@ -553,7 +586,7 @@ int vl_find_mode(vl_ctx* h, const vl_factor* f, const vl_lik* lik, const vl_newt
 // ---- LRAC -----------------------------------------------------------------------
 
 int vl_lrac_create(vl_ctx* h, const vl_factor* f, int k, double tol, vl_lrac** out, int32_t* piv_host, int* keff) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     auto* l = new vl_lrac();
     l->f = f;
     try {
@@ -574,7 +607,7 @@ int vl_lrac_destroy(vl_lrac* l) {
 }
 
 int vl_lrac_get_L(vl_ctx* h, const vl_lrac* l, double* host) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     const size_t cnt = (size_t)l->f->f.pat->n * l->lf.k;
     VL_CUDA(cudaMemcpyAsync(host, l->lf.L.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, h->c.stream));
     VL_CUDA(cudaStreamSynchronize(h->c.stream));
@@ -582,7 +615,7 @@ int vl_lrac_get_L(vl_ctx* h, const vl_lrac* l, double* host) {
 }
 
 int vl_lrac_prepare(vl_ctx* h, const vl_lrac* l, const double* W, vl_lracw** out, double* out2) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     const int64_t n = l->f->f.pat->n;
     if (count_nonpos(h->c, n, W) > 0)
       fail(kECapability, "lrac preconditions SigmaTilde + W^{-1} and needs W > 0 everywhere (eq7 split; log W "
@@ -608,12 +641,12 @@ int vl_lracw_destroy(vl_lracw* w) {
 }
 
 int vl_lrac_apply_inv(vl_ctx* h, const vl_lracw* w, int64_t t, const double* r, double* z) {
-  return guard([&] { lrac_apply_inv(h->c, w->p, (int)t, r, z); });
+  return guard_dev(h, [&] { lrac_apply_inv(h->c, w->p, (int)t, r, z); });
 }
 
 int vl_lrac_pcg(vl_ctx* h, const vl_lracw* w, int64_t t, const double* bm, double* u, double tol, int max_iter,
                 int capture, int32_t* iters, int32_t* conv, double* res, double* alpha, double* beta, int hist_cap) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (t < 1 || t > 128) fail(kECapacity, "right-hand sides per call must be in [1, 128]");
     PcgResult pr;
     pcg_lrac(h->c, w->p, (int)t, bm, u, tol, max_iter, capture != 0, &pr);
@@ -633,7 +666,7 @@ int vl_lrac_pcg(vl_ctx* h, const vl_lracw* w, int64_t t, const double* bm, doubl
 
 int vl_lrac_solve_system(vl_ctx* h, const vl_lracw* w, int64_t t, const double* rhs, double* u, double tol,
                          int max_iter, int32_t* iters) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     PcgResult pr;
     lrac_solve_system(h->c, w->p, (int)t, rhs, u, tol, max_iter, &pr);
     if (iters)
@@ -642,7 +675,7 @@ int vl_lrac_solve_system(vl_ctx* h, const vl_lracw* w, int64_t t, const double* 
 }
 
 int vl_apply_sigma_tilde(vl_ctx* h, const vl_factor* f, int64_t t, const double* x, double* y) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     DevBuf scr;
     scr.alloc(sizeof(double) * (size_t)f->f.pat->n * t);
     apply_sigma_tilde(h->c, f->f, (int)t, x, y, scr.as<double>());
@@ -651,18 +684,27 @@ int vl_apply_sigma_tilde(vl_ctx* h, const vl_factor* f, int64_t t, const double*
 
 int vl_lrac_probes(vl_ctx* h, const vl_lracw* w, int64_t t, const double* Gn, const double* Gk, double* Z, double* V,
                    double* w_host) {
-  return guard([&] { lrac_probes(h->c, w->p, (int)t, Gn, Gk, Z, V, w_host); });
+  return guard_dev(h, [&] { lrac_probes(h->c, w->p, (int)t, Gn, Gk, Z, V, w_host); });
 }
 
 int vl_lrac_grad(vl_ctx* h, const vl_lracw* w, int64_t t, const double* U, const double* V, const double* d3,
                  const double* md3x, double* s, double* hcols, double* rcols, double* dPt, double* xicols,
                  double* xis, int plain) {
-  return guard([&] { lrac_grad(h->c, w->p, (int)t, U, V, d3, md3x, s, hcols, rcols, dPt, xicols, xis, plain); });
+  return guard_dev(h, [&] { lrac_grad(h->c, w->p, (int)t, U, V, d3, md3x, s, hcols, rcols, dPt, xicols, xis, plain); });
+}
+
+int vl_lrac_grad_split(vl_ctx* h, const vl_lracw* w, int mode, int64_t t, int64_t t_glob, const double* U,
+                       const double* V, const double* d3, const double* md3x, double* rowA, double* rowB, double* s,
+                       double* hcols, double* rcols, double* dPt, double* xicols, double* xis, int plain) {
+  return guard_dev(h, [&] {
+    lrac_grad_split(h->c, w->p, mode, (int)t, (int)t_glob, U, V, d3, md3x, rowA, rowB, s, hcols, rcols, dPt, xicols,
+                    xis, plain);
+  });
 }
 
 int vl_lowrank_create(vl_ctx* h, const vl_factor* f, int kind, int k, double tol, vl_lrac** out, int32_t* piv_host,
                       int* keff) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     auto* l = new vl_lrac();
     l->f = f;
     try {
@@ -681,12 +723,12 @@ int vl_lowrank_create(vl_ctx* h, const vl_factor* f, int kind, int k, double tol
 }
 
 int vl_lowrank_einv(vl_ctx* h, int64_t n, int kind, const double* W, const double* diag_st, double* einv) {
-  return guard([&] { lowrank_einv(h->c, n, kind, W, diag_st, einv); });
+  return guard_dev(h, [&] { lowrank_einv(h->c, n, kind, W, diag_st, einv); });
 }
 
 int vl_lowrank_prepare(vl_ctx* h, const vl_factor* f, const vl_lrac* l, const double* Wop, const double* einv,
                        int eq6, vl_lracw** out, double* out2) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     auto* w = new vl_lracw();
     try {
       lowrank_prepare(h->c, f->f, l ? &l->lf : nullptr, Wop, einv, eq6, w->p);
@@ -703,13 +745,13 @@ int vl_lowrank_prepare(vl_ctx* h, const vl_factor* f, const vl_lrac* l, const do
 }
 
 int vl_diag_sigma_tilde(vl_ctx* h, const vl_factor* f, double* out) {
-  return guard([&] { diag_sigma_tilde(h->c, f->f, out); });
+  return guard_dev(h, [&] { diag_sigma_tilde(h->c, f->f, out); });
 }
 
 int vl_find_mode_lowrank(vl_ctx* h, const vl_factor* f, const vl_lrac* l, int wb_kind, const double* diag_st,
                          const vl_lik* lik, const vl_newton_cfg* cfg, const double* y, const double* Fv, double* b,
                          double* W, double* d1, double* d3, double* out, int32_t* cg_iters, int cg_iters_cap) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (wb_kind != 1 && wb_kind != 2) fail(kEConfig, "wb_kind must be 1 (eq6 low rank) or 2 (l2)");
     if (wb_kind == 1 && !l) fail(kEConfig, "low-rank factor required");
     LikSpec L{lik->family, lik->shape};
@@ -740,7 +782,7 @@ int vl_find_mode_lowrank(vl_ctx* h, const vl_factor* f, const vl_lrac* l, int wb
 int vl_find_mode_lrac(vl_ctx* h, const vl_factor* f, const vl_lrac* l, const vl_lik* lik, const vl_newton_cfg* cfg,
                       const double* y, const double* Fv, double* b, double* W, double* d1, double* d3, double* out,
                       int32_t* cg_iters, int cg_iters_cap) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     LikSpec L{lik->family, lik->shape};
     NewtonCfg nc{cfg->mode_cg_tol, cfg->cg_max_iter, cfg->newton_max_iter, cfg->newton_grad_tol, cfg->newton_obj_tol,
                  cfg->precond};
@@ -768,7 +810,7 @@ int vl_find_mode_lrac(vl_ctx* h, const vl_factor* f, const vl_lrac* l, const vl_
 
 int vl_probes_vadu(vl_ctx* h, const vl_factor* f, const double* W, int64_t t, const double* G, double* Z, double* V,
                    double* w_host) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (t < 1 || t > 128) fail(kECapacity, "probe count per call must be in [1, 128]");
     probes_vadu(h->c, f->f, W, (int)t, (int)t, G, Z, V, w_host);
   });
@@ -777,7 +819,7 @@ int vl_probes_vadu(vl_ctx* h, const vl_factor* f, const double* W, int64_t t, co
 int vl_pcg_vadu(vl_ctx* h, const vl_factor* f, const double* W, int64_t t, const double* bm, double* u, double tol,
                 int max_iter, int capture, int32_t* iters, int32_t* conv, double* res, double* alpha, double* beta,
                 int hist_cap) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (t < 1 || t > 128) fail(kECapacity, "right-hand sides per call must be in [1, 128]");
     const Factor& F = f->f;
     const int64_t n = F.pat->n;
@@ -804,26 +846,26 @@ int vl_pcg_vadu(vl_ctx* h, const vl_factor* f, const double* W, int64_t t, const
 }
 
 int vl_factor_sums(vl_ctx* h, const vl_factor* f, const double* W, double* out6) {
-  return guard([&] { factor_sums(h->c, f->f, W, out6); });
+  return guard_dev(h, [&] { factor_sums(h->c, f->f, W, out6); });
 }
 
 int vl_grad_probe_pass(vl_ctx* h, const vl_factor* f, const double* W, const double* d3, const double* U,
                        const double* V, int64_t t, double* s_out, double* cols4, const double* md3x, double* xicols2,
                        int plain) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (t < 1 || t > 128) fail(kECapacity, "probe count per call must be in [1, 128]");
     grad_probe_pass(h->c, f->f, W, d3, U, V, (int)t, (int)t, s_out, cols4, md3x, xicols2, plain);
   });
 }
 
 int vl_precond_dinv(vl_ctx* h, const vl_factor* f, int variant, const double* W, double* dinv) {
-  return guard([&] { precond_dinv(h->c, f->f, variant, W, dinv); });
+  return guard_dev(h, [&] { precond_dinv(h->c, f->f, variant, W, dinv); });
 }
 
 int vl_pcg_eq6(vl_ctx* h, const vl_factor* f, const double* W, const double* dinv, int pkind, int64_t t,
                const double* bm, double* u, double tol, int max_iter, int capture, int32_t* iters, int32_t* conv,
                double* res, double* alpha, double* beta, int hist_cap) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (t < 1 || t > 128) fail(kECapacity, "right-hand sides per call must be in [1, 128]");
     if (pkind != 0 && pkind != 1) fail(kEConfig, "pkind must be 0 (sandwich) or 1 (diagonal)");
     const Factor& F = f->f;
@@ -852,20 +894,20 @@ int vl_pcg_eq6(vl_ctx* h, const vl_factor* f, const double* W, const double* din
 
 int vl_probes_eq6(vl_ctx* h, const vl_factor* f, const double* dinv, int pkind, int64_t t, const double* G, double* Z,
                   double* V, double* w_host) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (t < 1 || t > 128) fail(kECapacity, "probe count per call must be in [1, 128]");
     probes_eq6(h->c, f->f, dinv, pkind, (int)t, (int)t, G, Z, V, w_host);
   });
 }
 
 int vl_sum_log(vl_ctx* h, int64_t n, const double* x, double* out) {
-  return guard([&] { *out = sum_log(h->c, n, x); });
+  return guard_dev(h, [&] { *out = sum_log(h->c, n, x); });
 }
 
 int vl_grad_probe_pass_split(vl_ctx* h, const vl_factor* f, int mode, const double* W, const double* d3,
                              const double* U, const double* V, int64_t t, int64_t t_glob, double* rowA, double* rowB,
                              double* s_out, double* cols4, const double* md3x, double* xicols2, int plain) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (mode != 3 && (t < 1 || t > 128)) fail(kECapacity, "probe shard width must be in [1, 128]");
     grad_probe_pass_split(h->c, f->f, mode, W, d3, U, V, (int)t, (int)t, (int)t_glob, rowA, rowB, s_out, cols4, md3x,
                           xicols2, plain);
@@ -873,28 +915,28 @@ int vl_grad_probe_pass_split(vl_ctx* h, const vl_factor* f, int mode, const doub
 }
 
 int vl_grad_scalar_terms(vl_ctx* h, const vl_factor* f, const double* b, const double* tvec, double* out4) {
-  return guard([&] { grad_scalar_terms(h->c, f->f, b, tvec, out4); });
+  return guard_dev(h, [&] { grad_scalar_terms(h->c, f->f, b, tvec, out4); });
 }
 
 int vl_grad_dbeta(vl_ctx* h, int64_t n, const double* d1, const double* s, const double* W, const double* tvec,
                   const double* X, int64_t p, double* dbeta) {
-  return guard([&] { grad_dF(h->c, n, d1, s, W, tvec, X, (int)p, dbeta); });
+  return guard_dev(h, [&] { grad_dF(h->c, n, d1, s, W, tvec, X, (int)p, dbeta); });
 }
 
 int vl_gamma_xi_terms(vl_ctx* h, const vl_factor* f, const double* y, const double* Fv, const double* b,
                       const double* W, const double* tvec, double* md3x, double* out3) {
-  return guard([&] { gamma_xi_terms(h->c, f->f, y, Fv, b, W, tvec, md3x, out3); });
+  return guard_dev(h, [&] { gamma_xi_terms(h->c, f->f, y, Fv, b, W, tvec, md3x, out3); });
 }
 
 int vl_spmm(vl_ctx* h, const vl_factor* f, int op, int64_t t, const double* x, double* y) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (t < 1 || t > (1 << 20)) fail(kEConfig, "invalid column count");
     op_spmm(h->c, f->f, op, (int)t, (int)t, x, y);
   });
 }
 
 int vl_sptrsv(vl_ctx* h, const vl_factor* f, int transpose, int64_t t, const double* x, double* y) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (t < 1 || t > (1 << 20)) fail(kEConfig, "invalid column count");
     op_trsv(h->c, f->f, transpose != 0, (int)t, (int)t, x, y);
   });
@@ -903,7 +945,7 @@ int vl_sptrsv(vl_ctx* h, const vl_factor* f, int transpose, int64_t t, const dou
 
 int vl_pred_create(vl_ctx* h, const vl_pattern* p, double sigma2, double rho, double nu, const double* qxy, int64_t np,
                    const int32_t* nbr, int take, vl_pred** out) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     if (!h || !p || !out || (np > 0 && (!qxy || !nbr))) fail(kEConfig, "null pointer");
     auto* b = new vl_pred();
     try {
@@ -921,7 +963,7 @@ int vl_pred_destroy(vl_pred* b) {
 }
 
 int vl_pred_get(vl_ctx* h, const vl_pred* b, int which, double* out) {
-  return guard([&] {
+  return guard_dev(h, [&] {
     const size_t cnt = which == 0 ? (size_t)b->b.np * b->b.take : (size_t)b->b.np;
     const DevBuf& src = which == 0 ? b->b.val : b->b.Dp;
     if (which != 0 && which != 1) fail(kEConfig, "unknown prediction field");
@@ -931,16 +973,16 @@ int vl_pred_get(vl_ctx* h, const vl_pred* b, int which, double* out) {
 }
 
 int vl_pred_mean(vl_ctx* h, const vl_pred* b, const double* b_dev, const double* Fp_dev, double* omega_dev) {
-  return guard([&] { pred_mean(h->c, b->b, b_dev, Fp_dev, omega_dev); });
+  return guard_dev(h, [&] { pred_mean(h->c, b->b, b_dev, Fp_dev, omega_dev); });
 }
 
 int vl_pred_z3(vl_ctx* h, const vl_factor* f, const double* W_dev, int64_t c, const double* z1, const double* z2,
                double* z3) {
-  return guard([&] { pred_z3(h->c, f->f, W_dev, (int)c, z1, z2, z3); });
+  return guard_dev(h, [&] { pred_z3(h->c, f->f, W_dev, (int)c, z1, z2, z3); });
 }
 
 int vl_pred_accum(vl_ctx* h, const vl_pred* b, const double* U_dev, int64_t c, double* acc_dev, double* cov_dev) {
-  return guard([&] { pred_accum(h->c, b->b, U_dev, (int)c, acc_dev, cov_dev); });
+  return guard_dev(h, [&] { pred_accum(h->c, b->b, U_dev, (int)c, acc_dev, cov_dev); });
 }
 
 }  // extern "C"

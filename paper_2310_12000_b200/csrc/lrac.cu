@@ -1028,23 +1028,130 @@ struct DQDotBody {
   }
 };
 
+// Probe-sharded LRAC mu-derivative (multi-GPU; the per-row control variate
+// needs all t probes), mirroring the VADU split of laplace.cu:
+//   MODE 1: rowA = [sum_c H, sum_c R] over the local columns (+ xi column sums)
+//   MODE 2: rowB = [sum_c (H - hbar)(R - rbar), sum_c (R - rbar)^2], global means rowA / tg
+template <int MODE, bool XI>
+struct LracMuSplitBody {
+  const double* U_;
+  const double* V_;
+  const double* W;
+  const double* md3x;
+  double* rowA;
+  double* rowB;
+  int tg;
+  int ld;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    constexpr int NC = NU * U;
+    double us[NC], vs[NC], H[NC], R[NC];
+    load_row<G, NU, U>(U_, ld, valid ? s : 0, gl, valid ? t : 0, us);
+    load_row<G, NU, U>(V_, ld, valid ? s : 0, gl, valid ? t : 0, vs);
+    const double w = valid ? W[s] : 1.0;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int c = vl::Cols<G, NU, U>::col(gl, i);
+      const bool on = valid && c < t;
+      H[i] = on ? us[i] * vs[i] / (w * w) : 0.0;
+      const double vw = vs[i] / w;
+      R[i] = on ? vw * vw : 0.0;
+    }
+    if constexpr (MODE == 1) {
+      double sh = 0.0, sr = 0.0;
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        sh += H[i];
+        sr += R[i];
+      }
+      sh = gsum_l<G>(sh);
+      sr = gsum_l<G>(sr);
+      if (valid && gl == 0) {
+        rowA[2 * s] = sh;
+        rowA[2 * s + 1] = sr;
+      }
+      if constexpr (XI) {
+        if (!valid) return;
+        const double q = md3x[s] / (w * w);
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+          const int c = vl::Cols<G, NU, U>::col(gl, i);
+          if (c >= t) continue;
+          acc[0][i] += -(q * us[i] * vs[i]);
+          acc[1][i] += -(q * vs[i] * vs[i]);
+        }
+      }
+    } else {
+      const double hm = valid ? rowA[2 * s] / tg : 0.0, rm = valid ? rowA[2 * s + 1] / tg : 0.0;
+      double svr = 0.0, scv = 0.0;
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        const int c = vl::Cols<G, NU, U>::col(gl, i);
+        if (valid && c < t) {
+          svr += (R[i] - rm) * (R[i] - rm);
+          scv += (H[i] - hm) * (R[i] - rm);
+        }
+      }
+      svr = gsum_l<G>(svr);
+      scv = gsum_l<G>(scv);
+      if (valid && gl == 0) {
+        rowB[2 * s] = scv;
+        rowB[2 * s + 1] = svr;
+      }
+    }
+  }
+};
+
+// MODE 3 of the split: s = 0.5 (-d3) (1/W + c (G2 - 1/W) - mean(H - c R)) from the reduced row sums
+struct LracMuFinishBody {
+  const double* rowA;
+  const double* rowB;
+  const double* G2;
+  const double* W;
+  const double* d3;
+  double* s_out;
+  int tg;
+  int plain;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int, int, double (&)[NR][NU * U]) const {
+    if (!valid) return;
+    double cw = 0.0;
+    if (tg >= 2 && !plain) {
+      const double vr = rowB[2 * s + 1] / (tg - 1), cv = rowB[2 * s] / (tg - 1);
+      cw = (vr >= 1e-300) ? cv / vr : 0.0;
+    }
+    const double w = W[s];
+    const double exact = 1.0 / w + cw * (G2[s] - 1.0 / w);
+    s_out[s] = 0.5 * ((-d3[s]) * (exact - (rowA[2 * s] - cw * rowA[2 * s + 1]) / tg));
+  }
+};
+
+// [sum G2 m3, sum m3 / W] (the xi dP_trace pieces) as a device reduction
+struct XiSumsBody {
+  const double* G2;
+  const double* m3;
+  const double* W;
+  template <int G, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int, int, double (&acc)[NR][NU * U]) const {
+    if (!valid) return;
+    acc[0][0] += G2[s] * m3[s];
+    acc[1][0] += m3[s] / W[s];
+  }
+};
+
 }  // namespace
 
 // out: s (n, device); hcols (2 x t: h_s2, h_rho), rcols (2 x t: r_s2, r_rho),
 // dPt (2); with md3x: xih (t), xir (t), xi_scalars [sum G2 m3, sum m3 / W]
-void lrac_grad(Ctx& C, const LracPrec& Pr, int t, const double* U, const double* V, const double* d3,
-               const double* md3x, double* s_out, double* hcols, double* rcols, double* dPt, double* xicols,
-               double* xis, int plain) {
-  const Factor& F = *Pr.F;
-  const Pattern& P = *F.pat;
-  const int64_t n = P.n;
+namespace {
+// G2 = diag(L M^-1 L^T) = column norms of Lm^-1 L^T (zero without a low-rank part)
+void lrac_G2(Ctx& C, const LracPrec& Pr, DevBuf& G2) {
+  const int64_t n = Pr.F->pat->n;
   const int k = Pr.LF->keff, kl = Pr.LF->k;
-  if (!F.has_grad) fail(kEConfig, "factor was built without gradient");
-  ProfScope ps(C, "lrac_grad", 0.0);
   cublasHandle_t hb = blas(C);
-  const double one = 1.0, zero = 0.0, mone = -1.0;
+  const double one = 1.0;
+  DevBuf Y;
   // G2 = diag(L M^-1 L^T) = column norms of Lm^-1 L^T
-  DevBuf Y, G2;
   Y.alloc(sizeof(double) * (size_t)n * kl);
   G2.alloc(sizeof(double) * n);
   if (k > 0) {
@@ -1056,21 +1163,20 @@ void lrac_grad(Ctx& C, const LracPrec& Pr, int t, const double* U, const double*
   } else {
     VL_CUDA(cudaMemsetAsync(G2.p, 0, sizeof(double) * n, C.stream));
   }
+}
+
+// The per-probe-column and scalar parts of the LRAC gradient (everything except
+// the mu-derivative): h (sigma2, rho) through SigmaTilde U / V and the dQ dot,
+// r = 2 (L^T v).(dL^T v), dP_trace, and the xi scalars.
+void lrac_grad_columns(Ctx& C, const LracPrec& Pr, int t, const double* U, const double* V, const double* md3x,
+                       const DevBuf& G2, double* hcols, double* rcols, double* dPt, double* xis) {
+  const Factor& F = *Pr.F;
+  const Pattern& P = *F.pat;
+  const int64_t n = P.n;
+  const int k = Pr.LF->keff, kl = Pr.LF->k;
+  cublasHandle_t hb = blas(C);
+  const double one = 1.0, zero = 0.0, mone = -1.0;
   double* sums = C.dev_scalars.as<double>();
-  dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
-    constexpr int G_ = decltype(g)::value, NU = decltype(nu)::value, U_ = decltype(uu)::value;
-    if (md3x)
-      launch_rows<G_, NU, U_, 2, 0>(C, n, t, LracMuBody<true>{U, V, Pr.Wop, G2.as<double>(), d3, md3x, s_out, t, plain},
-                                    CopySumsL<2>{sums});
-    else
-      launch_rows<G_, NU, U_, 0, 0>(C, n, t, LracMuBody<false>{U, V, Pr.Wop, G2.as<double>(), d3, nullptr, s_out, t,
-                                                               plain},
-                                    Fin0<0>{});
-  });
-  if (md3x) {
-    VL_CUDA(cudaMemcpyAsync(xicols, sums, sizeof(double) * 2 * t, cudaMemcpyDeviceToHost, C.stream));
-    VL_CUDA(cudaStreamSynchronize(C.stream));
-  }
   // h via SigmaTilde U, SigmaTilde V and the forward-only dQ dot
   DevBuf SU, SV, scr;
   SU.alloc(sizeof(double) * (size_t)n * t);
@@ -1089,19 +1195,10 @@ void lrac_grad(Ctx& C, const LracPrec& Pr, int t, const double* U, const double*
   VL_CUDA(cudaMemcpyAsync(hcols, sums, sizeof(double) * 2 * t, cudaMemcpyDeviceToHost, C.stream));
   VL_CUDA(cudaStreamSynchronize(C.stream));
   if (md3x && xis) {
-    // xi dP_trace pieces: sum G2 m3, sum m3 / W (host sums over device arrays)
-    std::vector<double> g2h(n), mh(n), wh(n);
-    VL_CUDA(cudaMemcpyAsync(g2h.data(), G2.p, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
-    VL_CUDA(cudaMemcpyAsync(mh.data(), md3x, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
-    VL_CUDA(cudaMemcpyAsync(wh.data(), Pr.Wop, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
+    // xi dP_trace pieces: sum G2 m3, sum m3 / W (device reduction)
+    launch_rows<1, 1, 1, 2, 0>(C, n, 1, XiSumsBody{G2.as<double>(), md3x, Pr.Wop}, CopySumsL<2>{sums});
+    VL_CUDA(cudaMemcpyAsync(xis, sums, sizeof(double) * 2, cudaMemcpyDeviceToHost, C.stream));
     VL_CUDA(cudaStreamSynchronize(C.stream));
-    double a = 0.0, b = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-      a += g2h[i] * mh[i];
-      b += mh[i] / wh[i];
-    }
-    xis[0] = a;
-    xis[1] = b;
   }
   if (k == 0) {
     for (int i = 0; i < 2 * t; ++i) rcols[i] = 0.0;
@@ -1207,6 +1304,79 @@ void lrac_grad(Ctx& C, const LracPrec& Pr, int t, const double* U, const double*
     for (int l = 0; l < k; ++l) s += a1[(size_t)c * k + l] * a2[(size_t)c * k + l];
     rcols[t + c] = 2.0 * s;
   }
+}
+}  // namespace
+
+// out: s (n, device); hcols (2 x t: h_s2, h_rho), rcols (2 x t: r_s2, r_rho),
+// dPt (2); with md3x: xih (t), xir (t), xi_scalars [sum G2 m3, sum m3 / W]
+void lrac_grad(Ctx& C, const LracPrec& Pr, int t, const double* U, const double* V, const double* d3,
+               const double* md3x, double* s_out, double* hcols, double* rcols, double* dPt, double* xicols,
+               double* xis, int plain) {
+  const Factor& F = *Pr.F;
+  const int64_t n = F.pat->n;
+  if (!F.has_grad) fail(kEConfig, "factor was built without gradient");
+  ProfScope ps(C, "lrac_grad", 0.0);
+  DevBuf G2;
+  lrac_G2(C, Pr, G2);
+  double* sums = C.dev_scalars.as<double>();
+  dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
+    constexpr int G_ = decltype(g)::value, NU = decltype(nu)::value, U_ = decltype(uu)::value;
+    if (md3x)
+      launch_rows<G_, NU, U_, 2, 0>(C, n, t, LracMuBody<true>{U, V, Pr.Wop, G2.as<double>(), d3, md3x, s_out, t, plain},
+                                    CopySumsL<2>{sums});
+    else
+      launch_rows<G_, NU, U_, 0, 0>(C, n, t, LracMuBody<false>{U, V, Pr.Wop, G2.as<double>(), d3, nullptr, s_out, t,
+                                                               plain},
+                                    Fin0<0>{});
+  });
+  if (md3x) {
+    VL_CUDA(cudaMemcpyAsync(xicols, sums, sizeof(double) * 2 * t, cudaMemcpyDeviceToHost, C.stream));
+    VL_CUDA(cudaStreamSynchronize(C.stream));
+  }
+  lrac_grad_columns(C, Pr, t, U, V, md3x, G2, hcols, rcols, dPt, xis);
+}
+
+void lrac_grad_split(Ctx& C, const LracPrec& Pr, int mode, int t, int t_glob, const double* U, const double* V,
+                     const double* d3, const double* md3x, double* rowA, double* rowB, double* s_out, double* hcols,
+                     double* rcols, double* dPt, double* xicols, double* xis, int plain) {
+  const Factor& F = *Pr.F;
+  const int64_t n = F.pat->n;
+  if (!F.has_grad) fail(kEConfig, "factor was built without gradient");
+  ProfScope ps(C, "lrac_grad_split", 0.0);
+  double* sums = C.dev_scalars.as<double>();
+  if (mode == 3) {
+    DevBuf G2;
+    lrac_G2(C, Pr, G2);
+    launch_rows<1, 1, 1, 0, 0>(C, n, 1, LracMuFinishBody{rowA, rowB, G2.as<double>(), Pr.Wop, d3, s_out, t_glob, plain},
+                               Fin0<0>{});
+    return;
+  }
+  if (t < 1 || 2 * t > 8192) fail(kECapacity, "invalid probe shard width");
+  if (mode == 2) {
+    dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
+      constexpr int G_ = decltype(g)::value, NU = decltype(nu)::value, U_ = decltype(uu)::value;
+      launch_rows<G_, NU, U_, 0, 0>(C, n, t, LracMuSplitBody<2, false>{U, V, Pr.Wop, nullptr, rowA, rowB, t_glob, t},
+                                    Fin0<0>{});
+    });
+    return;
+  }
+  if (mode != 1) fail(kEConfig, "unknown split mode");
+  DevBuf G2;
+  lrac_G2(C, Pr, G2);
+  dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
+    constexpr int G_ = decltype(g)::value, NU = decltype(nu)::value, U_ = decltype(uu)::value;
+    if (md3x)
+      launch_rows<G_, NU, U_, 2, 0>(C, n, t, LracMuSplitBody<1, true>{U, V, Pr.Wop, md3x, rowA, rowB, t_glob, t},
+                                    CopySumsL<2>{sums});
+    else
+      launch_rows<G_, NU, U_, 0, 0>(C, n, t, LracMuSplitBody<1, false>{U, V, Pr.Wop, nullptr, rowA, rowB, t_glob, t},
+                                    Fin0<0>{});
+  });
+  if (md3x) {
+    VL_CUDA(cudaMemcpyAsync(xicols, sums, sizeof(double) * 2 * t, cudaMemcpyDeviceToHost, C.stream));
+    VL_CUDA(cudaStreamSynchronize(C.stream));
+  }
+  lrac_grad_columns(C, Pr, t, U, V, md3x, G2, hcols, rcols, dPt, xis);
 }
 
 void lrac_solve_system(Ctx& C, const LracPrec& Pr, int t, const double* rhs, double* u, double tol, int max_iter,

@@ -66,6 +66,10 @@ void lrac_free_handles();
 void lrac_grad(Ctx& C, const LracPrec& Pr, int t, const double* U, const double* V, const double* d3,
                const double* md3x, double* s_out, double* hcols, double* rcols, double* dPt, double* xicols,
                double* xis, int plain = 0);
+// probe-sharded lrac_grad: mode 1 local row sums + per-column outputs, 2 centred sums, 3 s
+void lrac_grad_split(Ctx& C, const LracPrec& Pr, int mode, int t, int t_glob, const double* U, const double* V,
+                     const double* d3, const double* md3x, double* rowA, double* rowB, double* s_out, double* hcols,
+                     double* rcols, double* dPt, double* xicols, double* xis, int plain);
 double lrac_sumlogW(Ctx& C, int64_t n, const double* W);
 void lrac_probes(Ctx& C, const LracPrec& Pr, int t, const double* Gn, const double* Gk, double* Z, double* V,
                  double* w_host);

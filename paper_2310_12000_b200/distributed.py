@@ -55,6 +55,13 @@ class ProbeComm:
         return full.cpu().numpy()
 
     def allreduce_(self, tensor):
+        """In-place sum over ranks (device tensors through NCCL; with a CPU
+        backend such as gloo the data is staged through host memory)."""
+        if getattr(tensor, "is_cuda", False) and self.dist.get_backend(self.group) != "nccl":
+            host = tensor.cpu()
+            self.dist.all_reduce(host, group=self.group)
+            tensor.copy_(host)
+            return tensor
         self.dist.all_reduce(tensor, group=self.group)
         return tensor
 
@@ -86,3 +93,33 @@ class ProbeComm:
         full = np.stack([self.allgather_cols(cols[k], probes.shard) for k in range(4)])
         xfull = np.stack([self.allgather_cols(xicols[k], probes.shard) for k in range(2)]) if gamma else np.zeros((2, t_glob))
         return s, full, xfull
+
+    def lrac_grad_pass(self, factor, state, probes, P, md3x, plain=0):
+        """Sharded LRAC gradient pass (eq7): the mu-derivative's per-row
+        control variate through two row-sum allreduce rounds; the per-probe
+        h / r columns gathered in probe order; dP_trace and the xi scalars
+        do not depend on the probes and are identical on every rank."""
+        from . import _lib
+        from . import device as dev
+        ctx, n = factor.ctx, factor.n
+        dv = state._dev
+        t = probes.t
+        t_glob = int(probes.shard[1])
+        rowA = dev.empty(ctx, n, 2)
+        rowB = dev.empty(ctx, n, 2)
+        s = dev.empty(ctx, n, 1)
+        hcols, rcols, xicols = np.zeros((2, t)), np.zeros((2, t)), np.zeros((2, t))
+        dPt, xis = np.zeros(2), np.zeros(2)
+        gamma = md3x is not None
+        head = (ctx.h, P.h)
+        bufs = (_lib.ptr(probes.solves_dev), _lib.ptr(probes.psolves_dev), _lib.ptr(dv["d3"]),
+                _lib.ptr(md3x) if gamma else None, _lib.ptr(rowA), _lib.ptr(rowB), _lib.ptr(s))
+        outs = (_lib.ptr(hcols), _lib.ptr(rcols), _lib.ptr(dPt), _lib.ptr(xicols), _lib.ptr(xis))
+        _lib.call("vl_lrac_grad_split", *head, 1, t, t_glob, *bufs, *outs, int(plain))
+        self.allreduce_(rowA)
+        if not plain:
+            _lib.call("vl_lrac_grad_split", *head, 2, t, t_glob, *bufs, *outs, int(plain))
+            self.allreduce_(rowB)
+        _lib.call("vl_lrac_grad_split", *head, 3, t, t_glob, *bufs, *outs, int(plain))
+        gather = lambda a: np.stack([self.allgather_cols(a[k], probes.shard) for k in range(2)])  # noqa: E731
+        return s, gather(hcols), gather(rcols), dPt, gather(xicols) if gamma else np.zeros((2, t_glob)), xis

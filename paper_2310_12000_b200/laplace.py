@@ -573,7 +573,8 @@ def gradient(state, factor, lik, X, cfg, probes=None, P=None, comm=None):
         _lib.call("vl_grad_probe_pass", ctx.h, factor.h, _lib.ptr(dv["W"]), _lib.ptr(dv["d3"]),
                   _lib.ptr(probes.solves_dev), _lib.ptr(probes.psolves_dev), t, _lib.ptr(s), _lib.ptr(cols),
                   _lib.ptr(md3x) if gamma else None, _lib.ptr(xicols) if gamma else None, plain)
-    tvec, _ = solve_system(factor, state, s, cfg, tol=cfg.mode_cg_tol, P=P)
+    tvec, tvec_its = solve_system(factor, state, s, cfg, tol=cfg.mode_cg_tol, P=P)
+    probes.tvec_iters = int(tvec_its[0])
     terms = np.zeros(4)
     _lib.call("vl_grad_scalar_terms", ctx.h, factor.h, _lib.ptr(dv["b"]), _lib.ptr(tvec), _lib.ptr(terms))
     sums = P.sums()
@@ -606,20 +607,22 @@ def _gradient_lrac(state, factor, lik, X, cfg, probes, P, comm, md3x, s):
     """eq7 + LRAC branch of laplace.py:439-580: d logdet/d mu with the LRAC
     control variate (421-431), dA_op = -SigmaTilde dQ SigmaTilde, ex = 0,
     dP from d L (369-386, 527-533); xi: ex = sum m3/W, dA = dP = -m3/W^2."""
-    if comm is not None and comm.world > 1:
-        raise CapabilityError("probe-sharded gradients are implemented for the vadu preconditioner only")
     ctx, n, dv, t = factor.ctx, factor.n, state._dev, probes.t
     gamma = md3x is not None
-    hcols = np.zeros((2, t))
-    rcols = np.zeros((2, t))
-    dPt = np.zeros(2)
-    xicols = np.zeros((2, t))
-    xis = np.zeros(2)
     plain = 0 if cfg.preconditioner == "lrac" else 1
-    _lib.call("vl_lrac_grad", ctx.h, P.h, t, _lib.ptr(probes.solves_dev), _lib.ptr(probes.psolves_dev),
-              _lib.ptr(dv["d3"]), _lib.ptr(md3x) if gamma else None, _lib.ptr(s), _lib.ptr(hcols),
-              _lib.ptr(rcols), _lib.ptr(dPt), _lib.ptr(xicols), _lib.ptr(xis), plain)
-    tvec, _ = solve_system(factor, state, s, cfg, tol=cfg.mode_cg_tol, P=P)
+    if comm is not None and (comm.world > 1 or getattr(comm, "force_split", False)):
+        s, hcols, rcols, dPt, xicols, xis = comm.lrac_grad_pass(factor, state, probes, P, md3x, plain=plain)
+    else:
+        hcols = np.zeros((2, t))
+        rcols = np.zeros((2, t))
+        dPt = np.zeros(2)
+        xicols = np.zeros((2, t))
+        xis = np.zeros(2)
+        _lib.call("vl_lrac_grad", ctx.h, P.h, t, _lib.ptr(probes.solves_dev), _lib.ptr(probes.psolves_dev),
+                  _lib.ptr(dv["d3"]), _lib.ptr(md3x) if gamma else None, _lib.ptr(s), _lib.ptr(hcols),
+                  _lib.ptr(rcols), _lib.ptr(dPt), _lib.ptr(xicols), _lib.ptr(xis), plain)
+    tvec, tvec_its = solve_system(factor, state, s, cfg, tol=cfg.mode_cg_tol, P=P)
+    probes.tvec_iters = int(tvec_its[0])
     terms = np.zeros(4)
     _lib.call("vl_grad_scalar_terms", ctx.h, factor.h, _lib.ptr(dv["b"]), _lib.ptr(tvec), _lib.ptr(terms))
     dtheta = np.empty(2)

@@ -113,6 +113,32 @@ def _as_nbr_array(neighbors, n):
     return out
 
 
+def _content_key(a):
+    """Exact content digest of an array (shape, dtype and bytes)."""
+    import hashlib
+    a = np.ascontiguousarray(a)
+    h = hashlib.blake2b(digest_size=16)
+    h.update(repr((a.shape, a.dtype.str)).encode())
+    h.update(memoryview(a).cast("B"))
+    return h.hexdigest()
+
+
+_FP_W = {}
+
+
+def _coords_fingerprint(xy):
+    """Cheap content fingerprint of a coordinate array (a fixed pseudo-random
+    projection, ~1 ms at n = 1e6): detects coordinates that differ from the
+    ones a Pattern was built from."""
+    flat = np.ascontiguousarray(xy, dtype=float).reshape(-1)
+    w = _FP_W.get(flat.size)
+    if w is None:
+        w = np.random.default_rng(0x5EED).uniform(0.5, 1.5, size=flat.size)
+        _FP_W.clear()
+        _FP_W[flat.size] = w
+    return (xy.shape, float(flat @ w), float(flat[::7].sum()))
+
+
 class Pattern:
     """Device-resident sparsity pattern + solve schedules (once per dataset)."""
 
@@ -120,6 +146,7 @@ class Pattern:
         self.ctx = ctx or dev.context()
         xy = np.ascontiguousarray(xy, dtype=float)
         nbr = np.ascontiguousarray(nbr, dtype=np.int32)
+        self.coords_fp = _coords_fingerprint(xy)
         self.n, self.d = xy.shape
         self.m = nbr.shape[1] if nbr.ndim == 2 else 0
         if nbr.shape[0] != self.n:
@@ -133,8 +160,9 @@ class Pattern:
         _lib.call("vl_pattern_perm", self.h, _lib.ptr(self.sperm))
         self.siperm = np.empty(self.n, dtype=np.int64)
         self.siperm[self.sperm] = np.arange(self.n)
-        info = (C.c_int64 * 8)()
+        info = (C.c_int64 * 10)()
         _lib.call("vl_pattern_info", self.h, info)
+        self.head_levels, self.head_rows = int(info[8]), int(info[9])
         self.nnz_off = int(info[3])
         self.n_levels = int(info[4])
         self.n_levels_T = int(info[5])
@@ -184,18 +212,20 @@ class Pattern:
             pass
 
 
-_PATTERNS = []  # small LRU of (neighbors object, coords key, order, Pattern)
+_PATTERNS = []  # small LRU of (content key, Pattern)
 
 
 def pattern_for(xy, neighbors, order_kind=DEFAULT_ORDER):
     """Device pattern for (coords, neighbour sets), reused across theta when the
-    same neighbour object is passed again (the fit loop's case)."""
-    key = (xy.shape, float(xy[:64].sum()), float(xy[-64:].sum()), order_kind)
+    same coordinates and neighbour sets come back (keyed on their full
+    contents, so an in-place edit of either builds a fresh pattern)."""
+    nbr = _as_nbr_array(neighbors, xy.shape[0])
+    key = (_content_key(xy), _content_key(nbr), order_kind)
     for ent in _PATTERNS:
-        if ent[0] is neighbors and ent[1] == key:
-            return ent[2]
-    pat = Pattern(xy, _as_nbr_array(neighbors, xy.shape[0]), order_kind)
-    _PATTERNS.append((neighbors, key, pat))
+        if ent[0] == key:
+            return ent[1]
+    pat = Pattern(xy, nbr, order_kind)
+    _PATTERNS.append((key, pat))
     del _PATTERNS[:-4]
     return pat
 
@@ -396,6 +426,9 @@ def build_factor(locs, spec, neighbors, perm=None, want_grad=True, order_kind=DE
     pat = neighbors if isinstance(neighbors, Pattern) else pattern_for(xy, neighbors, order_kind)
     if pat.n != n:
         raise ConfigError("neighbor sets must have one entry per point")
+    if isinstance(neighbors, Pattern) and _coords_fingerprint(xy) != pat.coords_fp:
+        # the factor is assembled from the pattern's device copy of the coordinates
+        raise ConfigError("locations differ from the ones the Pattern was built from")
     m = pat.max_count()
     h = C.c_void_p()
     _lib.call("vl_factor_build", pat.ctx.h, pat.h, float(spec.sigma2), float(spec.rho), float(spec.nu),

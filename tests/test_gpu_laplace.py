@@ -72,10 +72,13 @@ def test_nll_and_gradient_match_reference(vg, name):
     assert np.abs(np.array(got_len) - np.array(ref_len)).max() <= (5 if weak else 1)  # iteration-count flips
     assert val == pytest.approx(float(g["nll"]), rel=1e-8)
     grad = vg.gradient(st, f, lik, X, cfg, probes=probes, P=P)
-    rt = 5e-3 if weak else 1e-7
-    np.testing.assert_allclose(grad["dtheta"], g["dtheta"], rtol=rt, atol=1e-9)
-    np.testing.assert_allclose(grad["dbeta"], g["dbeta"], rtol=rt, atol=1e-9)
-    np.testing.assert_allclose(grad["dxi"], g["dxi"], rtol=rt, atol=1e-9)
+    # SURVEY 8(c) bar: gradients within 1e-8 relative (measured spread <= 5.2e-9, Poisson dtheta[0];
+    # tools/parity_report.py -> profiles/r2_parity_report.jsonl).  The weak preconditioners run
+    # 60-190 CG steps per system and differ from the reference at the CG-tolerance level.
+    rt, at = (5e-3, 1e-9) if weak else (1e-8, 1e-12)
+    np.testing.assert_allclose(grad["dtheta"], g["dtheta"], rtol=rt, atol=at)
+    np.testing.assert_allclose(grad["dbeta"], g["dbeta"], rtol=rt, atol=at)
+    np.testing.assert_allclose(grad["dxi"], g["dxi"], rtol=rt, atol=at)
 
 
 def test_probe_solves_match_oracle_replay(vg):
@@ -158,6 +161,6 @@ def test_lrac_nll_and_gradient_match_reference(vg, name):
     val = vg.neg_marginal_loglik(st, f, cfg, probes=probes, P=P)
     assert val == pytest.approx(float(g["nll"]), rel=1e-8)
     grad = vg.gradient(st, f, lik, X, cfg, probes=probes, P=P)
-    np.testing.assert_allclose(grad["dtheta"], g["dtheta"], rtol=1e-7, atol=1e-9)
-    np.testing.assert_allclose(grad["dbeta"], g["dbeta"], rtol=1e-7, atol=1e-9)
-    np.testing.assert_allclose(grad["dxi"], g["dxi"], rtol=1e-7, atol=1e-9)
+    np.testing.assert_allclose(grad["dtheta"], g["dtheta"], rtol=1e-8, atol=1e-12)
+    np.testing.assert_allclose(grad["dbeta"], g["dbeta"], rtol=1e-8, atol=1e-12)
+    np.testing.assert_allclose(grad["dxi"], g["dxi"], rtol=1e-8, atol=1e-12)
