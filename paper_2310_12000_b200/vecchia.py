@@ -119,7 +119,7 @@ def _content_key(a):
     a = np.ascontiguousarray(a)
     h = hashlib.blake2b(digest_size=16)
     h.update(repr((a.shape, a.dtype.str)).encode())
-    h.update(memoryview(a).cast("B"))
+    h.update(a.reshape(-1).view(np.uint8))
     return h.hexdigest()
 
 
