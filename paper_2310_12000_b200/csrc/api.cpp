@@ -196,10 +196,8 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
   int heavy_rows = 64, heavy_deps = 64;
   if (const char* e = std::getenv("VL_HEAVY_LEVEL_ROWS")) heavy_rows = std::atoi(e);
   if (const char* e = std::getenv("VL_HEAVY_DEPS")) heavy_deps = std::atoi(e);
-  std::vector<int32_t> ilvl_tmp;
   auto items = [&](const std::vector<int32_t>& order, const std::vector<int32_t>& lptr, bool fwd_dir) {
     std::vector<uint32_t> it;
-    ilvl_tmp.clear();
     for (size_t L = 0; L + 1 < lptr.size(); ++L) {
       const int32_t q0 = lptr[L], q1 = lptr[L + 1];
       const bool thin = (q1 - q0) <= heavy_rows;
@@ -213,13 +211,9 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
         }
         if (!heavy) {
           it.push_back((uint32_t)c);
-          ilvl_tmp.push_back((int32_t)L);
         } else {
           for (int32_t p = c; p < c + 32; ++p)
-            if (order[p] >= 0) {
-              it.push_back((uint32_t)p | 0x80000000u);
-              ilvl_tmp.push_back((int32_t)L);
-            }
+            if (order[p] >= 0) it.push_back((uint32_t)p | 0x80000000u);
         }
       }
     }
@@ -281,17 +275,8 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
     upload(C, S.idx, idx);
     upload(C, S.map, map);
   };
-  // per-item level and per-level item counts (the lagged start of trsv1)
-  auto levels = [&](DevBuf& ilvl, DevBuf& lcnt, size_t nlev) {
-    std::vector<uint32_t> cntl(std::max<size_t>(nlev, 1), 0);
-    for (int32_t L : ilvl_tmp) cntl[L]++;
-    upload(C, ilvl, ilvl_tmp);
-    upload(C, lcnt, cntl);
-  };
   auto fi = items(fwd, P.fwd_level_ptr, true);
-  levels(P.fwd_ilvl, P.fwd_lcnt, P.fwd_level_ptr.size() - 1);
   auto bi = items(bwd, P.bwd_level_ptr, false);
-  levels(P.bwd_ilvl, P.bwd_lcnt, P.bwd_level_ptr.size() - 1);
   P.fwd_nitems = (int64_t)fi.size();
   P.bwd_nitems = (int64_t)bi.size();
   // dense head block + backward schedule without it
@@ -306,7 +291,6 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
     for (uint32_t it : fi)
       if ((int64_t)(it & 0x7fffffffu) < P.fwd_level_ptr[P.head_L]) ++P.fwd_items_head_end;
   auto bni = items(P.bwdnh_order_h, P.bwdnh_level_ptr, false);
-  levels(P.bwdnh_ilvl, P.bwdnh_lcnt, P.bwdnh_level_ptr.size() - 1);
   P.bwdnh_nitems = (int64_t)bni.size();
   slabs(fwd, fi, true, P.fwd_sl);
   slabs(bwd, bi, false, P.bwd_sl);
@@ -342,8 +326,6 @@ int vl_ctx_create(int device, void* stream, vl_ctx** out) {
     C.num_sms = prop.multiProcessorCount;
     if (const char* e = std::getenv("VL_TRSV_BPS")) C.trsv_blocks_per_sm = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("VL_SPIN_MAX_NS")) C.spin_max_ns = std::max(0, std::atoi(e));
-    if (const char* e = std::getenv("VL_TRSV_LAG")) C.trsv_lag = std::max(0, std::atoi(e));
-    if (const char* e = std::getenv("VL_LAG_NS")) C.lag_spin_ns = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("VL_THIN_PASSES")) C.thin_passes = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("VL_MIN_THICK")) C.min_thick_levels = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("VL_USE_HEAD")) C.use_head = std::atoi(e) != 0;

@@ -62,12 +62,6 @@ struct Ctx {
   int trsv_blocks_per_sm = 4;
   // max nanosleep backoff while spinning on a dependency (0 = pure polling)
   int spin_max_ns = 64;
-  // single-RHS solves: an item of level L starts gathering only once every item
-  // of level L - trsv_lag is complete (0 = off); cuts the polling traffic of
-  // warps that hold items far ahead of the completion front
-  int trsv_lag = 0;
-  int lag_spin_ns = 256;
-  DevBuf lvl_done;      // per-level completed-item counters (zeroed per solve)
   // thin solve levels: <= thin_passes * (1024 / G) rows run on a single CTA
   int thin_passes = 0;
   int min_thick_levels = 4;
@@ -120,8 +114,6 @@ struct Pattern {
   int64_t fwd_len = 0, bwd_len = 0;
   DevBuf fwd_lptr, bwd_lptr;  // device copies of the padded level pointers
   DevBuf fwd_items, bwd_items;  // single-RHS work items (light 32-row chunks / heavy rows)
-  DevBuf fwd_ilvl, bwd_ilvl, bwdnh_ilvl;  // level of each work item (int32)
-  DevBuf fwd_lcnt, bwd_lcnt, bwdnh_lcnt;  // work items per level (uint32)
   int64_t fwd_nitems = 0, bwd_nitems = 0;
   // dense head block (see pattern.cpp): rows of forward levels < head_L
   int64_t head_max = 3072;

@@ -139,8 +139,6 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
   int L0;
   const uint32_t* items;
   int64_t nitems, npos;
-  LagSched lg{nullptr, nullptr, C.lvl_done.as<unsigned>(), C.trsv_lag, 0, (unsigned)C.lag_spin_ns};
-  int64_t nlev_main = 0;
   Slab sl{nullptr, nullptr, nullptr, nullptr};
   auto pick = [&](const Pattern::Slabs& S, const DevBuf& sv, int64_t skip) {
     sl.off = S.off.as<uint32_t>() + skip;  // also the heavy items' descriptors
@@ -158,10 +156,6 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
     nitems = P.fwd_nitems - (head ? P.fwd_items_head_end : 0);
     npos = P.fwd_len;
     pick(P.fwd_sl, F.sv_fwd, head ? P.fwd_items_head_end : 0);
-    lg.ilvl = P.fwd_ilvl.as<int32_t>() + (head ? P.fwd_items_head_end : 0);
-    lg.lcnt = P.fwd_lcnt.as<uint32_t>();
-    lg.Lmin = L0;
-    nlev_main = (int64_t)P.fwd_level_ptr.size() - 1;
   } else if (head) {
     order = P.bwdnh_order.as<int32_t>();
     lptr_d = P.bwdnh_lptr.as<int32_t>();
@@ -171,9 +165,6 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
     nitems = P.bwdnh_nitems;
     npos = P.bwdnh_len;
     pick(P.bwdnh_sl, F.sv_bwdnh, 0);
-    lg.ilvl = P.bwdnh_ilvl.as<int32_t>();
-    lg.lcnt = P.bwdnh_lcnt.as<uint32_t>();
-    nlev_main = (int64_t)P.bwdnh_level_ptr.size() - 1;
   } else {
     order = P.bwd_order.as<int32_t>();
     lptr_d = P.bwd_lptr.as<int32_t>();
@@ -183,9 +174,6 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
     nitems = P.bwd_nitems;
     npos = P.bwd_len;
     pick(P.bwd_sl, F.sv_bwd, 0);
-    lg.ilvl = P.bwd_ilvl.as<int32_t>();
-    lg.lcnt = P.bwd_lcnt.as<uint32_t>();
-    nlev_main = (int64_t)P.bwd_level_ptr.size() - 1;
   }
   const bool single = (G == 1 && NU == 1 && U == 1) && C.thin_passes == 0;
   // launch geometry and slot counts
@@ -276,17 +264,10 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
   auto run_main = [&](int slot0) {
     if (single) {
       int sb = slot0;
-      if (lg.lag > 0 && nlev_main > 0) {
-        C.lvl_done.alloc(sizeof(unsigned) * (size_t)nlev_main);
-        lg.done = C.lvl_done.as<unsigned>();
-        VL_CUDA(cudaMemsetAsync(lg.done, 0, sizeof(unsigned) * (size_t)nlev_main, C.stream));
-      } else {
-        lg.lag = 0;
-      }
       void* args[] = {(void*)&nitems, (void*)&npos,  (void*)&items,    (void*)&order,  (void*)&deps,
                       (void*)&x,      (void*)&body,  (void*)&fin,      (void*)&partials, (void*)&counter,
                       (void*)&gate,   (void*)&smax,  (void*)&tstamp,   (void*)&sb,     (void*)&total,
-                      (void*)&sl,     (void*)&lg};
+                      (void*)&sl};
       if (nitems > 0)
         VL_CUDA(cudaLaunchCooperativeKernel((const void*)k1, dim3(grid1), dim3(kRowsThreads), args, smem1,
                                             C.stream));

@@ -856,20 +856,6 @@ constexpr uint32_t kHeavyBit = 0x80000000u;
 #define VL_HPREFETCH 0
 #endif
 
-// Lagged start of the single-RHS work items: an item of level L first waits
-// until every item of level L - lag has completed (lane 0 polls one counter),
-// and only then gathers / polls its dependencies.  Correctness never depends
-// on the counters (values stay the flags); they only keep warps whose items are
-// far ahead of the completion front off the L2 with dependency polls.
-struct LagSched {
-  const int32_t* ilvl;  // level of each work item (same offset as items)
-  const uint32_t* lcnt; // items per level
-  unsigned* done;       // completed items per level (zeroed before the launch)
-  int lag;              // 0 = off
-  int Lmin;             // levels below are complete before the launch (head block)
-  unsigned ns;          // max backoff while waiting on a level counter
-};
-
 template <int NR, class Deps, class Body, class Fin>
 __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int64_t npos,
                                                              const uint32_t* __restrict__ items,
@@ -879,7 +865,7 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
                                                              unsigned* __restrict__ counter,
                                                              const int* __restrict__ gate, unsigned smax,
                                                              long long* __restrict__ tstamp, int slot_base,
-                                                             int total_slots, Slab sl, LagSched lg) {
+                                                             int total_slots, Slab sl) {
   if (gate != nullptr && *((volatile const int*)gate) == 0) return;
   extern __shared__ double rsh[];
   constexpr int NRR = NR > 0 ? NR : 1;
@@ -928,28 +914,11 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
     }
     c_d = n_d; c_o = n_o; c_w = n_w;
     desc(it + 2 * nwarps, n_d, n_o, n_w);
-    int lvl = 0;
-    if (lg.lag > 0) {
-      lvl = __ldg(lg.ilvl + it);
-      const int lw = lvl - lg.lag;
-      if (lw >= lg.Lmin) {
-        if (lane == 0) {
-          const unsigned target = __ldg(lg.lcnt + lw);
-          unsigned ns = 32;
-          while (*((volatile unsigned*)(lg.done + lw)) < target) {
-            __nanosleep(ns);
-            ns = ns < lg.ns ? ns * 2 : lg.ns;
-          }
-        }
-        __syncwarp();
-      }
-    }
     if (!(item & kHeavyBit)) {
       if (sl.idx != nullptr)
         trsv_row1s((int64_t)item + lane, npos, order, off, (int)wk, sl, lane, x, body, smax, tstamp, acc[0][0]);
       else
         trsv_row1((int64_t)item + lane, npos, order, deps, x, body, smax, tstamp, acc[0][0]);
-      if (lg.lag > 0 && lane == 0) atomicAdd(lg.done + lvl, 1u);
       continue;
     }
     const int64_t s = (int64_t)(item & ~kHeavyBit);
@@ -1008,7 +977,6 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
         tstamp[s] = g;
       }
-      if (lg.lag > 0) atomicAdd(lg.done + lvl, 1u);
     }
   }
   if constexpr (NR > 0) {
