@@ -320,6 +320,30 @@ int vl_pred_z3(vl_ctx* ctx, const vl_factor* f, const double* W_dev, int64_t c, 
                const double* z2_dev, double* z3_dev);
 int vl_pred_accum(vl_ctx* ctx, const vl_pred* b, const double* U_dev, int64_t c, double* acc_dev, double* cov_dev);
 
+/* ---- dense fp64 kernels of the low-rank paths (debug / test entry points) ----
+ * Column-major, BLAS argument meaning: C = alpha op(A) [diag(kw)] op(B) + beta C with
+ * op(A) m x k, op(B) k x n; kw (length k, device) optional; lower != 0 writes only
+ * C(i, j), i >= j.  Replaces the cublasDgemm / cublasDsyrk calls of the LRAC Woodbury
+ * core (preconditioners.py:176-202) and of _lrac_dL (laplace.py:369-386). */
+int vl_dgemm(vl_ctx* ctx, int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha, const double* A_dev,
+             int64_t lda, const double* B_dev, int64_t ldb, double beta, double* C_dev, int64_t ldc,
+             const double* kw_dev, int lower);
+/* Linv = L^-1 for lower-triangular L (k x k, column-major); replaces cublasDtrsm
+ * (triangular solves are applied as products with the inverse). */
+int vl_dtrtri_lower(vl_ctx* ctx, int64_t k, const double* L_dev, int64_t ldl, double* Linv_dev, int64_t ldi);
+
+/* Probes supplied by the caller instead of drawn from N(0, P) -- the reference's
+ * ProbeSet injection into neg_marginal_loglik / gradient (laplace.py:340, 439;
+ * iterative.py:222-244), e.g. Rademacher probes.
+ * vl_probes_rademacher: Z (n x t, storage order) with entry (factor row i, column c) =
+ *   -1 if the top bit of splitmix64(seed * 0x9E3779B97F4A7C15 + i * t_glob + c0 + c) is set, else +1.
+ * vl_probes_given: V = P^-1 Z (eq6 sandwich / diagonal preconditioner of vl_precond_dinv) and
+ *   w_host[c] = z_c . v_c (the SLQ weights, iterative.py:268-271). */
+int vl_probes_rademacher(vl_ctx* ctx, const vl_pattern* p, int64_t t, int64_t t_glob, int64_t c0, uint64_t seed,
+                         double* Z_dev);
+int vl_probes_given(vl_ctx* ctx, const vl_factor* f, const double* dinv_dev, int pkind, int64_t t, const double* Z_dev,
+                    double* V_dev, double* w_host);
+
 #ifdef __cplusplus
 }
 #endif

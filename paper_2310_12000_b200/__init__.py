@@ -28,7 +28,8 @@ from .vecchia import (
 )
 
 __version__ = "0.1.0"
-from .laplace import BackendConfig, LaplaceState, find_mode, gradient, make_probes, neg_marginal_loglik
+from .laplace import (BackendConfig, LaplaceState, find_mode, gradient, make_probes, neg_marginal_loglik,
+                      probes_from_Z, rademacher_probes)
 from .likelihoods import get_likelihood
 from .iterative import ProbeSet, Tridiag
 from .predict import (

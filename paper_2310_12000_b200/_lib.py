@@ -143,6 +143,11 @@ _SIGS.update({
     "vl_lrac_probes": [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "vl_lrac_grad": [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                      c_void_p, c_void_p, c_void_p, c_int],
+    "vl_probes_rademacher": [c_void_p, c_void_p, c_int64, c_int64, c_int64, C.c_uint64, c_void_p],
+    "vl_probes_given": [c_void_p, c_void_p, c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p],
+    "vl_dgemm": [c_void_p, c_int, c_int, c_int64, c_int64, c_int64, c_double, c_void_p, c_int64, c_void_p, c_int64,
+                 c_double, c_void_p, c_int64, c_void_p, c_int],
+    "vl_dtrtri_lower": [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64],
     "vl_lrac_grad_split": [c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                            c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int],
     "vl_lowrank_create": [c_void_p, c_void_p, c_int, c_int, c_double, c_void_p, c_void_p, c_void_p],

@@ -67,7 +67,7 @@ def build(verbose=False, jobs=None, defines=(), lib=LIB):
                 print(f"--- {s}\n{log}")
     newest = max(os.path.getmtime(o) for o in objs)
     if not (os.path.exists(lib) and os.path.getmtime(lib) >= newest):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-lcudart", "-lcublas", "-lcusolver", "-Xcompiler", "-pthread"]
+        cmd = [nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-lcudart", "-lcusolver", "-Xcompiler", "-pthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

@@ -14,6 +14,7 @@
 #include "lrac.h"
 #include "ops.h"
 #include "predict.h"
+#include "dense.h"
 #include "pcg.h"
 
 struct vl_ctx {
@@ -691,6 +692,41 @@ int vl_lrac_grad(vl_ctx* h, const vl_lracw* w, int64_t t, const double* U, const
                  const double* md3x, double* s, double* hcols, double* rcols, double* dPt, double* xicols,
                  double* xis, int plain) {
   return guard_dev(h, [&] { lrac_grad(h->c, w->p, (int)t, U, V, d3, md3x, s, hcols, rcols, dPt, xicols, xis, plain); });
+}
+
+int vl_probes_rademacher(vl_ctx* h, const vl_pattern* p, int64_t t, int64_t t_glob, int64_t c0, uint64_t seed,
+                         double* Z) {
+  return guard_dev(h, [&] {
+    if (t < 1 || c0 < 0 || c0 + t > t_glob) fail(kEConfig, "invalid probe column range");
+    rademacher_probes(h->c, p->p, (int)t, (int)t_glob, (int)c0, seed, Z);
+  });
+}
+
+int vl_probes_given(vl_ctx* h, const vl_factor* f, const double* dinv, int pkind, int64_t t, const double* Z,
+                    double* V, double* w_host) {
+  return guard_dev(h, [&] { probes_given(h->c, f->f, dinv, pkind, (int)t, (int)t, Z, V, w_host); });
+}
+
+int vl_dgemm(vl_ctx* h, int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+             int64_t lda, const double* B, int64_t ldb, double beta, double* Cm, int64_t ldc, const double* kw,
+             int lower) {
+  return guard_dev(h, [&] {
+    Gemm g;
+    g.ta = transa != 0; g.tb = transb != 0;
+    g.m = (int)m; g.n = (int)n; g.k = (int)k;
+    g.alpha = alpha; g.beta = beta;
+    g.A = A; g.lda = (int)lda; g.B = B; g.ldb = (int)ldb; g.C = Cm; g.ldc = (int)ldc;
+    g.kw = kw; g.lower = lower != 0;
+    dgemm(h->c, g);
+    VL_CUDA(cudaStreamSynchronize(h->c.stream));
+  });
+}
+
+int vl_dtrtri_lower(vl_ctx* h, int64_t k, const double* L, int64_t ldl, double* Li, int64_t ldi) {
+  return guard_dev(h, [&] {
+    dtrtri_lower(h->c, (int)k, L, (int)ldl, Li, (int)ldi);
+    VL_CUDA(cudaStreamSynchronize(h->c.stream));
+  });
 }
 
 int vl_lrac_grad_split(vl_ctx* h, const vl_lracw* w, int mode, int64_t t, int64_t t_glob, const double* U,

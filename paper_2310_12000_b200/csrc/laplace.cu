@@ -563,6 +563,94 @@ void probes_eq6(Ctx& C, const Factor& F, const double* dinv, int pkind, int t, i
   read_sums(C, sums, w_host, t);
 }
 
+namespace {
+// forward solve of P^-1 z = B^-1 (dinv o B^-T z) with the SLQ weight z_c . v_c fused
+struct RhsDinvDotZ {
+  const double* y;
+  const double* dinv;
+  const double* Z;
+  int ld;
+  VL_D double rhs(int64_t s, int c, double&) const { return y[s * ld + c] * dinv[s]; }
+  VL_D void out(int64_t s, int c, double x, double& acc) const { acc += Z[s * ld + c] * x; }
+};
+// diagonal P: V = dinv o Z, w_c = z_c . v_c
+struct GivenDiagBody {
+  const double* Z;
+  const double* dinv;
+  double* V;
+  int ld;
+  template <int G_, int NU, int U, int NR>
+  VL_D void run(int64_t s, bool valid, int gl, int t, double (&acc)[NR][NU * U]) const {
+    if (!valid) return;
+    double z[NU * U], v[NU * U];
+    load_row<G_, NU, U>(Z, ld, s, gl, t, z);
+    const double f = dinv[s];
+#pragma unroll
+    for (int i = 0; i < NU * U; ++i) {
+      v[i] = f * z[i];
+      if (vl::Cols<G_, NU, U>::col(gl, i) < t) acc[0][i] += z[i] * v[i];
+    }
+    store_row<G_, NU, U>(V, ld, s, gl, t, v);
+  }
+};
+
+VL_D uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Rademacher probes: entry (factor row i, column c) = sign bit of
+// splitmix64(seed * golden + i * t_glob + c0 + c) -> -1 / +1; written in storage order
+__global__ void rademacher_kernel(int64_t n, int t, int ld, int t_glob, int c0, uint64_t seed,
+                                  const int32_t* __restrict__ fidx, double* __restrict__ Z) {
+  const int64_t tot = n * (int64_t)t;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = e / t;
+    const int c = (int)(e % t);
+    const uint64_t key = seed * 0x9E3779B97F4A7C15ull + (uint64_t)fidx[s] * (uint64_t)t_glob + (uint64_t)(c0 + c);
+    Z[s * ld + c] = (splitmix64(key) >> 63) ? -1.0 : 1.0;
+  }
+}
+}  // namespace
+
+void rademacher_probes(Ctx& C, const Pattern& P, int t, int t_glob, int c0, uint64_t seed, double* Z) {
+  const int64_t tot = P.n * (int64_t)t;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, 8LL * C.num_sms));
+  rademacher_kernel<<<blocks, 256, 0, C.stream>>>(P.n, t, t, t_glob, c0, seed, P.fidx.as<int32_t>(), Z);
+  VL_LAUNCH_CHECK();
+}
+
+// Caller-supplied probes Z (laplace.py:340 ProbeSet injection): V = P^-1 Z for the eq6
+// sandwich / diagonal preconditioners, w_c = z_c . v_c (iterative.py:268-271)
+void probes_given(Ctx& C, const Factor& F, const double* dinv, int pkind, int t, int ld, const double* Z, double* V,
+                  double* w_host) {
+  const Pattern& P = *F.pat;
+  const int64_t n = P.n;
+  double* sums = C.dev_scalars.as<double>();
+  if (t > 256) fail(kECapacity, "too many probe columns per call");
+  if (pkind == 1) {
+    dispatch_cols(t, ld, [&](auto g, auto nu, auto uu) {
+      constexpr int G_ = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
+      launch_rows<G_, NU, U, 1, 0>(C, n, t, GivenDiagBody{Z, dinv, V, ld}, CopySums<1>{sums});
+    });
+    read_sums(C, sums, w_host, t);
+    return;
+  }
+  DevBuf Y;
+  Y.alloc(sizeof(double) * (size_t)n * ld);
+  DepsEll dfw{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
+  DepsCsr dbw{P.tptr.as<int32_t>(), P.tidx.as<int32_t>(), F.valT.as<double>()};
+  dispatch_cols(t, ld, [&](auto g, auto nu, auto uu) {
+    constexpr int G_ = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
+    ProfScope ps(C, "probe_given", 2.0 * bapply_bytes(P, t, 1));
+    launch_trsv<G_, NU, U, 0>(C, F, false, t, ld, dbw, Y.as<double>(), TrsvPlain{Z, ld}, Fin0<0>{});
+    launch_trsv<G_, NU, U, 1>(C, F, true, t, ld, dfw, V, RhsDinvDotZ{Y.as<double>(), dinv, Z, ld}, CopySums<1>{sums});
+  });
+  read_sums(C, sums, w_host, t);
+}
+
 void probes_vadu(Ctx& C, const Factor& F, const double* W, int t, int ld, const double* G, double* Z, double* V,
                  double* w_host) {
   const Pattern& P = *F.pat;

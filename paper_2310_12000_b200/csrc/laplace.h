@@ -63,6 +63,11 @@ void precond_dinv(Ctx& C, const Factor& F, int variant, const double* W, double*
 inline int precond_pkind(int variant) { return variant <= 2 ? 0 : 1; }
 double sum_log(Ctx& C, int64_t n, const double* x);
 // Z ~ N(0, P) from base normals G, V = P^-1 Z, w_c = z_c . v_c for either kind
+// Rademacher probe block (factor-order counter hash, storage-order output), columns c0..c0+t of t_glob
+void rademacher_probes(Ctx& C, const Pattern& P, int t, int t_glob, int c0, uint64_t seed, double* Z);
+// V = P^-1 Z and w_c = z_c . v_c for caller-supplied probes
+void probes_given(Ctx& C, const Factor& F, const double* dinv, int pkind, int t, int ld, const double* Z, double* V,
+                  double* w_host);
 void probes_eq6(Ctx& C, const Factor& F, const double* dinv, int pkind, int t, int ld, const double* G, double* Z,
                 double* V, double* w_host);
 

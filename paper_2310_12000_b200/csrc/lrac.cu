@@ -8,7 +8,6 @@
 // operator applies, all elementwise/reduction passes.  Library: the plain
 // n x k GEMMs / k x k triangular solves of the Woodbury core (cuBLAS) and the
 // k x k Cholesky of M (cuSOLVER potrf).
-#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include <cmath>
@@ -17,6 +16,7 @@
 #include "bodies.cuh"
 #include "launch.cuh"
 #include "lrac.h"
+#include "dense.h"
 #include "ops.h"
 #include "pcg_common.cuh"
 
@@ -25,18 +25,8 @@ namespace vl {
 namespace {
 
 std::mutex g_h_mu;
-cublasHandle_t g_blas[16] = {};
 cusolverDnHandle_t g_solv[16] = {};
 
-cublasHandle_t blas(Ctx& C) {
-  std::lock_guard<std::mutex> lk(g_h_mu);
-  cublasHandle_t& h = g_blas[C.device & 15];
-  if (!h) {
-    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) fail(kECuda, "cublasCreate failed");
-  }
-  cublasSetStream(h, C.stream);
-  return h;
-}
 cusolverDnHandle_t solver(Ctx& C) {
   std::lock_guard<std::mutex> lk(g_h_mu);
   cusolverDnHandle_t& h = g_solv[C.device & 15];
@@ -45,9 +35,6 @@ cusolverDnHandle_t solver(Ctx& C) {
   }
   cusolverDnSetStream(h, C.stream);
   return h;
-}
-void blas_ok(cublasStatus_t s, const char* what) {
-  if (s != CUBLAS_STATUS_SUCCESS) fail(kECuda, std::string("cuBLAS failure in ") + what);
 }
 
 struct MaternK {
@@ -298,11 +285,6 @@ __global__ void __launch_bounds__(kPcThreads) pchol_step_kernel(int64_t n, int d
   }
 }
 
-__global__ void scale_rows_kernel(int64_t n, int k, const double* __restrict__ W, const double* __restrict__ L,
-                                  double* __restrict__ S) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * k; e += (int64_t)gridDim.x * blockDim.x)
-    S[e] = sqrt(W[e / k]) * L[e];
-}
 
 __global__ void add_identity_kernel(int k, double* M) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) M[(size_t)i * k + i] += 1.0;
@@ -487,8 +469,6 @@ struct RzFin {
 
 void lrac_free_handles() {
   std::lock_guard<std::mutex> lk(g_h_mu);
-  for (auto& h : g_blas)
-    if (h) { cublasDestroy(h); h = nullptr; }
   for (auto& h : g_solv)
     if (h) { cusolverDnDestroy(h); h = nullptr; }
 }
@@ -559,16 +539,21 @@ void lowrank_prepare(Ctx& C, const Factor& F, const LracFactor* LFp, const doubl
     return;
   }
   ProfScope ps(C, "lrac_prepare", 0.0);
-  DevBuf S, info, ld;
-  S.alloc(sizeof(double) * (size_t)n * LF.k);
-  scale_rows_kernel<<<C.num_sms * 8, 256, 0, C.stream>>>(n, LF.k, W, LF.L.as<double>(), S.as<double>());
-  VL_LAUNCH_CHECK();
+  DevBuf info, ld;
   Pr.Lm.alloc(sizeof(double) * (size_t)k * k);
-  // M = S_k S_k^T with S viewed column-major as (LF.k x n); only the leading keff rows are used
-  const double one = 1.0, zero = 0.0;
-  blas_ok(cublasDsyrk(blas(C), CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, k, (int)n, &one, S.as<double>(), LF.k, &zero,
-                      Pr.Lm.as<double>(), k),
-          "dsyrk");
+  // M = L^T diag(W) L (lower triangle): L (n x LF.k row-major) is the column-major (LF.k x n)
+  // matrix A, so M = A diag(W) A^T -- the hand-written weighted SYRK (dense.cu), no scaled copy of L
+  {
+    Gemm g;
+    g.tb = true;
+    g.m = k; g.n = k; g.k = (int)n;
+    g.A = LF.L.as<double>(); g.lda = LF.k;
+    g.B = LF.L.as<double>(); g.ldb = LF.k;
+    g.C = Pr.Lm.as<double>(); g.ldc = k;
+    g.kw = W;
+    g.lower = true;
+    dgemm(C, g);
+  }
   add_identity_kernel<<<8, 256, 0, C.stream>>>(k, Pr.Lm.as<double>());
   VL_LAUNCH_CHECK();
   cusolverDnHandle_t sh = solver(C);
@@ -589,6 +574,17 @@ void lowrank_prepare(Ctx& C, const Factor& F, const LracFactor* LFp, const doubl
   VL_CUDA(cudaMemcpyAsync(&Pr.logdetM, ld.p, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
   VL_CUDA(cudaStreamSynchronize(C.stream));
   if (h_info != 0) fail(kEFactorization, "LRAC Woodbury core M is not positive definite");
+  // explicit Lm^-1 and M^-1 = Lm^-T Lm^-1: the Woodbury solves become one k x k product
+  Pr.Lmi.alloc(sizeof(double) * (size_t)k * k);
+  Pr.Minv.alloc(sizeof(double) * (size_t)k * k);
+  dtrtri_lower(C, k, Pr.Lm.as<double>(), k, Pr.Lmi.as<double>(), k);
+  Gemm g;
+  g.ta = true;
+  g.m = k; g.n = k; g.k = k;
+  g.A = Pr.Lmi.as<double>(); g.lda = k;
+  g.B = Pr.Lmi.as<double>(); g.ldb = k;
+  g.C = Pr.Minv.as<double>(); g.ldc = k;
+  dgemm(C, g);
 }
 
 // z = W o r - W o (L M^-1 L^T (W o r))
@@ -606,22 +602,31 @@ static void woodbury(Ctx& C, const LracPrec& Pr, int t, const double* r, double*
     launch_rows<G, NU, U, 0, 0>(C, n, t, MulWBody{Pr.W, r, x.as<double>(), t}, Fin0<0>{}, gate);
   });
   if (k > 0) {
-    const double one = 1.0, zero = 0.0;
-    cublasHandle_t hb = blas(C);
-    // w (k x t) = A (k x n) * Xc^T ; A = L^T viewed column-major (lda = kl), Xc = x viewed (t x n, ld t)
-    blas_ok(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, k, t, (int)n, &one, Pr.LF->L.as<double>(), kl, x.as<double>(),
-                        t, &zero, w.as<double>(), k),
-            "dgemm Lt x");
-    blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, k, t, &one,
-                        Pr.Lm.as<double>(), k, w.as<double>(), k),
-            "dtrsm");
-    blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, k, t, &one,
-                        Pr.Lm.as<double>(), k, w.as<double>(), k),
-            "dtrsm T");
-    // Yc (t x n) = w^T (t x k) * A (k x n)
-    blas_ok(cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, t, (int)n, k, &one, w.as<double>(), k, Pr.LF->L.as<double>(),
-                        kl, &zero, y.as<double>(), t),
-            "dgemm L w");
+    DevBuf u;
+    u.alloc(sizeof(double) * (size_t)k * t);
+    // w (k x t) = A (k x n) x^T ; A = L^T viewed column-major (lda = kl), x viewed (t x n, ld t)
+    Gemm g1;
+    g1.tb = true;
+    g1.m = k; g1.n = t; g1.k = (int)n;
+    g1.A = Pr.LF->L.as<double>(); g1.lda = kl;
+    g1.B = x.as<double>(); g1.ldb = t;
+    g1.C = w.as<double>(); g1.ldc = k;
+    dgemm(C, g1);
+    // u = M^-1 w
+    Gemm g2;
+    g2.m = k; g2.n = t; g2.k = k;
+    g2.A = Pr.Minv.as<double>(); g2.lda = k;
+    g2.B = w.as<double>(); g2.ldb = k;
+    g2.C = u.as<double>(); g2.ldc = k;
+    dgemm(C, g2);
+    // y (t x n, column-major) = u^T (t x k) A (k x n)
+    Gemm g3;
+    g3.ta = true;
+    g3.m = t; g3.n = (int)n; g3.k = k;
+    g3.A = u.as<double>(); g3.lda = k;
+    g3.B = Pr.LF->L.as<double>(); g3.ldb = kl;
+    g3.C = y.as<double>(); g3.ldc = t;
+    dgemm(C, g3);
   } else {
     VL_CUDA(cudaMemsetAsync(y.p, 0, sizeof(double) * (size_t)n * t, C.stream));
   }
@@ -810,10 +815,13 @@ void lrac_probes(Ctx& C, const LracPrec& Pr, int t, const double* Gn, const doub
   const int k = Pr.LF->keff, kl = Pr.LF->k;
   ProfScope ps(C, "lrac_probes", 0.0);
   if (k > 0) {
-    const double one = 1.0, zero = 0.0;
-    blas_ok(cublasDgemm(blas(C), CUBLAS_OP_N, CUBLAS_OP_N, t, (int)n, k, &one, Gk, t, Pr.LF->L.as<double>(), kl,
-                        &zero, Z, t),
-            "dgemm L Gk");
+    // Z (t x n, column-major) = Gk (t x k, column-major view of the k x t row-major draws) A (k x n)
+    Gemm g;
+    g.m = t; g.n = (int)n; g.k = k;
+    g.A = Gk; g.lda = t;
+    g.B = Pr.LF->L.as<double>(); g.ldb = kl;
+    g.C = Z; g.ldc = t;
+    dgemm(C, g);
   } else {
     VL_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * (size_t)n * t, C.stream));
   }
@@ -1148,17 +1156,17 @@ namespace {
 void lrac_G2(Ctx& C, const LracPrec& Pr, DevBuf& G2) {
   const int64_t n = Pr.F->pat->n;
   const int k = Pr.LF->keff, kl = Pr.LF->k;
-  cublasHandle_t hb = blas(C);
-  const double one = 1.0;
   DevBuf Y;
   // G2 = diag(L M^-1 L^T) = column norms of Lm^-1 L^T
   Y.alloc(sizeof(double) * (size_t)n * kl);
   G2.alloc(sizeof(double) * n);
   if (k > 0) {
-    VL_CUDA(cudaMemcpyAsync(Y.p, Pr.LF->L.p, sizeof(double) * (size_t)n * kl, cudaMemcpyDeviceToDevice, C.stream));
-    blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, k, (int)n,
-                        &one, Pr.Lm.as<double>(), k, Y.as<double>(), kl),
-            "trsm G2");
+    Gemm g;  // Y (k x n, ld kl) = Lm^-1 A, A = L^T viewed column-major
+    g.m = k; g.n = (int)n; g.k = k;
+    g.A = Pr.Lmi.as<double>(); g.lda = k;
+    g.B = Pr.LF->L.as<double>(); g.ldb = kl;
+    g.C = Y.as<double>(); g.ldc = kl;
+    dgemm(C, g);
     colnorm2_kernel<<<C.num_sms * 4, 256, 0, C.stream>>>(n, k, kl, Y.as<double>(), G2.as<double>());
   } else {
     VL_CUDA(cudaMemsetAsync(G2.p, 0, sizeof(double) * n, C.stream));
@@ -1174,8 +1182,6 @@ void lrac_grad_columns(Ctx& C, const LracPrec& Pr, int t, const double* U, const
   const Pattern& P = *F.pat;
   const int64_t n = P.n;
   const int k = Pr.LF->keff, kl = Pr.LF->k;
-  cublasHandle_t hb = blas(C);
-  const double one = 1.0, zero = 0.0, mone = -1.0;
   double* sums = C.dev_scalars.as<double>();
   // h via SigmaTilde U, SigmaTilde V and the forward-only dQ dot
   DevBuf SU, SV, scr;
@@ -1205,32 +1211,27 @@ void lrac_grad_columns(Ctx& C, const LracPrec& Pr, int t, const double* U, const
     dPt[0] = dPt[1] = 0.0;
     return;
   }
+  // dense chain on the hand-written GEMM (dense.cu); triangular solves as products with inverses
+  auto gemm = [&](bool ta, bool tb, int m_, int n_, int k_, double alpha, const double* A_, int lda_, const double* B_,
+                  int ldb_, double beta, double* C_, int ldc_, const double* kw = nullptr) {
+    Gemm g;
+    g.ta = ta; g.tb = tb; g.m = m_; g.n = n_; g.k = k_; g.alpha = alpha; g.beta = beta;
+    g.A = A_; g.lda = lda_; g.B = B_; g.ldb = ldb_; g.C = C_; g.ldc = ldc_; g.kw = kw;
+    dgemm(C, g);
+  };
+  const double* Lp = Pr.LF->L.as<double>();  // column-major (kl x n) view of L^T
   // A1 = L^T V (k x t)
-  DevBuf A1, A2;
+  DevBuf A1, A2, tr;
   A1.alloc(sizeof(double) * (size_t)k * t);
   A2.alloc(sizeof(double) * (size_t)k * t);
-  blas_ok(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, k, t, (int)n, &one, Pr.LF->L.as<double>(), kl, V, t, &zero,
-                      A1.as<double>(), k),
-          "A1");
+  tr.alloc(64);
+  gemm(false, true, k, t, (int)n, 1.0, Lp, kl, V, t, 0.0, A1.as<double>(), k);
   std::vector<double> a1((size_t)k * t), a2((size_t)k * t);
   VL_CUDA(cudaMemcpyAsync(a1.data(), A1.p, sizeof(double) * a1.size(), cudaMemcpyDeviceToHost, C.stream));
   // --- sigma2: dL = L / (2 sigma2): r = 2 (L^T v).(dL^T v) = (L^T v)^2 / sigma2 ;
   //     dPt = 2 tr(M^-1 L^T W L) / (2 sigma2) = (k - tr M^-1) / sigma2
-  DevBuf Minv, tr;
-  Minv.alloc(sizeof(double) * (size_t)k * k);
-  tr.alloc(64);
-  {
-    std::vector<double> I((size_t)k * k, 0.0);
-    for (int i = 0; i < k; ++i) I[(size_t)i * k + i] = 1.0;
-    VL_CUDA(cudaMemcpyAsync(Minv.p, I.data(), sizeof(double) * I.size(), cudaMemcpyHostToDevice, C.stream));
-    blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, k, k, &one,
-                        Pr.Lm.as<double>(), k, Minv.as<double>(), k),
-            "minv1");
-    blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, k, k, &one,
-                        Pr.Lm.as<double>(), k, Minv.as<double>(), k),
-            "minv2");
-    diag_sum_kernel<<<1, 256, 0, C.stream>>>(k, Minv.as<double>(), tr.as<double>());
-  }
+  const double* Minv = Pr.Minv.as<double>();
+  diag_sum_kernel<<<1, 256, 0, C.stream>>>(k, Minv, tr.as<double>());
   double trMinv = 0.0;
   VL_CUDA(cudaMemcpyAsync(&trMinv, tr.p, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
   VL_CUDA(cudaStreamSynchronize(C.stream));
@@ -1242,57 +1243,38 @@ void lrac_grad_columns(Ctx& C, const LracPrec& Pr, int t, const double* U, const
   dPt[0] = ((double)k - trMinv) / Pr.F->sigma2;
   // --- rho: dL = (dS - L dR^T) R^-T, dR = R Phi(R^-1 dS_pp R^-T), R = L[piv]
   const MaternK Km = make_matern(F);
-  DevBuf dS, R, X, dR;
+  DevBuf dS, dL, R, Ri, X, X1, dR;
   dS.alloc(sizeof(double) * (size_t)n * kl);
+  dL.alloc(sizeof(double) * (size_t)n * kl);
   R.alloc(sizeof(double) * (size_t)k * k);
+  Ri.alloc(sizeof(double) * (size_t)k * k);
   X.alloc(sizeof(double) * (size_t)k * k);
+  X1.alloc(sizeof(double) * (size_t)k * k);
   dR.alloc(sizeof(double) * (size_t)k * k);
   dsigma_kernel<<<C.num_sms * 8, 256, 0, C.stream>>>(n, P.d, k, kl, P.xy.as<double>(), Pr.LF->piv_s.as<int32_t>(), Km,
                                                      dS.as<double>());
-  gather_piv_rows_kernel<<<64, 256, 0, C.stream>>>(k, kl, Pr.LF->piv_s.as<int32_t>(), Pr.LF->L.as<double>(),
-                                                   R.as<double>());
+  gather_piv_rows_kernel<<<64, 256, 0, C.stream>>>(k, kl, Pr.LF->piv_s.as<int32_t>(), Lp, R.as<double>());
   gather_piv_rows_kernel<<<64, 256, 0, C.stream>>>(k, kl, Pr.LF->piv_s.as<int32_t>(), dS.as<double>(), X.as<double>());
   VL_LAUNCH_CHECK();
-  // X = R^-1 dSpp R^-T
-  blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, k, k, &one,
-                      R.as<double>(), k, X.as<double>(), k),
-          "X1");
-  blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, k, k, &one,
-                      R.as<double>(), k, X.as<double>(), k),
-          "X2");
+  dtrtri_lower(C, k, R.as<double>(), k, Ri.as<double>(), k);
+  // X = R^-1 dS_pp R^-T, then Phi(X) in place
+  gemm(false, false, k, k, k, 1.0, Ri.as<double>(), k, X.as<double>(), k, 0.0, X1.as<double>(), k);
+  gemm(false, true, k, k, k, 1.0, X1.as<double>(), k, Ri.as<double>(), k, 0.0, X.as<double>(), k);
   phi_kernel<<<64, 256, 0, C.stream>>>(k, X.as<double>());
+  VL_LAUNCH_CHECK();
   // dR = R Phi
-  blas_ok(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, k, k, k, &one, R.as<double>(), k, X.as<double>(), k, &zero,
-                      dR.as<double>(), k),
-          "dR");
-  // dL^T (k x n col-major view of row-major dL) = R^-1 (dS^T - dR L^T) : work on the (kl x n) views
-  // dS^T - dR L^T  ->  dS view (k x n, ld kl) -= dR (k x k) * L view (k x n, ld kl)
-  blas_ok(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, k, (int)n, k, &mone, dR.as<double>(), k, Pr.LF->L.as<double>(), kl,
-                      &one, dS.as<double>(), kl),
-          "dS - dR L^T");
-  blas_ok(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, k, (int)n, &one,
-                      R.as<double>(), k, dS.as<double>(), kl),
-          "dL");
-  // now dS holds dL (row-major n x k, ld kl).  A2 = dL^T V
-  blas_ok(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, k, t, (int)n, &one, dS.as<double>(), kl, V, t, &zero,
-                      A2.as<double>(), k),
-          "A2");
-  // T1 = L^T (W o dL) (k x k): scale dL rows by W into scr-sized buffer, GEMM
-  DevBuf WdL, T1, MT;
-  WdL.alloc(sizeof(double) * (size_t)n * kl);
+  gemm(false, false, k, k, k, 1.0, R.as<double>(), k, X.as<double>(), k, 0.0, dR.as<double>(), k);
+  // dL^T (k x n view, ld kl) = R^-1 (dS^T - dR L^T)
+  gemm(false, false, k, (int)n, k, -1.0, dR.as<double>(), k, Lp, kl, 1.0, dS.as<double>(), kl);
+  gemm(false, false, k, (int)n, k, 1.0, Ri.as<double>(), k, dS.as<double>(), kl, 0.0, dL.as<double>(), kl);
+  // A2 = dL^T V
+  gemm(false, true, k, t, (int)n, 1.0, dL.as<double>(), kl, V, t, 0.0, A2.as<double>(), k);
+  // T1 = L^T diag(W) dL (k x k), MT = M^-1 T1 -> tr(M^-1 T1)
+  DevBuf T1, MT;
   T1.alloc(sizeof(double) * (size_t)k * k);
   MT.alloc(sizeof(double) * (size_t)k * k);
-  // W o dL = sqrt(W) o (sqrt(W) o dL)   (W > 0 is guaranteed for LRAC)
-  scale_rows_kernel<<<C.num_sms * 8, 256, 0, C.stream>>>(n, kl, Pr.W, dS.as<double>(), WdL.as<double>());
-  scale_rows_kernel<<<C.num_sms * 8, 256, 0, C.stream>>>(n, kl, Pr.W, WdL.as<double>(), WdL.as<double>());
-  // T1 (k x k) = Lv (k x n) * WdLv^T (n x k)
-  blas_ok(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_T, k, k, (int)n, &one, Pr.LF->L.as<double>(), kl, WdL.as<double>(), kl,
-                      &zero, T1.as<double>(), k),
-          "T1");
-  // tr(M^-1 T1) = sum_ij Minv_ij T1_ji
-  blas_ok(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, k, k, k, &one, Minv.as<double>(), k, T1.as<double>(), k, &zero,
-                      MT.as<double>(), k),
-          "MT");
+  gemm(false, true, k, k, (int)n, 1.0, Lp, kl, dL.as<double>(), kl, 0.0, T1.as<double>(), k, Pr.W);
+  gemm(false, false, k, k, k, 1.0, Minv, k, T1.as<double>(), k, 0.0, MT.as<double>(), k);
   diag_sum_kernel<<<1, 256, 0, C.stream>>>(k, MT.as<double>(), tr.as<double>());
   double trMT = 0.0;
   VL_CUDA(cudaMemcpyAsync(&trMT, tr.p, sizeof(double), cudaMemcpyDeviceToHost, C.stream));
@@ -1503,6 +1485,88 @@ struct DX2Body {  // acc[c] += D_s X_sc^2
 
 }  // namespace
 
+namespace {
+// Deterministic device argmax over storage rows: largest v[s], ties to the
+// lowest factor index fidx[s] (the reference's argmax / lexsort tie rule);
+// pass 1 per block, pass 2 one block over the block winners.
+constexpr int kAmThreads = 256;
+VL_D bool am_better(double va, int32_t fa, double vb, int32_t fb) { return va > vb || (va == vb && fa < fb); }
+
+__global__ void __launch_bounds__(kAmThreads) argmax_pass1(int64_t n, const double* __restrict__ v,
+                                                           const int32_t* __restrict__ fidx, double* __restrict__ bv,
+                                                           int32_t* __restrict__ bsr) {
+  __shared__ double sv[kAmThreads];
+  __shared__ int32_t sf[kAmThreads], ss[kAmThreads];
+  double best = -INFINITY;
+  int32_t bf = INT32_MAX, bs = -1;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const double x = v[r];
+    const int32_t f = fidx[r];
+    if (bs < 0 || am_better(x, f, best, bf)) { best = x; bf = f; bs = (int32_t)r; }
+  }
+  sv[threadIdx.x] = best; sf[threadIdx.x] = bf; ss[threadIdx.x] = bs;
+  __syncthreads();
+  for (int o = kAmThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const int q = threadIdx.x + o;
+      if (ss[q] >= 0 && (ss[threadIdx.x] < 0 || am_better(sv[q], sf[q], sv[threadIdx.x], sf[threadIdx.x]))) {
+        sv[threadIdx.x] = sv[q]; sf[threadIdx.x] = sf[q]; ss[threadIdx.x] = ss[q];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { bv[blockIdx.x] = sv[0]; bsr[blockIdx.x] = ss[0]; }
+}
+
+// pass 2: winner -> out_s / out_v (pivoted-Cholesky state: i[0] = row, i[1..3] = 0);
+// with knock_out, v[winner] = -inf (the next round of a top-k selection)
+__global__ void __launch_bounds__(kAmThreads) argmax_pass2(int nb, const double* __restrict__ bv,
+                                                           const int32_t* __restrict__ bsr,
+                                                           const int32_t* __restrict__ fidx, int* out_i,
+                                                           double* out_v, int32_t* sel_f, int32_t* sel_s, int slot,
+                                                           double* knock_out) {
+  __shared__ double sv[kAmThreads];
+  __shared__ int32_t sf[kAmThreads], ss[kAmThreads];
+  double best = -INFINITY;
+  int32_t bf = INT32_MAX, bs = -1;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    const int32_t r = bsr[b];
+    if (r < 0) continue;
+    const int32_t f = fidx[r];
+    if (bs < 0 || am_better(bv[b], f, best, bf)) { best = bv[b]; bf = f; bs = r; }
+  }
+  sv[threadIdx.x] = best; sf[threadIdx.x] = bf; ss[threadIdx.x] = bs;
+  __syncthreads();
+  for (int o = kAmThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const int q = threadIdx.x + o;
+      if (ss[q] >= 0 && (ss[threadIdx.x] < 0 || am_better(sv[q], sf[q], sv[threadIdx.x], sf[threadIdx.x]))) {
+        sv[threadIdx.x] = sv[q]; sf[threadIdx.x] = sf[q]; ss[threadIdx.x] = ss[q];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (out_i) { out_i[0] = ss[0]; out_i[1] = out_i[2] = out_i[3] = 0; }
+    if (out_v) *out_v = sv[0];
+    if (sel_f) { sel_f[slot] = sf[0]; sel_s[slot] = ss[0]; }
+    if (knock_out && ss[0] >= 0) knock_out[ss[0]] = -INFINITY;
+  }
+}
+
+void device_argmax(Ctx& C, int64_t n, double* v, const int32_t* fidx, DevBuf& scratch, int* out_i, double* out_v,
+                   int32_t* sel_f, int32_t* sel_s, int slot, bool knock_out) {
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(4LL * C.num_sms, (n + kAmThreads - 1) / kAmThreads));
+  scratch.alloc((sizeof(double) + sizeof(int32_t)) * nb);
+  double* bv = scratch.as<double>();
+  int32_t* bsr = reinterpret_cast<int32_t*>(bv + nb);
+  argmax_pass1<<<nb, kAmThreads, 0, C.stream>>>(n, v, fidx, bv, bsr);
+  argmax_pass2<<<1, kAmThreads, 0, C.stream>>>(nb, bv, bsr, fidx, out_i, out_v, sel_f, sel_s, slot,
+                                               knock_out ? v : nullptr);
+  VL_LAUNCH_CHECK();
+}
+}  // namespace
+
 void pchol_precision(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol) {
   const Pattern& P = *F.pat;
   const int64_t n = P.n;
@@ -1525,18 +1589,11 @@ void pchol_precision(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol)
   part.alloc(sizeof(double) * 4 * (size_t)grid);
   BView Bv = bview(F, false);
   launch_rows<1, 1, 1, 0, 0>(C, n, 1, DiagQBody{Bv, F.D.as<double>(), d.as<double>()}, Fin0<0>{});
-  // first pivot: argmax of diag(Q), ties to the lowest factor index (preconditioners.py:311)
-  std::vector<double> dh(n);
-  VL_CUDA(cudaMemcpyAsync(dh.data(), d.p, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
-  VL_CUDA(cudaStreamSynchronize(C.stream));
-  int32_t bs = 0;
-  for (int64_t s = 1; s < n; ++s)
-    if (dh[s] > dh[bs] || (dh[s] == dh[bs] && P.sperm[s] < P.sperm[bs])) bs = (int32_t)s;
-  int h_i[4] = {bs, 0, 0, 0};
-  double h_dp = dh[bs];
-  VL_CUDA(cudaMemcpyAsync(st.p, h_i, sizeof(h_i), cudaMemcpyHostToDevice, C.stream));
-  VL_CUDA(cudaMemcpyAsync(st.as<char>() + 32, &h_dp, sizeof(double), cudaMemcpyHostToDevice, C.stream));
+  // first pivot: argmax of diag(Q), ties to the lowest factor index (preconditioners.py:311), on the device
   PcState S{st.as<int>(), reinterpret_cast<double*>(st.as<char>() + 32)};
+  DevBuf amw;
+  device_argmax(C, n, d.as<double>(), P.fidx.as<int32_t>(), amw, S.i, S.dp, nullptr, nullptr, 0, false);
+  int h_i[4] = {0, 0, 0, 0};
   const MaternK K = make_matern(F);
   unsigned* counter = next_counter(C);
   ProfScope ps(C, "pchol_precision", 0.0);
@@ -1569,16 +1626,18 @@ void rowsel_factor(Ctx& C, const Factor& F, LracFactor& LF, int k) {
   DevBuf sc;
   sc.alloc(sizeof(double) * n);
   launch_rows<1, 1, 1, 0, 0>(C, n, 1, RowScoreBody{bview(F, false), F.D.as<double>(), sc.as<double>()}, Fin0<0>{});
-  std::vector<double> sh(n);
-  VL_CUDA(cudaMemcpyAsync(sh.data(), sc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, C.stream));
+  // top-k of the scores with lexsort((arange, -scores)) semantics -- descending score, ties to
+  // the lower factor index -- as k device argmax rounds (each knocks its winner out); only the
+  // k winners come back to the host
+  DevBuf amw, selb;
+  selb.alloc(sizeof(int32_t) * 2 * (size_t)k);
+  int32_t* sel_f = selb.as<int32_t>();
+  int32_t* sel_s = sel_f + k;
+  for (int c = 0; c < k; ++c)
+    device_argmax(C, n, sc.as<double>(), P.fidx.as<int32_t>(), amw, nullptr, nullptr, sel_f, sel_s, c, true);
+  std::vector<int32_t> sel(k);
+  VL_CUDA(cudaMemcpyAsync(sel.data(), sel_f, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, C.stream));
   VL_CUDA(cudaStreamSynchronize(C.stream));
-  // scores in factor order; lexsort((arange, -scores)): descending score, ties to the lower index
-  std::vector<double> sf(n);
-  for (int64_t s = 0; s < n; ++s) sf[P.sperm[s]] = sh[s];
-  std::vector<int32_t> ord(n);
-  for (int64_t i = 0; i < n; ++i) ord[i] = (int32_t)i;
-  std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return sf[a] > sf[b]; });
-  std::vector<int32_t> sel(ord.begin(), ord.begin() + k);
   std::sort(sel.begin(), sel.end());  // S_k ascending (preconditioners.py:375)
   std::vector<int32_t> rows(k);
   for (int c = 0; c < k; ++c) rows[c] = P.iperm[sel[c]];

@@ -31,6 +31,8 @@ struct LracPrec {
   const double* Wop = nullptr;  // operator W
   int eq6 = 0;
   DevBuf Lm;                // k x k column-major lower Cholesky factor of M
+  DevBuf Lmi;               // Lm^-1 (k x k, column-major, lower)
+  DevBuf Minv;              // M^-1 = Lm^-T Lm^-1 (k x k, column-major, symmetric)
   DevBuf own;               // owned 1/e buffer when computed here
   LracFactor empty;         // k = 0 factor for the diagonal-only (l2) form
   double logdetM = 0.0;

@@ -7,7 +7,7 @@
 //             (multi-RHS PCG, one column per sample), z4 = Bpo u,
 //             acc += z4^2 in sample order (and the full n_p x n_p second
 //             moment with a rank-c update when requested).
-#include <cublas_v2.h>
+#include "dense.h"
 
 #include "bodies.cuh"
 #include "launch.cuh"
@@ -115,13 +115,6 @@ __global__ void accum_sq_kernel(int64_t np, int c, const double* __restrict__ Z,
   }
 }
 
-cublasHandle_t g_pblas[16] = {};
-cublasHandle_t pblas(Ctx& C) {
-  cublasHandle_t& h = g_pblas[C.device & 15];
-  if (!h && cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) fail(kECuda, "cublasCreate failed");
-  cublasSetStream(h, C.stream);
-  return h;
-}
 
 }  // namespace
 
@@ -187,10 +180,14 @@ void pred_accum(Ctx& C, const PredBlocks& B, const double* U_dev, int c, double*
   VL_LAUNCH_CHECK();
   if (cov_dev) {
     // cov (np x np, symmetric, both triangles) += Z Z^T ; Z row-major np x c == column-major c x np
-    const double one = 1.0;
-    if (cublasDgemm(pblas(C), CUBLAS_OP_T, CUBLAS_OP_N, (int)B.np, (int)B.np, c, &one, Z.as<double>(), c,
-                    Z.as<double>(), c, &one, cov_dev, (int)B.np) != CUBLAS_STATUS_SUCCESS)
-      fail(kECuda, "cuBLAS failure in the predictive second moment");
+    Gemm g;
+    g.ta = true;
+    g.m = (int)B.np; g.n = (int)B.np; g.k = c;
+    g.A = Z.as<double>(); g.lda = c;
+    g.B = Z.as<double>(); g.ldb = c;
+    g.beta = 1.0;
+    g.C = cov_dev; g.ldc = (int)B.np;
+    dgemm(C, g);
   }
 }
 

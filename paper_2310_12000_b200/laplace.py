@@ -443,21 +443,54 @@ def make_probes(factor, state, cfg, cols=None):
     return ps, P
 
 
-def probes_from_Z(factor, state, cfg, Z):
-    """Inject caller-supplied probes (e.g. Rademacher): psolves are
-    computed with the full VADU solve P^-1 Z = B^-1 d^-1 B^-T Z."""
+def _given_probes(factor, state, cfg, Zd, seed, cols):
     P = build_preconditioner(factor, state._dev["W"], cfg)
-    Z = np.asarray(Z, dtype=float)
-    Zd = factor.pattern.to_dev(Z)
-    n, t = Z.shape
-    dinv = factor.pattern.from_dev(P.dinv)  # factor order, (n, 1)
-    if P.pkind == 0:  # P^-1 Z = B^-1 (B^-T Z / d)
-        V = factor.solve_B(factor.solve_B(Z, transpose=True) * dinv)
-    else:
-        V = Z * dinv
-    Vd = factor.pattern.to_dev(V)
-    w = np.einsum("it,it->t", Z, V)
-    return ProbeSet(Zd, cfg.probe_seed, P.name, pattern=factor.pattern, psolves_dev=Vd, weights=w), P
+    if cfg.preconditioner in LOWRANK_VARIANTS:
+        raise CapabilityError("caller-supplied probes are implemented for the eq6 (vadu-family) preconditioners")
+    t = int(Zd.shape[1])
+    V = dev.empty(factor.ctx, factor.n, t)
+    w = np.zeros(t)
+    _lib.call("vl_probes_given", factor.ctx.h, factor.h, _lib.ptr(P.dinv), P.pkind, t, _lib.ptr(Zd), _lib.ptr(V),
+              _lib.ptr(w))
+    shard = (0 if cols is None else cols[0], cfg.t if cols is not None else t)
+    return ProbeSet(Zd, seed, P.name, pattern=factor.pattern, psolves_dev=V, weights=w, shard=shard), P
+
+
+def probes_from_Z(factor, state, cfg, Z):
+    """Inject caller-supplied probes (the reference's ``ProbeSet(Z, seed,
+    P.name)`` passed to neg_marginal_loglik / gradient, laplace.py:340, 439;
+    e.g. Rademacher probes).  Z is (n, t) in factor order; it is
+    uploaded once and P^-1 Z and the SLQ weights z^T P^-1 z are formed on
+    the device (two triangular solves, weights fused)."""
+    Z = np.ascontiguousarray(np.asarray(Z, dtype=float))
+    if Z.ndim != 2 or Z.shape[0] != factor.n:
+        raise ConfigError(f"probes must have shape (n, t) with n = {factor.n}")
+    return _given_probes(factor, state, cfg, factor.pattern.to_dev(Z), cfg.probe_seed, None)
+
+
+def rademacher_probes(factor, state, cfg, seed=None, cols=None):
+    """Probes with the preconditioner's covariance built from Rademacher base
+    draws instead of Gaussian ones: Z = B^T (sqrt(d) o R) for the
+    VADU-family sandwich (sqrt(d) o R for diagonal P), the same construction
+    as sample_block (preconditioners.py:121-122) with R in place of G.  R is
+    drawn on the device: entry (factor row i, column c) is -1 or +1 by the top
+    bit of splitmix64(seed * 0x9E3779B97F4A7C15 + i * t + c); ``cols`` selects
+    a column shard.  P^-1 Z and the SLQ weights follow as in make_probes."""
+    if cfg.preconditioner in LOWRANK_VARIANTS:
+        raise CapabilityError("Rademacher probes are implemented for the eq6 (vadu-family) preconditioners")
+    seed = cfg.probe_seed if seed is None else int(seed)
+    c0, c1 = (0, cfg.t) if cols is None else cols
+    t = c1 - c0
+    P = build_preconditioner(factor, state._dev["W"], cfg)
+    R = dev.empty(factor.ctx, factor.n, t)
+    _lib.call("vl_probes_rademacher", factor.ctx.h, factor.pattern.h, t, cfg.t, c0, seed & 0xFFFFFFFFFFFFFFFF,
+              _lib.ptr(R))
+    Z = dev.empty(factor.ctx, factor.n, t)
+    V = dev.empty(factor.ctx, factor.n, t)
+    w = np.zeros(t)
+    _lib.call("vl_probes_eq6", factor.ctx.h, factor.h, _lib.ptr(P.dinv), P.pkind, t, _lib.ptr(R), _lib.ptr(Z),
+              _lib.ptr(V), _lib.ptr(w))
+    return ProbeSet(Z, seed, P.name, pattern=factor.pattern, psolves_dev=V, weights=w, shard=(c0, cfg.t)), P
 
 
 def _run_probe_solves(factor, state, P, cfg, probes):

@@ -286,11 +286,49 @@ def replay():
     print("replay", json.dumps({k: out[k] for k in ("nll", "dtheta", "newton_iters", "probe_cg")}))
 
 
+def rademacher_case():
+    """The reference's ProbeSet injection (laplace.py:340) with probes built from
+    Rademacher base draws R (tests/golden/rademacher.py) on the logit_vadu_n1500
+    dataset: Z = B^T (sqrt(d) o R), the sample_block construction
+    (preconditioners.py:121-122) with R for the Gaussian draws.  vadu (d = W + 1/D)
+    and lva (d = 1/D).  With R_i^2 = 1 the VADU per-row control variate divides
+    rounding noise by rounding noise (Var_t((BV)_i^2) = Var_t(1 / d_i) = 0), so only
+    its NLL is a meaningful comparison; lva's plain estimator gives the gradient."""
+    from vlgp.covariance import CovarianceSpec
+    from vlgp.iterative import ProbeSet
+    from vlgp.laplace import BackendConfig, build_preconditioner, find_mode, gradient, neg_marginal_loglik
+    from vlgp.likelihoods import get_likelihood
+    from vlgp.vecchia import build_factor
+    sys.path.insert(0, HERE)
+    from rademacher import rademacher
+    g = np.load(os.path.join(HERE, "logit_vadu_n1500.npz"))
+    n, t, seed = int(g["n"]), 16, 4242
+    nb = [r[r >= 0].astype(int) for r in g["nbr"]]
+    f = build_factor(g["coords"], CovarianceSpec(float(g["sigma2"]), float(g["rho"]), float(g["nu"])), nb, g["perm"])
+    lik = get_likelihood("bernoulli-logit")
+    R = rademacher(n, t, seed)
+    out, arrays = {"case": "logit_vadu_n1500", "t": t, "seed": seed}, {}
+    for pc in ("vadu", "lva"):
+        cfg = BackendConfig(preconditioner=pc, t=t, probe_seed=seed)
+        st = find_mode(f, lik, g["y"][g["perm"]], g["F"][g["perm"]], cfg)
+        P = build_preconditioner(f, st.W, cfg)
+        d = st.W + 1.0 / f.D if pc == "vadu" else 1.0 / f.D
+        Z = f.B.T @ (np.sqrt(d)[:, None] * R)
+        pr = ProbeSet(Z, seed, P.name)
+        nll = neg_marginal_loglik(st, f, cfg, probes=pr, P=P)
+        gr = gradient(st, f, lik, np.zeros((n, 0)), cfg, probes=pr, P=P)
+        out[pc] = dict(nll=float(nll), dtheta=[float(v) for v in gr["dtheta"]],
+                       probe_cg=[int(tr.order) for tr in pr.tridiags])
+        arrays[f"Z_{pc}"] = Z
+    np.savez_compressed(os.path.join(HERE, "rademacher_n1500.npz"), meta=json.dumps(out), **arrays)
+    print("rademacher", json.dumps(out)[:400])
+
+
 def main():
     _ref()
     for job in sys.argv[1:]:
         {"data3": data3, "c3": c3, "c3mode6": c3mode6, "c1": c1, "c2": c2,
-         "c2lrac": lambda: c2("lrac"), "replay": replay}[job]()
+         "c2lrac": lambda: c2("lrac"), "replay": replay, "rademacher": rademacher_case}[job]()
 
 
 if __name__ == "__main__":
