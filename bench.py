@@ -49,6 +49,7 @@ def parse():
     # fp64 resolution of the Newton gradient d1 - Q b is ~eps*||Q||_inf*|b| ~ 6e-6 at
     # n=1e6, rho=0.02 (D_min ~ 3e-10): the reference default 1e-6 is unattainable there
     ap.add_argument("--newton-grad-tol", type=float, default=1e-5)
+    ap.add_argument("--no-c4", action="store_true", help="skip the config-4 prediction side measurement")
     ap.add_argument("--ref-budget-s", type=float, default=1500.0,
                     help="--impl reference: stop timing further evaluations past this many seconds")
     return ap.parse_args()
@@ -287,6 +288,47 @@ def reference_arm(a, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def config4_prediction(s=1000, n=500_000, n_p=500_000, rho=0.05, m=20, seed=4):
+    """BASELINE configs[3] on one GPU, reported beside the headline line:
+    500k training + 500k prediction points, Poisson-log, Matern 1.5, rho 0.05,
+    VADU mode, prediction blocks, latent mean and s = 1000 simulation samples
+    for the predictive variances (predict.py:70-101; device normals).  Times
+    are CUDA-event device times of the prediction stages (mode excluded)."""
+    import torch
+
+    import paper_2310_12000_b200 as vg
+    from paper_2310_12000_b200.vecchia import build_factor, neighbor_array
+    rng = np.random.default_rng(seed)
+    N = n + n_p
+    xy = rng.uniform(size=(N, 2))
+    spec = vg.CovarianceSpec(1.0, rho, 1.5)
+    permS = vg.order_random(N, seed + 95)
+    fS = build_factor(xy, spec, neighbor_array(xy, permS, 30), permS, want_grad=False)
+    latent = np.empty(N)
+    latent[permS] = fS.solve_B(np.sqrt(fS.D) * rng.standard_normal(N))
+    lik = vg.get_likelihood("poisson")
+    y = lik.sample(latent[:n], rng)
+    perm = vg.order_random(n, seed + 3)
+    f = build_factor(xy[:n], spec, neighbor_array(xy[:n], perm, m), perm, want_grad=False)
+    cfg = vg.BackendConfig(preconditioner="vadu", t=50, cg_tol=1e-3)
+    st = vg.find_mode(f, lik, y[perm], np.zeros(n), cfg)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    torch.cuda.synchronize()
+    ev[0].record()
+    blocks = vg.prediction_blocks(f, xy[n:])
+    omega = vg.latent_mean(st, blocks, np.zeros(n_p))
+    ev[1].record()
+    var = vg.latent_var_sim(st, f, blocks, s=s, seed=seed + 1, cfg=cfg, rng="device")
+    ev[2].record()
+    torch.cuda.synchronize()
+    t_mean, t_var = ev[0].elapsed_time(ev[1]) / 1e3, ev[1].elapsed_time(ev[2]) / 1e3
+    return {"workload": f"predict_n{n}_np{n_p}_s{s}", "likelihood": "poisson", "rho": rho, "m": m,
+            "blocks_mean_s": round(t_mean, 4), "var_sim_s": round(t_var, 4),
+            "samples_per_s": round(s / t_var, 2), "predictions_per_s": round(n_p / (t_mean + t_var), 1),
+            "rmse_latent": float(np.sqrt(np.mean((omega - latent[n:]) ** 2))), "mean_var": float(var.mean()),
+            "newton_iters": int(st.newton_iters)}
+
+
 def spawn_ranks(a):
     """--gpus N without a torchrun environment: re-launch under torch.distributed.run."""
     import socket
@@ -479,6 +521,12 @@ def main():
                              "evaluations: --impl reference)", "details": det}
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
+    c4 = None
+    if rank == 0 and world == 1 and not a.no_c4:
+        try:
+            c4 = config4_prediction()
+        except Exception as exc:  # pragma: no cover
+            c4 = {"failed": f"{type(exc).__name__}: {exc}"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong",
@@ -490,7 +538,7 @@ def main():
                 "phase_ms": {k: round(v, 3) for k, v in phase_ms.items()},
                 "phases": {"replicated": ["factor", "mode"], "probe_sharded": ["probes_nll", "gradient"],
                            "note": "gradient includes the replicated single-RHS tvec solve"},
-                "iterations": counts, "kernels": tags}
+                "iterations": counts, "config4_prediction": c4, "kernels": tags}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
