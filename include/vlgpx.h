@@ -319,6 +319,18 @@ int vl_pred_mean(vl_ctx* ctx, const vl_pred* b, const double* b_dev, const doubl
 int vl_pred_z3(vl_ctx* ctx, const vl_factor* f, const double* W_dev, int64_t c, const double* z1_dev,
                const double* z2_dev, double* z3_dev);
 int vl_pred_accum(vl_ctx* ctx, const vl_pred* b, const double* U_dev, int64_t c, double* acc_dev, double* cov_dev);
+/* vl_pred_lanczos: rank-k Lanczos approximation of diag(Omega_p) (predict.py:104-172
+ * latent_var_lanczos / _lanczos_correction, iterative.py:181-219 lanczos_partial).
+ * variant 0 "none", 1 "l1", 2 "l2" (needs W > 0: status 5, and dsig_dev =
+ * diag(SigmaTilde), n).  start_dev (n, storage order) = the column mean of
+ * RT = Bpo^T, i.e. (1/np) Bpo^T 1; the variant's transformation of RT is applied
+ * by the library.  RT is never materialised densely: S = Q^T RT is formed as
+ * Bpo Q' over the transformed Lanczos basis, O((n + np) k) memory.  var_dev (np)
+ * receives Dp + correction; *achieved = Krylov order reached (k unless a
+ * recurrence norm fell below breakdown_tol; 0 = zero start vector, var = Dp). */
+int vl_pred_lanczos(vl_ctx* ctx, const vl_factor* f, const vl_pred* b, const double* W_dev, int variant, int64_t k,
+                    const double* start_dev, const double* dsig_dev, double breakdown_tol, double* var_dev,
+                    int* achieved);
 
 /* ---- dense fp64 kernels of the low-rank paths (debug / test entry points) ----
  * Column-major, BLAS argument meaning: C = alpha op(A) [diag(kw)] op(B) + beta C with

@@ -163,6 +163,8 @@ _SIGS.update({
     "vl_pred_mean": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "vl_pred_z3": [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p],
     "vl_pred_accum": [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p],
+    "vl_pred_lanczos": [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int64, c_void_p, c_void_p, c_double,
+                        c_void_p, c_void_p],
     "vl_find_mode_lrac": [c_void_p, c_void_p, c_void_p, C.POINTER(VlLik), C.POINTER(VlNewtonCfg), c_void_p, c_void_p,
                           c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int],
 })

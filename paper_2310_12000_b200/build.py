@@ -35,11 +35,26 @@ def sources():
     return sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
 
 
+def _includes(path, seen):
+    """Transitive quoted includes of a source file (csrc/ and include/)."""
+    if path in seen or not os.path.exists(path):
+        return
+    seen.add(path)
+    with open(path) as fh:
+        for line in fh:
+            line = line.strip()
+            if line.startswith("#include \""):
+                name = line.split('"')[1]
+                for base in (CSRC, os.path.join(HERE, "..", "include")):
+                    _includes(os.path.join(base, name), seen)
+
+
 def _compile(src, verbose_ptxas=False, defines=(), out_dir=OUT_DIR):
     obj = os.path.join(out_dir, src + ".o")
     path = os.path.join(CSRC, src)
-    deps = [path] + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))]
-    deps.append(os.path.join(HERE, "..", "include", "vlgpx.h"))
+    deps = set()
+    _includes(path, deps)
+    deps = sorted(deps)
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj, ""
     cmd = [nvcc(), *ARCH, *COMMON, *[f"-D{d}" for d in defines], "-c", path, "-o", obj]

@@ -1021,4 +1021,15 @@ int vl_pred_accum(vl_ctx* h, const vl_pred* b, const double* U_dev, int64_t c, d
   return guard_dev(h, [&] { pred_accum(h->c, b->b, U_dev, (int)c, acc_dev, cov_dev); });
 }
 
+int vl_pred_lanczos(vl_ctx* h, const vl_factor* f, const vl_pred* b, const double* W_dev, int variant, int64_t k,
+                    const double* start_dev, const double* dsig_dev, double breakdown_tol, double* var_dev,
+                    int* achieved) {
+  return guard_dev(h, [&] {
+    if (!h || !f || !b || !W_dev || !start_dev || !achieved || (b->b.np > 0 && !var_dev))
+      fail(kEConfig, "null pointer");
+    if (k > (int64_t)1 << 20) fail(kECapacity, "Lanczos rank too large");
+    *achieved = pred_lanczos(h->c, f->f, b->b, W_dev, variant, (int)k, start_dev, dsig_dev, breakdown_tol, var_dev);
+  });
+}
+
 }  // extern "C"

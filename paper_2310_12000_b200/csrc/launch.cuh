@@ -19,6 +19,9 @@ using IC = std::integral_constant<int, V>;
 //   U  = 2 (16-byte units) when ld is even and t > 1, else 1
 //   G  = lanes per row = min(32, pow2ceil(#units))
 //   NU = units per lane
+#ifndef VL_G16
+#define VL_G16 0
+#endif
 template <class F>
 void dispatch_cols(int t, int ld, F&& f) {
   if (t <= 0 || ld < t) fail(kEConfig, "invalid column count / leading dimension");
@@ -31,7 +34,11 @@ void dispatch_cols(int t, int ld, F&& f) {
     else if (units <= 4) f(IC<4>{}, IC<1>{}, IC<U>{});
     else if (units <= 8) f(IC<8>{}, IC<1>{}, IC<U>{});
     else if (units <= 16) f(IC<16>{}, IC<1>{}, IC<U>{});
+#if VL_G16
+    else if (units <= 32) f(IC<16>{}, IC<2>{}, IC<U>{});   // two rows per warp, two units per lane
+#else
     else if (units <= 32) f(IC<32>{}, IC<1>{}, IC<U>{});
+#endif
     else if (units <= 64) f(IC<32>{}, IC<2>{}, IC<U>{});
     else fail(kECapacity, "more than 128 right-hand sides per call are not supported; shard the probes");
   };

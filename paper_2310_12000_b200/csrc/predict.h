@@ -21,5 +21,8 @@ void pred_create(Ctx& C, const Pattern& P, double sigma2, double rho, double nu,
 void pred_mean(Ctx& C, const PredBlocks& B, const double* b_dev, const double* Fp_dev, double* omega_dev);
 void pred_z3(Ctx& C, const Factor& F, const double* W, int c, const double* z1, const double* z2, double* z3);
 void pred_accum(Ctx& C, const PredBlocks& B, const double* U_dev, int c, double* acc_dev, double* cov_dev);
+// Rank-k Lanczos variances (lanczos.cu); returns the achieved rank (0: zero start vector).
+int pred_lanczos(Ctx& C, const Factor& F, const PredBlocks& B, const double* W, int variant, int k,
+                 const double* start_raw, const double* dsig, double breakdown_tol, double* var_out);
 
 }  // namespace vl

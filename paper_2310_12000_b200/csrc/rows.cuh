@@ -535,6 +535,30 @@ VL_D void trsv_row(int64_t p, int64_t pend_, int t, int ld, const int32_t* __res
 // the slowest row of the warp.  Without this, a row of level l+1 effectively
 // waits for the slowest of ~32 x deg rows of level l (a per-level barrier with
 // tail latency); with it, each row waits only for its own dependencies.
+// xs -= sum_q w[q] v[q] over one batch.  VL_TREE_SUM = 0: the entries in order
+// (one dependent fma chain of B); 1: four interleaved partial sums folded
+// pairwise (chain of B/4 + 2), a fixed order as well.
+#ifndef VL_TREE_SUM
+#define VL_TREE_SUM 0
+#endif
+template <int B>
+VL_D void fold_batch(const double (&w)[B], const double (&v)[B], double& xs) {
+#if VL_TREE_SUM
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+  for (int q = 0; q < B; q += 4) {
+    a0 = fma(w[q], v[q], a0);
+    a1 = fma(w[q + 1], v[q + 1], a1);
+    a2 = fma(w[q + 2], v[q + 2], a2);
+    a3 = fma(w[q + 3], v[q + 3], a3);
+  }
+  xs -= (a0 + a1) + (a2 + a3);
+#else
+#pragma unroll
+  for (int q = 0; q < B; ++q) xs -= w[q] * v[q];
+#endif
+}
+
 #ifndef VL_POLL_ONE
 #define VL_POLL_ONE 0
 #endif
@@ -593,8 +617,7 @@ VL_D void trsv_row1(int64_t p, int64_t pend_, const int32_t* __restrict__ order,
       }
 #endif
       if (!pend) {
-#pragma unroll
-        for (int q = 0; q < B; ++q) xs -= w[q] * v[q];
+        fold_batch<B>(w, v, xs);
         const int eb = e0;
         e0 += B;
         if (e0 >= cs) {
@@ -741,8 +764,7 @@ VL_D void trsv_row1s(int64_t p, int64_t pend_, const int32_t* __restrict__ order
       }
 #endif
       if (!pend) {
-#pragma unroll
-        for (int q = 0; q < B; ++q) xs -= w[q] * v[q];
+        fold_batch<B>(w, v, xs);
         const int eb = e0;
         e0 += B;
         if (e0 >= wk) {

@@ -332,83 +332,12 @@ __all__ = ["PredictionBlocks", "PredictiveDistribution", "prediction_blocks", "l
 
 # ---------------------------------------------------------------------------
 # Rank-k Lanczos variances (predict.py:104-172, iterative.py:181-219).  The
-# reference materializes RT = Bpo^T densely (n x n_p), so these variants are
-# desk-scale there and here; the operators run on the device (library
-# SpMM / triangular-solve kernels), the dense Krylov basis and the small
-# tridiagonal solves through torch on the same device.
+# reference materializes RT = Bpo^T densely (n x n_p); the device path keeps RT
+# sparse and moves each variant's transformation of RT onto the k Lanczos
+# vectors (csrc/lanczos.cu), so config-4 sizes (5e5 x 5e5) fit.
 # ---------------------------------------------------------------------------
 LANCZOS_BREAKDOWN_TOL = 1e-12
-
-
-def _dapply(factor, name, arg, X):
-    """Device (storage order) n x t -> n x t through vl_spmm / vl_sptrsv, <= 128 columns per call."""
-    T = dev.torch()
-    out = T.empty_like(X)
-    for c0 in range(0, X.shape[1], 128):
-        blk = X[:, c0:c0 + 128].contiguous()
-        y = T.empty_like(blk)
-        _lib.call(name, factor.ctx.h, factor.h, arg, int(blk.shape[1]), _lib.ptr(blk), _lib.ptr(y))
-        out[:, c0:c0 + 128] = y
-    return out
-
-
-def _precision(factor, X, D):
-    return _dapply(factor, "vl_spmm", 1, _dapply(factor, "vl_spmm", 0, X) / D)
-
-
-def _sigma_tilde(factor, X, D):
-    return _dapply(factor, "vl_sptrsv", 0, _dapply(factor, "vl_sptrsv", 1, X) * D)
-
-
-def _lanczos_partial(matvec, start, k):
-    """iterative.py:181-219 on the device: full reorthogonalization (twice)."""
-    T = dev.torch()
-    n = start.shape[0]
-    norm0 = float(T.linalg.norm(start))
-    if norm0 == 0.0:
-        raise ConfigError("Lanczos start vector must be nonzero")
-    Q = T.zeros((n, k), dtype=T.float64, device=start.device)
-    alphas = np.empty(k)
-    betas = np.empty(max(k - 1, 0))
-    Q[:, 0] = start / norm0
-    achieved = k
-    for j in range(k):
-        w = matvec(Q[:, j:j + 1])[:, 0]
-        alphas[j] = float(Q[:, j] @ w)
-        w = w - alphas[j] * Q[:, j]
-        if j > 0:
-            w = w - betas[j - 1] * Q[:, j - 1]
-        for _ in range(2):
-            w = w - Q[:, :j + 1] @ (Q[:, :j + 1].T @ w)
-        if j == k - 1:
-            break
-        beta = float(T.linalg.norm(w))
-        if beta < LANCZOS_BREAKDOWN_TOL:
-            achieved = j + 1
-            break
-        betas[j] = beta
-        Q[:, j + 1] = w / beta
-    return Q[:, :achieved], alphas[:achieved], betas[:achieved - 1]
-
-
-def _lanczos_correction(matvec, RT_left, RT_right, k):
-    """diag(RT_left^T M^-1 RT_right) through one shared rank-k Krylov space (predict.py:104-123)."""
-    T = dev.torch()
-    start = RT_right.mean(dim=1)
-    if float(T.linalg.norm(start)) < LANCZOS_BREAKDOWN_TOL:
-        return np.zeros(RT_right.shape[1]), 0
-    Q, al, be = _lanczos_partial(matvec, start, k)
-    kk = Q.shape[1]
-    Td = np.diag(al)
-    if kk > 1:
-        Td += np.diag(be, 1) + np.diag(be, -1)
-    S_right = Q.T @ RT_right
-    X = T.linalg.solve(T.tensor(Td, dtype=T.float64, device=Q.device), S_right)
-    if RT_left is RT_right:
-        corr = (S_right * X).sum(dim=0)
-    else:
-        corr = ((Q.T @ RT_left) * X).sum(dim=0)
-    return corr.cpu().numpy(), kk
+_LANCZOS_VARIANTS = {"none": 0, "l1": 1, "l2": 2}
 
 
 def latent_var_lanczos(state, factor, blocks, k, variant="none", cfg=None):
@@ -416,46 +345,29 @@ def latent_var_lanczos(state, factor, blocks, k, variant="none", cfg=None):
     "none" factorizes W + SigmaTilde^-1, "l1" its triangular-sandwich
     preconditioned form through P^{1/2} = B^T diag(sqrt(d)), "l2" the diagonally
     preconditioned SigmaTilde + W^-1 (needs W > 0).  Returns (var, achieved rank)."""
-    T = dev.torch()
-    n = factor.n
+    n, n_p = factor.n, blocks.n_p
     if not 1 <= k <= n:
         raise ConfigError(f"rank k must be in [1, {n}], got {k}")
-    if variant not in ("none", "l1", "l2"):
+    if variant not in _LANCZOS_VARIANTS:
         raise ConfigError(f"unknown Lanczos variant {variant!r}")
-    if n * blocks.n_p > 200_000_000:
-        raise CapacityError("Lanczos variances materialize Bpo^T densely (n x n_p); limit 2e8 entries")
-    pat, tdev = factor.pattern, factor.ctx.tdev
+    ctx, pat = factor.ctx, factor.pattern
     W = state._dev["W"]
-    D = pat.to_dev(np.asarray(factor.D, dtype=float)[:, None])
-    # RT = Bpo^T, dense n x n_p in storage order
-    RT = T.zeros((n, blocks.n_p), dtype=T.float64, device=tdev)
-    if blocks.n_p:
-        rows = T.tensor(pat.siperm[blocks._nbr], device=tdev)  # factor -> storage index
-        cols = T.arange(blocks.n_p, device=tdev)[:, None].expand_as(rows)
-        RT[rows.reshape(-1), cols.reshape(-1)] = T.tensor(blocks.values, dtype=T.float64, device=tdev).reshape(-1)
-    if variant == "none":
-        corr, order = _lanczos_correction(lambda v: W * v + _precision(factor, v, D), RT, RT, k)
-    elif variant == "l1":
-        sd = T.sqrt(W + 1.0 / D)
-
-        def matvec(v):
-            x = _dapply(factor, "vl_sptrsv", 0, v / sd)
-            x = W * x + _precision(factor, x, D)
-            return _dapply(factor, "vl_sptrsv", 1, x) / sd
-
-        RT2 = _dapply(factor, "vl_sptrsv", 1, RT) / sd
-        corr, order = _lanczos_correction(matvec, RT2, RT2, k)
-    else:
+    dsig = None
+    if variant == "l2":
         if bool((W <= 0).any()):
             raise CapabilityError("l2 variant needs W > 0 everywhere")
         from .laplace import diag_sigma_tilde_dev
-        inv_sqrt = 1.0 / T.sqrt(diag_sigma_tilde_dev(factor) + 1.0 / W)
-
-        def matvec(v):
-            x = inv_sqrt * v
-            return inv_sqrt * (_sigma_tilde(factor, x, D) + x / W)
-
-        right = inv_sqrt * _sigma_tilde(factor, RT, D)
-        left = inv_sqrt * (RT / W)
-        corr, order = _lanczos_correction(matvec, left, right, k)
-    return blocks.Dp + corr, order
+        dsig = diag_sigma_tilde_dev(factor)
+    # column mean of RT = Bpo^T: (1/n_p) Bpo^T 1, summed in prediction-point order
+    start = np.zeros(n)
+    if n_p:
+        start = np.bincount(blocks._nbr.ravel(), weights=blocks.values.ravel(), minlength=n) / n_p
+    start_d = pat.to_dev(start)
+    var_d = dev.empty(ctx, max(n_p, 1))
+    achieved = C.c_int(0)
+    _lib.call("vl_pred_lanczos", ctx.h, factor.h, blocks.h, _lib.ptr(W), _LANCZOS_VARIANTS[variant], int(k),
+              _lib.ptr(start_d), _lib.ptr(dsig) if dsig is not None else None, LANCZOS_BREAKDOWN_TOL,
+              _lib.ptr(var_d), C.byref(achieved))
+    if n_p == 0:
+        return np.empty(0), int(achieved.value)
+    return dev.download(var_d)[:n_p], int(achieved.value)
