@@ -402,11 +402,34 @@ def main():
         if world > 1:
             torch.distributed.barrier()
 
+    L.vl_prof_only.argtypes = [_lib.c_void_p, _lib.C.c_char_p]
+
+    def prof_table():
+        buf = _lib.C.create_string_buffer(1 << 16)
+        nl = _lib.C.c_int64(0)
+        _lib.check(L.vl_prof_report(ctx.h, buf, 1 << 16, _lib.C.byref(nl)))
+        out = {}
+        for ln in buf.value.decode().splitlines():
+            tg, cnt, tms, by = ln.split("\t")
+            out[tg] = {"launches": int(cnt), "ms": float(tms), "bytes": float(by)}
+        return out, int(nl.value)
+
     for _ in range(a.warmup):
         val, grad = obj.evaluate(theta, beta, xi, want_grad=True)
     torch.cuda.synchronize()
+    # One more untimed evaluation with CUDA events around EVERY launch: the per-tag table
+    # ("kernels") and the dominant kernel.  Two timing events per launch cost ~4 % of the step
+    # (22 000 events), so the timed region below keeps events only on the dominant kernel.
+    _lib.check(L.vl_prof_only(ctx.h, None))
     _lib.check(L.vl_prof_reset(ctx.h))
     _lib.check(L.vl_prof_enable(ctx.h, 1))
+    val, grad = obj.evaluate(theta, beta, xi, want_grad=True)
+    torch.cuda.synchronize()
+    tags, launches_step = prof_table()
+    cand0 = {k: v for k, v in tags.items() if v["bytes"] > 0}
+    dom = max(cand0, key=lambda k: cand0[k]["ms"]) if cand0 else None
+    _lib.check(L.vl_prof_only(ctx.h, dom.encode() if dom else None))
+    _lib.check(L.vl_prof_reset(ctx.h))
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -437,25 +460,19 @@ def main():
         tt = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         ms = float(tt.item())
-    buf = _lib.C.create_string_buffer(1 << 16)
-    launches = _lib.C.c_int64(0)
-    _lib.check(L.vl_prof_report(ctx.h, buf, 1 << 16, _lib.C.byref(launches)))
+    timed_tags, n_launches = prof_table()     # dominant kernel only, live in the timed region
+    launches = _lib.C.c_int64(n_launches)
     _lib.check(L.vl_prof_enable(ctx.h, 0))
-    tags = {}
-    for ln in buf.value.decode().splitlines():
-        tg, cnt, tms, by = ln.split("\t")
-        tags[tg] = {"launches": int(cnt), "ms": float(tms), "bytes": float(by)}
+    _lib.check(L.vl_prof_only(ctx.h, None))
     # one evaluation is the unit of work; with N ranks its probes are sharded
     # (strong scaling of a fixed evaluation) -> whole-job evals/s
     value = a.steps / (ms / 1000.0)
 
     # ---- roofline of the dominant kernel (by total device time, bytes-tagged) ----
     peak, peak_kind = measured_peak()
-    cand = {k: v for k, v in tags.items() if v["bytes"] > 0}
-    dom = max(cand, key=lambda k: cand[k]["ms"]) if cand else None
     roof = None
-    if dom:
-        d = tags[dom]
+    if dom and dom in timed_tags:
+        d = timed_tags[dom]
         avg_ms = d["ms"] / d["launches"]
         per_launch = d["bytes"] / d["launches"]
         ach = per_launch / (avg_ms / 1e3) / 1e9
@@ -468,8 +485,9 @@ def main():
                 traffic = None
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                "bytes_per_launch": per_launch, "avg_launch_ms": avg_ms,
-                "share_of_step": round(d["ms"] / ms, 4)}
+                "bytes_per_launch": per_launch, "avg_launch_ms": avg_ms, "launches_timed": d["launches"],
+                "share_of_step": round(d["ms"] / ms, 4),
+                "timing": "CUDA events around every launch of this kernel inside the timed region"}
 
     # ---- end-to-end through the public API with host buffers -------------------
     e2e_steps = a.e2e_steps if a.e2e_steps is not None else max(1, min(a.steps, 5))
@@ -551,7 +569,9 @@ def main():
                 "phase_ms": {k: round(v, 3) for k, v in phase_ms.items()},
                 "phases": {"replicated": ["factor", "mode"], "probe_sharded": ["probes_nll", "gradient"],
                            "note": "gradient includes the replicated single-RHS tvec solve"},
-                "iterations": counts, "config4_prediction": c4, "kernels": tags}
+                "iterations": counts, "config4_prediction": c4,
+                "kernels_note": "per-tag device time of ONE untimed evaluation with events around every launch",
+                "kernels": tags}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -114,6 +114,9 @@ int vl_sptrsv(vl_ctx* ctx, const vl_factor* f, int transpose, int64_t t, const d
  * lines into buf. */
 int vl_prof_enable(vl_ctx* ctx, int on);
 int vl_prof_reset(vl_ctx* ctx);
+/* restrict the events to launches under one tag (NULL / "": every tagged launch);
+ * the launch counter keeps counting every launch */
+int vl_prof_only(vl_ctx* ctx, const char* tag);
 int vl_prof_report(vl_ctx* ctx, char* buf, int len, int64_t* launches);
 
 /* ---- Laplace objective (iterative backend, VADU preconditioner) ---------- */

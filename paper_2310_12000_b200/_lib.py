@@ -119,6 +119,7 @@ def ptr(a):
 _SIGS.update({
     "vl_prof_enable": [c_void_p, c_int],
     "vl_prof_reset": [c_void_p],
+    "vl_prof_only": [c_void_p, C.c_char_p],
     "vl_prof_report": [c_void_p, C.c_char_p, c_int, P_int64],
 })
 EXPORTED = sorted(_SIGS)

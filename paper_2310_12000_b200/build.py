@@ -68,13 +68,22 @@ def _compile(src, verbose_ptxas=False, defines=(), out_dir=OUT_DIR):
     return obj, r.stderr
 
 
-def build(verbose=False, jobs=None, defines=(), lib=LIB):
+def build(verbose=False, jobs=None, defines=(), lib=LIB, only=None):
+    """``defines`` builds a variant library into its own object directory; with ``only``
+    (source names) just those sources are compiled with the defines and every other object
+    is taken from the default build (A/B experiments on one kernel family)."""
     out_dir = OUT_DIR if not defines else OUT_DIR + "_" + "_".join(d.replace("=", "") for d in defines)
     os.makedirs(out_dir, exist_ok=True)
     srcs = sources()
     jobs = jobs or min(len(srcs), os.cpu_count() or 4)
+
+    def one(s):
+        if only is not None and s not in only:
+            return _compile(s, verbose, (), OUT_DIR)
+        return _compile(s, verbose, defines, out_dir)
+
     with cf.ThreadPoolExecutor(jobs) as ex:
-        results = list(ex.map(lambda s: _compile(s, verbose, defines, out_dir), srcs))
+        results = list(ex.map(one, srcs))
     objs = [o for o, _ in results]
     if verbose:
         for (o, log), s in zip(results, srcs):

@@ -520,6 +520,13 @@ int vl_prof_enable(vl_ctx* h, int on) {
   });
 }
 
+int vl_prof_only(vl_ctx* h, const char* tag) {
+  return guard_dev(h, [&] {
+    prof_collect(h->c);
+    h->c.prof.only = tag ? tag : "";
+  });
+}
+
 int vl_prof_reset(vl_ctx* h) {
   return guard_dev(h, [&] {
     prof_collect(h->c);

@@ -19,6 +19,7 @@ struct BView {
   const int32_t* tidx;
   const double* valT;
   int m;
+  int64_t nnzT;         // entries of the children CSR
 };
 
 // Strided vector view: x[row * ld + col]
@@ -90,9 +91,12 @@ constexpr int kStreamWin = 256;
 #ifndef VL_STREAM_PROD
 #define VL_STREAM_PROD 1
 #endif
+#ifndef VL_STREAM_PF
+#define VL_STREAM_PF 0
+#endif
 template <class Idx, class Wt, class Load>
 VL_D void stream_rows1(int64_t E0, int64_t E1, int64_t b, int64_t e, const Idx& idx, const Wt& wt, const Load& load,
-                       double& acc) {
+                       double& acc, const int32_t* pf_i = nullptr, const double* pf_w = nullptr, int64_t pf_end = 0) {
   __shared__ double s_w[kRowsThreads / 32][kStreamWin];
   __shared__ double s_x[kRowsThreads / 32][kStreamWin];
   const int lane = threadIdx.x & 31;
@@ -102,6 +106,15 @@ VL_D void stream_rows1(int64_t E0, int64_t E1, int64_t b, int64_t e, const Idx& 
   for (int64_t w0 = E0; w0 < E1; w0 += kStreamWin) {
     int32_t j[K];
     double wv[K], xv[K];
+#if VL_STREAM_PF
+    // the window VL_STREAM_PF ahead: its 8 index lines and 16 value lines into L2
+    // (entries past E1 belong to the next rows of the stream, read by the next warp)
+    const int64_t nw = w0 + (int64_t)VL_STREAM_PF * kStreamWin;
+    if (pf_i != nullptr && nw + kStreamWin <= pf_end) {
+      if (lane < 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf_i + nw + lane * 32));
+      else if (lane < 24) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf_w + nw + (lane - 8) * 16));
+    }
+#endif
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int64_t g = w0 + k * 32 + lane;
@@ -217,7 +230,7 @@ VL_D void gather_Bt(const BView& B, int64_t s, bool valid, int gl, int t, const 
     const int64_t E1 = __shfl_sync(0xffffffffu, e0 + cs, nv - 1);
     stream_rows1(
         E0, E1, e0, (int64_t)e0 + cs, [&](int64_t g) { return B.tidx[g]; }, [&](int64_t g) { return B.valT[g]; },
-        load, acc[0]);
+        load, acc[0], B.tidx, B.valT, B.nnzT);
     return;
   }
   const int32_t* ti = B.tidx + e0;
@@ -306,6 +319,7 @@ struct TrsvPlain {
   int ld;
   VL_D double rhs(int64_t s, int c, double&) const { return b[s * ld + c]; }
   VL_D void out(int64_t, int, double, double&) const {}
+  VL_D void prefetch(int64_t s) const { asm volatile("prefetch.global.L2 [%0];" ::"l"(b + s * ld)); }
 };
 
 }  // namespace vl

@@ -34,7 +34,8 @@ struct DevBuf {
 // live roofline) + a launch counter (gpu_launches).
 struct Prof {
   bool on = false;
-  const char* tag = nullptr;  // current tag (set by ProfScope at call sites)
+  std::string only;           // when non-empty: events only around launches under this tag
+  const char* tag = nullptr;  // current tag (set by ProfScope at call sites; null = untimed)
   double bytes = 0;           // algorithmic bytes of one launch under the current tag
   struct Rec {
     std::string tag;
@@ -80,6 +81,9 @@ struct Ctx {
   DevBuf head_Y, head_Xh;
   // debug: per-row completion timestamps of the next triangular solves (n entries)
   long long* debug_tstamp = nullptr;
+  // VL_FRONT: completed single-RHS solve items (device counter) and the host's running total
+  DevBuf front;
+  unsigned front_total = 0;
   // deterministic reduction scratch: per-block partials + ticket counters
   DevBuf red_partial;   // doubles
   DevBuf red_counter;   // unsigned ints (ring of slots)

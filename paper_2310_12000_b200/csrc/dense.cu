@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(256) thin_nt_kernel(int m, int K, int kchunk, 
 #pragma unroll
   for (int c = 0; c < NT; ++c) acc[c] = 0.0;
   if (i < m) {
+#pragma unroll 8
     for (int kk = k0; kk < k1; ++kk) {
       const double a = A[i + (int64_t)kk * lda] * (KW ? kw[kk] : 1.0);
 #pragma unroll
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(256) thin_tn_kernel(int n, int K, const double
 #pragma unroll
     for (int c = 0; c < MT; ++c) acc[c] = 0.0;
     const double* bj = B + j * ldb;
+#pragma unroll 8
     for (int kk = lane; kk < K; kk += 32) {
       const double b = bj[kk];
 #pragma unroll

@@ -299,7 +299,7 @@ void factor_head_inverse(Ctx& C, Factor& F) {
   const int blocks = std::max(1, std::min((H + 3) / 4, std::max(occ, 1) * C.num_sms));
   ProfScope ps(C, "factor_head_inverse", 0.0);
   C.prof.launches++;
-  cudaEvent_t ev = C.prof.on ? prof_begin(C) : nullptr;
+  cudaEvent_t ev = (C.prof.on && C.prof.tag) ? prof_begin(C) : nullptr;
   head_inverse_kernel<<<blocks, 128, smem, C.stream>>>(H, P.m, P.head_rows.as<int32_t>(), P.head_nbr.as<int32_t>(),
                                                        P.cnt.as<int32_t>(), F.val.as<double>(), F.headX.as<double>());
   VL_LAUNCH_CHECK();
@@ -362,7 +362,7 @@ static void launch_build(Ctx& C, const Pattern& P, Factor& F, const Matern& K, i
   if (blocks < 1) blocks = 1;
   ProfScope ps(C, "factor_build", 0.0);
   C.prof.launches++;
-  cudaEvent_t ev = C.prof.on ? prof_begin(C) : nullptr;
+  cudaEvent_t ev = (C.prof.on && C.prof.tag) ? prof_begin(C) : nullptr;
   factor_build_kernel<Q, DIM><<<blocks, threads, smem, C.stream>>>(
       P.n, P.d, P.m, P.xy.as<double>(), P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), P.fidx.as<int32_t>(), K, want_grad,
       F.val.as<double>(), F.D.as<double>(), want_grad ? F.dval.as<double>() : nullptr,

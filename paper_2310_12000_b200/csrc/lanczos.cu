@@ -430,24 +430,26 @@ int pred_lanczos(Ctx& C, const Factor& F, const PredBlocks& B, const double* W, 
   };
   for (int c0 = 0; c0 < kk; c0 += kPanel) {
     const int cw = std::min(kPanel, kk - c0);
-    const int ld = cw + (cw & 1);
-    if (ld != cw) VL_CUDA(cudaMemsetAsync(P1.p, 0, sizeof(double) * (size_t)n * ld, C.stream));
+    // an odd panel is widened by one zero column (contiguous 16-byte column units: ld == t
+    // even), so the solves and the gather treat the pad like any other column
+    const int ct = cw + (cw & 1);
+    if (ct != cw) VL_CUDA(cudaMemsetAsync(P1.p, 0, sizeof(double) * (size_t)n * ct, C.stream));
     if (variant == 0) {
-      panel(c0, cw, ld, nullptr, 0, nullptr, 0, P1.as<double>());
-      bpo(P1.as<double>(), ld, cw, Zr.as<double>() + c0);
+      panel(c0, cw, ct, nullptr, 0, nullptr, 0, P1.as<double>());
+      bpo(P1.as<double>(), ct, ct, Zr.as<double>() + c0);
     } else if (variant == 1) {
-      panel(c0, cw, ld, s, -1, nullptr, 0, P1.as<double>());
-      op_trsv(C, F, false, cw, ld, P1.as<double>(), P2.as<double>());
-      bpo(P2.as<double>(), ld, cw, Zr.as<double>() + c0);
+      panel(c0, cw, ct, s, -1, nullptr, 0, P1.as<double>());
+      op_trsv(C, F, false, ct, ct, P1.as<double>(), P2.as<double>());
+      bpo(P2.as<double>(), ct, ct, Zr.as<double>() + c0);
     } else {
-      panel(c0, cw, ld, s, 1, W, -1, P1.as<double>());                     // left: Q o is / W
-      bpo(P1.as<double>(), ld, cw, Zl.as<double>() + c0);
-      panel(c0, cw, ld, s, 1, nullptr, 0, P1.as<double>());                // right: SigmaTilde (is o Q)
-      op_trsv(C, F, true, cw, ld, P1.as<double>(), P2.as<double>());
-      panel_rowscale_kernel<<<nblocks(C, n * cw), kLzThreads, 0, C.stream>>>(n, cw, ld, D, P2.as<double>());
+      panel(c0, cw, ct, s, 1, W, -1, P1.as<double>());                     // left: Q o is / W
+      bpo(P1.as<double>(), ct, ct, Zl.as<double>() + c0);
+      panel(c0, cw, ct, s, 1, nullptr, 0, P1.as<double>());                // right: SigmaTilde (is o Q)
+      op_trsv(C, F, true, ct, ct, P1.as<double>(), P2.as<double>());
+      panel_rowscale_kernel<<<nblocks(C, n * ct), kLzThreads, 0, C.stream>>>(n, ct, ct, D, P2.as<double>());
       VL_LAUNCH_CHECK();
-      op_trsv(C, F, false, cw, ld, P2.as<double>(), P1.as<double>());
-      bpo(P1.as<double>(), ld, cw, Zr.as<double>() + c0);
+      op_trsv(C, F, false, ct, ct, P2.as<double>(), P1.as<double>());
+      bpo(P1.as<double>(), ct, ct, Zr.as<double>() + c0);
     }
   }
   tri_corr_kernel<<<nblocks(C, np), kLzThreads, 0, C.stream>>>(np, kk, ldz, Zr.as<double>(),

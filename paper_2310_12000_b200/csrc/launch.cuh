@@ -57,7 +57,7 @@ struct ProfScope {
   const char* old_tag;
   double old_bytes;
   ProfScope(Ctx& c, const char* tag, double bytes) : C(c), old_tag(c.prof.tag), old_bytes(c.prof.bytes) {
-    C.prof.tag = tag;
+    C.prof.tag = (c.prof.only.empty() || c.prof.only == tag) ? tag : nullptr;
     C.prof.bytes = bytes;
   }
   ~ProfScope() {
@@ -275,6 +275,16 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
                       (void*)&x,      (void*)&body,  (void*)&fin,      (void*)&partials, (void*)&counter,
                       (void*)&gate,   (void*)&smax,  (void*)&tstamp,   (void*)&sb,     (void*)&total,
                       (void*)&sl};
+#if VL_FRONT
+      if (C.front.p == nullptr) {
+        C.front.alloc(sizeof(unsigned) * 32);
+        VL_CUDA(cudaMemsetAsync(C.front.p, 0, sizeof(unsigned) * 32, C.stream));
+        C.front_total = 0;
+      }
+      sl.front = C.front.as<unsigned>();
+      sl.fbase = C.front_total;
+      if (nitems > 0) C.front_total += (unsigned)nitems;
+#endif
       if (nitems > 0)
         VL_CUDA(cudaLaunchCooperativeKernel((const void*)k1, dim3(grid1), dim3(kRowsThreads), args, smem1,
                                             C.stream));

@@ -497,7 +497,7 @@ void lrac_pchol(Ctx& C, const Factor& F, LracFactor& LF, int k, double tol) {
   const MaternK K = make_matern(F);
   unsigned* counter = next_counter(C);
   ProfScope ps(C, "lrac_pchol", 0.0);
-  cudaEvent_t pev = C.prof.on ? prof_begin(C) : nullptr;  // the k steps as one timed region
+  cudaEvent_t pev = (C.prof.on && C.prof.tag) ? prof_begin(C) : nullptr;  // the k steps as one timed region
   for (int j = 0; j < k; ++j) {
     pchol_step_kernel<<<grid, kPcThreads, 0, C.stream>>>(n, P.d, P.xy.as<double>(), P.fidx.as<int32_t>(), K, j, k,
                                                          LF.L.as<double>(), d.as<double>(), S, tol,

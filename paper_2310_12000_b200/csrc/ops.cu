@@ -117,6 +117,7 @@ BView bview(const Factor& F, bool grad) {
   v.tidx = P.tidx.as<int32_t>();
   v.valT = F.valT.as<double>();
   v.m = P.m;
+  v.nnzT = P.nnz_off;
   return v;
 }
 
@@ -138,6 +139,9 @@ void op_spmm(Ctx& C, const Factor& F, int op, int t, int ld, const double* x, do
 void op_trsv(Ctx& C, const Factor& F, bool transpose, int t, int ld, const double* b, double* x) {
   const Pattern& P = *F.pat;
   if (b == x) fail(kEConfig, "triangular solve cannot run in place");
+  // the dense head block works on H x t panels: a padded leading dimension would leave the
+  // pad column of the head rows at the "not ready" sentinel and the dependent rows polling
+  if (t > 1 && ld != t) fail(kEConfig, "multi-column triangular solves need contiguous columns (ld == t)");
   dispatch_cols(t, ld, [&](auto g, auto nu, auto u) {
     constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(u)::value;
     if (!transpose) {

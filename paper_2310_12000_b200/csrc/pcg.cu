@@ -49,6 +49,12 @@ struct RhsScaleDot {  // z = B^-1 (w * dinv) ; acc += (r - alpha v) . z
     const double rn = DEFER ? fma(-alpha[c], v[o], r[o]) : r[o];
     acc += rn * x;
   }
+  VL_D void prefetch(int64_t s) const {  // single-RHS items: next item's lines into L2
+    prefetch_l2(w + s * ld);
+    prefetch_l2(dinv + s);
+    prefetch_l2(r + s * ld);
+    if (DEFER) prefetch_l2(v + s * ld);
+  }
 };
 struct RzInitFin {
   CgCols K;
@@ -241,6 +247,10 @@ struct K3Rhs {
     return rn;
   }
   VL_D void out(int64_t, int, double, double&) const {}
+  VL_D void prefetch(int64_t s) const {
+    prefetch_l2(r + s * ld);
+    prefetch_l2(v + s * ld);
+  }
 };
 struct K3RhsFused {
   double* r;

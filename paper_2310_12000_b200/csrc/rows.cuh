@@ -538,25 +538,30 @@ VL_D void trsv_row(int64_t p, int64_t pend_, int t, int ld, const int32_t* __res
 // xs -= sum_q w[q] v[q] over one batch.  VL_TREE_SUM = 0: the entries in order
 // (one dependent fma chain of B); 1: four interleaved partial sums folded
 // pairwise (chain of B/4 + 2), a fixed order as well.
+// xs -= sum_q w[q] v[q] over one batch: the entries in order (one dependent
+// fma chain of B), or, with TREE, four interleaved partial sums folded
+// pairwise (chain of B/4 + 2; a fixed order as well).  Measured on the t = 1
+// PCG: forward solve 0.371 -> 0.354 ms; the backward solve (fused product
+// children CSR, two batches per item) 0.402 -> 0.431 ms, so it keeps the chain.
 #ifndef VL_TREE_SUM
-#define VL_TREE_SUM 0
+#define VL_TREE_SUM 1
 #endif
-template <int B>
+template <int B, bool TREE>
 VL_D void fold_batch(const double (&w)[B], const double (&v)[B], double& xs) {
-#if VL_TREE_SUM
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if constexpr (TREE && VL_TREE_SUM) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-  for (int q = 0; q < B; q += 4) {
-    a0 = fma(w[q], v[q], a0);
-    a1 = fma(w[q + 1], v[q + 1], a1);
-    a2 = fma(w[q + 2], v[q + 2], a2);
-    a3 = fma(w[q + 3], v[q + 3], a3);
+    for (int q = 0; q < B; q += 4) {
+      a0 = fma(w[q], v[q], a0);
+      a1 = fma(w[q + 1], v[q + 1], a1);
+      a2 = fma(w[q + 2], v[q + 2], a2);
+      a3 = fma(w[q + 3], v[q + 3], a3);
+    }
+    xs -= (a0 + a1) + (a2 + a3);
+  } else {
+#pragma unroll
+    for (int q = 0; q < B; ++q) xs -= w[q] * v[q];
   }
-  xs -= (a0 + a1) + (a2 + a3);
-#else
-#pragma unroll
-  for (int q = 0; q < B; ++q) xs -= w[q] * v[q];
-#endif
 }
 
 #ifndef VL_POLL_ONE
@@ -617,7 +622,7 @@ VL_D void trsv_row1(int64_t p, int64_t pend_, const int32_t* __restrict__ order,
       }
 #endif
       if (!pend) {
-        fold_batch<B>(w, v, xs);
+        fold_batch<B, !csr_deps<Deps>()>(w, v, xs);
         const int eb = e0;
         e0 += B;
         if (e0 >= cs) {
@@ -704,18 +709,34 @@ struct Slab {
   const uint32_t* w;
   const int32_t* idx;
   const double* val;
+  // VL_FRONT: running count of completed single-RHS items (all launches of the context) and
+  // the count at this launch's start; a waiting item backs off by its distance to the count
+  unsigned* front = nullptr;
+  unsigned fbase = 0;
 };
+#ifndef VL_FRONT
+#define VL_FRONT 0
+#endif
+#ifndef VL_FRONT_D0
+#define VL_FRONT_D0 96      // items ahead of the completed count that poll at full rate
+#endif
+#ifndef VL_FRONT_NS
+#define VL_FRONT_NS 4       // back-off per item of distance beyond D0 (ns)
+#endif
+#ifndef VL_FRONT_MAX
+#define VL_FRONT_MAX 1500   // back-off cap (ns)
+#endif
 
 // trsv_row1 over the item's slab: the 32 lanes read entry e of their rows as
 // one 128-byte (index) and one 256-byte (value) transaction, instead of 32
 // scattered row segments; padded entries have idx -1 / value 0.  Same
 // per-lane early completion and the same summation order as trsv_row1.
-template <class Body>
+template <class Body, bool TREE>
 VL_D void trsv_row1s(int64_t p, int64_t pend_, const int32_t* __restrict__ order, uint32_t off, int wk,
                      const Slab& sl, int lane, double* __restrict__ x, const Body& body, unsigned smax,
-                     long long* __restrict__ tstamp, double& acc0) {
+                     long long* __restrict__ tstamp, double& acc0, int32_t so_in = -2, unsigned my = 0u) {
   constexpr int B = 32;
-  const int32_t so = (p < pend_) ? order[p] : -1;
+  const int32_t so = so_in != -2 ? so_in : ((p < pend_) ? order[p] : -1);
   const bool valid = so >= 0;
   const int64_t s = valid ? so : 0;
   constexpr bool PS = PsumOf<Body>::value;
@@ -741,6 +762,13 @@ VL_D void trsv_row1s(int64_t p, int64_t pend_, const int32_t* __restrict__ order
     j[q] = on ? __ldg(ip + q * 32) : -1;
     w[q] = on ? __ldg(vp + q * 32) : 0.0;
   }
+#ifdef VL_TS_EXT
+  if (tstamp != nullptr && valid && j[0] >= -1) {  // slab entries arrived
+    long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    tstamp[4LL * VL_TS_EXT + s] = g;
+  }
+#endif
 #pragma unroll
   for (int q = 0; q < B; ++q) {
     if (j[q] >= 0) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
@@ -749,6 +777,9 @@ VL_D void trsv_row1s(int64_t p, int64_t pend_, const int32_t* __restrict__ order
   if (valid) xs = rh = body.rhs(s, 0, acc0);
   bool done = !valid;
   unsigned ns = 8;
+#if VL_FRONT
+  unsigned fcount = my, fnext = 0u;  // first round: distance unknown -> regular back-off
+#endif
   for (;;) {
     if (!done) {
       bool pend = false;
@@ -764,7 +795,7 @@ VL_D void trsv_row1s(int64_t p, int64_t pend_, const int32_t* __restrict__ order
       }
 #endif
       if (!pend) {
-        fold_batch<B>(w, v, xs);
+        fold_batch<B, TREE>(w, v, xs);
         const int eb = e0;
         e0 += B;
         if (e0 >= wk) {
@@ -798,6 +829,22 @@ VL_D void trsv_row1s(int64_t p, int64_t pend_, const int32_t* __restrict__ order
       }
     }
     if (__all_sync(0xffffffffu, done)) break;
+#if VL_FRONT
+    if (sl.front != nullptr) {
+      // distance of this item to the completed count as read in the previous round
+      const int dist = (int)(my - fcount);
+      if (dist > VL_FRONT_D0) {
+        const int bo = (dist - VL_FRONT_D0) * VL_FRONT_NS;
+        __nanosleep(bo < VL_FRONT_MAX ? bo : VL_FRONT_MAX);
+      } else if (smax) {
+        __nanosleep(ns);
+        ns = ns < smax ? ns * 2 : smax;
+      }
+      unsigned f = 0u;
+      if (lane == 0) asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(f) : "l"(sl.front));
+      fnext = f;
+    } else
+#endif
     if (smax) {
       __nanosleep(ns);
       ns = ns < smax ? ns * 2 : smax;
@@ -807,6 +854,9 @@ VL_D void trsv_row1s(int64_t p, int64_t pend_, const int32_t* __restrict__ order
       for (int q = 0; q < B; ++q)
         if (is_sentinel(v[q])) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
     }
+#if VL_FRONT
+    if (sl.front != nullptr) fcount = __shfl_sync(0xffffffffu, fnext, 0);
+#endif
   }
   if constexpr (PS) {
     // fused B^T(om o y) of the row: once per item, after the warp's poll loop,
@@ -871,6 +921,14 @@ __global__ void __launch_bounds__(kRowsThreads, (trsv_min_blocks<U, Body, Deps>(
 // one row solved warp-per-row with the lanes over its dependencies (rows of
 // thin levels / rows with many children), then a shuffle reduction.
 constexpr uint32_t kHeavyBit = 0x80000000u;
+#ifndef VL_CARRY
+#define VL_CARRY 0
+#endif
+template <class T, class = void>
+struct HasPrefetch : std::false_type {};
+template <class T>
+struct HasPrefetch<T, std::void_t<decltype(std::declval<const T&>().prefetch(0))>> : std::true_type {};
+VL_D void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 #ifndef VL_PREFETCH
 #define VL_PREFETCH 1
 #endif
@@ -888,7 +946,12 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
                                                              const int* __restrict__ gate, unsigned smax,
                                                              long long* __restrict__ tstamp, int slot_base,
                                                              int total_slots, Slab sl) {
-  if (gate != nullptr && *((volatile const int*)gate) == 0) return;
+  if (gate != nullptr && *((volatile const int*)gate) == 0) {
+#if VL_FRONT
+    if (sl.front != nullptr && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(sl.front, (unsigned)nitems);
+#endif
+    return;
+  }
   extern __shared__ double rsh[];
   constexpr int NRR = NR > 0 ? NR : 1;
   constexpr int HB = 8;  // deps per lane per heavy round (256 per warp)
@@ -916,9 +979,26 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
   uint32_t c_d, c_o, c_w, n_d, n_o, n_w;
   desc(gwarp, c_d, c_o, c_w);
   desc(gwarp + nwarps, n_d, n_o, n_w);
+#if VL_CARRY
+  // the lane's row of the current / next light item, loaded one item ahead
+  // (takes the order -> row load off the item's dependent-load chain), and the
+  // next item's right-hand-side lines prefetched into L2 through the body hook
+  auto row_of = [&](uint32_t d) -> int32_t {
+    if (d & kHeavyBit) return -1;
+    const int64_t p = (int64_t)d + lane;
+    return p < npos ? __ldg(order + p) : -1;
+  };
+  int32_t c_s = row_of(c_d), n_s = row_of(n_d);
+#endif
   for (int64_t it = gwarp; it < nitems; it += nwarps) {
     const uint32_t item = c_d;
     const uint32_t off = c_o, wk = c_w;
+#if VL_CARRY
+    const int32_t so = c_s;
+    if constexpr (HasPrefetch<Body>::value) {
+      if (it + nwarps < nitems && n_s >= 0) body.prefetch(n_s);
+    }
+#endif
     if (VL_HPREFETCH && it + nwarps < nitems && (n_d & kHeavyBit)) {
       // next heavy item: its first round of dependency indices / values
       const int64_t nb = n_o;
@@ -927,7 +1007,9 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
       if (lane * 16 < ne) asm volatile("prefetch.global.L2 [%0];" ::"l"(deps.vaddr(nb + lane * 16)));
     }
     if (VL_PREFETCH && sl.idx != nullptr && it + nwarps < nitems && !(n_d & kHeavyBit)) {
+#if !VL_CARRY
       asm volatile("prefetch.global.L2 [%0];" ::"l"(order + n_d + lane));
+#endif
       for (uint32_t l = lane; l < 3 * n_w; l += 32) {
         const char* a = l < n_w ? reinterpret_cast<const char*>(sl.idx + ((int64_t)n_o + l) * 32)
                                 : reinterpret_cast<const char*>(sl.val + (int64_t)n_o * 32) + (int64_t)(l - n_w) * 128;
@@ -936,11 +1018,24 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
     }
     c_d = n_d; c_o = n_o; c_w = n_w;
     desc(it + 2 * nwarps, n_d, n_o, n_w);
+#if VL_CARRY
+    c_s = n_s;
+    n_s = row_of(n_d);
+#endif
     if (!(item & kHeavyBit)) {
       if (sl.idx != nullptr)
-        trsv_row1s((int64_t)item + lane, npos, order, off, (int)wk, sl, lane, x, body, smax, tstamp, acc[0][0]);
+#if VL_CARRY
+        trsv_row1s<Body, !csr_deps<Deps>()>((int64_t)item + lane, npos, order, off, (int)wk, sl, lane, x, body, smax,
+                                            tstamp, acc[0][0], so, sl.fbase + (unsigned)it);
+#else
+        trsv_row1s<Body, !csr_deps<Deps>()>((int64_t)item + lane, npos, order, off, (int)wk, sl, lane, x, body, smax,
+                                            tstamp, acc[0][0], -2, sl.fbase + (unsigned)it);
+#endif
       else
         trsv_row1((int64_t)item + lane, npos, order, deps, x, body, smax, tstamp, acc[0][0]);
+#if VL_FRONT
+      if (sl.front != nullptr && lane == 0) asm volatile("red.global.add.u32 [%0], 1;" ::"l"(sl.front) : "memory");
+#endif
       continue;
     }
     const int64_t s = (int64_t)(item & ~kHeavyBit);
@@ -999,6 +1094,9 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
         tstamp[s] = g;
       }
+#if VL_FRONT
+      if (sl.front != nullptr) asm volatile("red.global.add.u32 [%0], 1;" ::"l"(sl.front) : "memory");
+#endif
     }
   }
   if constexpr (NR > 0) {

@@ -22,7 +22,7 @@ pat = Pattern(xyp, nbr, 1)
 f = build_factor(xyp, vg.CovarianceSpec(1.0, 0.02, 1.5), pat, want_grad=False)
 L = _lib.lib()
 L.vl_debug_set_tstamp.argtypes = [C.c_void_p, C.c_void_p]
-ts = torch.zeros(4 * n, dtype=torch.int64, device="cuda")
+ts = torch.zeros(5 * n, dtype=torch.int64, device="cuda")
 lev = np.zeros(n, dtype=np.int64)
 for i in range(n):
     row = nbr[i][nbr[i] >= 0]
@@ -37,9 +37,9 @@ L.vl_debug_set_tstamp(f.ctx.h, C.c_void_p(ts.data_ptr()))
 _lib.call("vl_sptrsv", f.ctx.h, f.h, 0, 1, _lib.ptr(X), _lib.ptr(Y))
 torch.cuda.synchronize()
 L.vl_debug_set_tstamp(f.ctx.h, None)
-a = ts.cpu().numpy().reshape(4, n)
-done, start, ready, rounds = (np.empty(n, dtype=np.int64) for _ in range(4))
-for arr, k in ((done, 0), (start, 1), (ready, 2), (rounds, 3)):
+a = ts.cpu().numpy().reshape(5, n)
+done, start, ready, rounds, slab = (np.empty(n, dtype=np.int64) for _ in range(5))
+for arr, k in ((done, 0), (start, 1), (ready, 2), (rounds, 3), (slab, 4)):
     arr[pat.sperm] = a[k]
 ok = start > 0
 t0 = start[ok].min()
@@ -57,5 +57,10 @@ for lo in range(150, nl, 20):
     sd = (start[sel] - depmax[sel]) / 1e3
     rd = (ready[sel] - depmax[sel]) / 1e3
     dr = (done[sel] - ready[sel]) / 1e3
+    ss = (slab[sel] - start[sel]) / 1e3          # item start -> slab entries in registers
+    r1 = sel & (rounds == 1)
+    rs = (ready[r1] - slab[r1]) / 1e3 if r1.sum() else np.zeros(1)   # gathers + rhs (no polling needed)
+    tot = (done[sel] - start[sel]) / 1e3
     print(f"L{lo:3d}-{lo+19:3d} {sel.sum():7d}  {np.median(sd):9.2f}  {np.median(rd):9.2f}  {np.median(dr):9.2f}  "
-          f"{np.median(rounds[sel]):6.0f}   p90 ready-dep {np.percentile(rd, 90):.2f}")
+          f"{np.median(rounds[sel]):6.0f}   p90 ready-dep {np.percentile(rd, 90):.2f}  slab-start {np.median(ss):.2f} "
+          f"ready-slab(rounds=1) {np.median(rs):.2f} item {np.median(tot):.2f}")
