@@ -2,22 +2,26 @@
 
 Usage:  python -m paper_2310_12000_b200.build   (or __graft_entry__.build())
 
-Objects are compiled in parallel into ``paper_2310_12000_b200/_build`` and
-linked into ``paper_2310_12000_b200/libvlgpx.so`` (git-ignored, but shipped
+Objects are compiled in parallel into a per-checkout directory under the
+system temp dir (``VLGPX_BUILD_DIR`` overrides it) and linked into ``paper_2310_12000_b200/libvlgpx.so`` (git-ignored, but shipped
 to the GPU box by gpurun because it lives in the tree).
 """
 
 from __future__ import annotations
 
 import concurrent.futures as cf
+import hashlib
 import os
 import shutil
 import subprocess
 import sys
+import tempfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT_DIR = os.path.join(HERE, "_build")
+# object files live outside the tree (only the linked library travels to the GPU box)
+OUT_DIR = os.environ.get("VLGPX_BUILD_DIR") or os.path.join(
+    tempfile.gettempdir(), "vlgpx_build_" + hashlib.sha1(HERE.encode()).hexdigest()[:10], "_build")
 LIB = os.path.join(HERE, "libvlgpx.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3,-pthread", "--expt-relaxed-constexpr",

@@ -3,6 +3,8 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <type_traits>
 #include <vector>
 
@@ -46,6 +48,15 @@ void dispatch_cols(int t, int ld, F&& f) {
   else go(IC<1>{});
 }
 
+// VL_DEBUG_SYNC=1: synchronise after every launch of the row / solve launchers and name the
+// failing instantiation (compute-sanitizer is not always available)
+inline void debug_sync(Ctx& C, const char* what) {
+  static const bool on = std::getenv("VL_DEBUG_SYNC") != nullptr;
+  if (!on) return;
+  const cudaError_t e = cudaStreamSynchronize(C.stream);
+  if (e != cudaSuccess) fail(kECuda, std::string("kernel failed: ") + what + ": " + cudaGetErrorString(e));
+}
+
 unsigned* next_counter(Ctx& C);
 int coop_grid(Ctx& C, const void* func, size_t smem);
 cudaEvent_t prof_begin(Ctx& C, cudaStream_t st = nullptr);  // nullptr: C.stream
@@ -87,6 +98,7 @@ void launch_rows(Ctx& C, int64_t n, int t, const Body& body, const Fin& fin, con
                                                  wptr);
   VL_LAUNCH_CHECK();
   if (ev) prof_end(C, ev);
+  debug_sync(C, __PRETTY_FUNCTION__);
 }
 
 // SM-local sweep (rows_local_kernel) for gather bodies over a spatially
@@ -114,6 +126,7 @@ void launch_rows_local(Ctx& C, const Pattern& P, int64_t n, int t, const Body& b
                                                      gate, wptr);
   VL_LAUNCH_CHECK();
   if (ev) prof_end(C, ev);
+  debug_sync(C, __PRETTY_FUNCTION__);
 }
 
 // Split a level sequence (padded position pointer, nlev levels) into
@@ -324,6 +337,7 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
     if (head) run_head(main_slots, main_slots + hgrid);
   }
   if (ev) prof_end(C, ev);
+  debug_sync(C, __PRETTY_FUNCTION__);
 }
 
 }  // namespace vl
