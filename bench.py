@@ -333,13 +333,22 @@ def config4_prediction(s=1000, n=500_000, n_p=500_000, rho=0.05, m=20, seed=4, m
     var = vg.latent_var_sim(st, f, blocks, s=s, seed=seed + 1, cfg=cfg, rng="device")
     ev[2].record()
     torch.cuda.synchronize()
+    # rank-k Lanczos variances at the same size (the reference's dense n x n_p RT would be 2 TB)
+    lz = {}
+    for variant, k in (("none", 100), ("l1", 100)):
+        t0 = time.perf_counter()
+        v_lz, order = vg.latent_var_lanczos(st, f, blocks, k, variant=variant, cfg=cfg)
+        torch.cuda.synchronize()
+        lz[variant] = {"k": k, "achieved": int(order), "s": round(time.perf_counter() - t0, 3),
+                       "mean_var": float(v_lz.mean()),
+                       "corr_with_sim": float(np.corrcoef(v_lz, var)[0, 1])}
     t_mean, t_var = ev[0].elapsed_time(ev[1]) / 1e3, ev[1].elapsed_time(ev[2]) / 1e3
     return {"workload": f"predict_n{n}_np{n_p}_s{s}", "likelihood": "poisson", "rho": rho, "m": m,
             "locations": f"uniform, pairs closer than {min_sep:g} re-drawn (reference D floor)",
             "blocks_mean_s": round(t_mean, 4), "var_sim_s": round(t_var, 4),
             "samples_per_s": round(s / t_var, 2), "predictions_per_s": round(n_p / (t_mean + t_var), 1),
             "rmse_latent": float(np.sqrt(np.mean((omega - latent[n:]) ** 2))), "mean_var": float(var.mean()),
-            "newton_iters": int(st.newton_iters), "newton_grad_tol": cfg.newton_grad_tol}
+            "newton_iters": int(st.newton_iters), "newton_grad_tol": cfg.newton_grad_tol, "lanczos": lz}
 
 
 def spawn_ranks(a):

@@ -2,6 +2,7 @@
 // every call maps failures onto a status code + thread-local message.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -197,6 +198,8 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
   int heavy_rows = 64, heavy_deps = 64;
   if (const char* e = std::getenv("VL_HEAVY_LEVEL_ROWS")) heavy_rows = std::atoi(e);
   if (const char* e = std::getenv("VL_HEAVY_DEPS")) heavy_deps = std::atoi(e);
+  bool slab_sort = false;
+  if (const char* e = std::getenv("VL_SLAB_SORT")) slab_sort = std::atoi(e) != 0;
   auto items = [&](const std::vector<int32_t>& order, const std::vector<int32_t>& lptr, bool fwd_dir) {
     std::vector<uint32_t> it;
     for (size_t L = 0; L + 1 < lptr.size(); ++L) {
@@ -255,16 +258,22 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
         const int32_t s = order[c + l];
         if (s < 0) continue;
         const int d = deg(s);
+        std::vector<std::pair<int32_t, int32_t>> ent(d);  // (dependency row, ELL slot of its value)
         for (int e = 0; e < d; ++e) {
-          const size_t q = ((size_t)off[k] + e) * 32 + l;
           if (fwd_dir) {
-            idx[q] = ell[(size_t)s * P.m + e];
-            map[q] = (int32_t)((int64_t)s * P.m + e);
+            ent[e] = {ell[(size_t)s * P.m + e], (int32_t)((int64_t)s * P.m + e)};
           } else {
             const int32_t pos = tptr[s] + e;
-            idx[q] = tidx[pos];
-            map[q] = tmap[pos];
+            ent[e] = {tidx[pos], tmap[pos]};
           }
+        }
+        // VL_SLAB_SORT=1: a row's entries by dependency storage row, so entry e of the 32
+        // spatially adjacent rows of an item falls into nearby lines of x
+        if (slab_sort) std::sort(ent.begin(), ent.end());
+        for (int e = 0; e < d; ++e) {
+          const size_t q = ((size_t)off[k] + e) * 32 + l;
+          idx[q] = ent[e].first;
+          map[q] = ent[e].second;
         }
       }
     }

@@ -92,7 +92,7 @@ constexpr int kStreamWin = 256;
 #define VL_STREAM_PROD 1
 #endif
 #ifndef VL_STREAM_PF
-#define VL_STREAM_PF 0
+#define VL_STREAM_PF 8   // windows ahead (measured on the t = 1 product: 0.114 -> 0.106 ms; 20: 0.110)
 #endif
 template <class Idx, class Wt, class Load>
 VL_D void stream_rows1(int64_t E0, int64_t E1, int64_t b, int64_t e, const Idx& idx, const Wt& wt, const Load& load,
