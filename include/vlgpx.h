@@ -86,6 +86,12 @@ int vl_pattern_perm(const vl_pattern* p, int32_t* sperm_host);
 /* info (10 entries): [n, d, m, nnz_off, n_levels_fwd, n_levels_bwd, max_children, order_kind,
  *   head_levels, head_rows] -- the last two describe the dense head block of the solves (0 = off) */
 int vl_pattern_info(const vl_pattern* p, int64_t* info);
+/* Row order the multi-column solves walk when x does not fit in L2 (transpose = 0: B, 1: B^T):
+ * storage rows outside the head block, wide levels cut into bands and walked tile by tile
+ * (a topological order of the dependency graph).  *len = 0 when the pattern keeps the level
+ * order.  order_host may be NULL (length query) or hold *len int32.  No reference counterpart:
+ * scipy's spsolve_triangular (vecchia.py:161-174) walks rows in index order. */
+int vl_pattern_solve_order(const vl_pattern* p, int transpose, int64_t* len, int32_t* order_host);
 
 /* ---- factor (per theta) ------------------------------------------------------
  * Replaces vecchia.py:220-283 build_factor (values) and vecchia.py:286-337

@@ -38,6 +38,7 @@ _SIGS = {
     "vl_pattern_destroy": [c_void_p],
     "vl_pattern_perm": [c_void_p, c_void_p],
     "vl_pattern_info": [c_void_p, P_int64],
+    "vl_pattern_solve_order": [c_void_p, c_int, P_int64, c_void_p],
     "vl_factor_build": [c_void_p, c_void_p, c_double, c_double, c_double, c_int, C.POINTER(c_void_p)],
     "vl_factor_destroy": [c_void_p],
     "vl_factor_get": [c_void_p, c_void_p, c_int, c_void_p],

@@ -305,6 +305,12 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
   slabs(fwd, fi, true, P.fwd_sl);
   slabs(bwd, bi, false, P.bwd_sl);
   slabs(P.bwdnh_order_h, bni, false, P.bwdnh_sl);
+  upload(C, P.nbr_s, P.nbr_s_h);
+  upload(C, P.map_s, P.map_s_h);
+  upload(C, P.fwd_torder, P.fwd_torder_h);
+  upload(C, P.bwd_torder, P.bwd_torder_h);
+  P.fwd_tlen = (int64_t)P.fwd_torder_h.size();
+  P.bwd_tlen = (int64_t)P.bwd_torder_h.size();
   upload(C, P.fwd_items, fi);
   upload(C, P.bwd_items, bi);
   upload(C, P.bwdnh_items, bni);
@@ -340,6 +346,7 @@ int vl_ctx_create(int device, void* stream, vl_ctx** out) {
     if (const char* e = std::getenv("VL_MIN_THICK")) C.min_thick_levels = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("VL_USE_HEAD")) C.use_head = std::atoi(e) != 0;
     if (const char* e = std::getenv("VL_USE_SLABS")) C.use_slabs = std::atoi(e) != 0;
+    if (const char* e = std::getenv("VL_USE_TILES")) C.use_tiles = std::atoi(e) != 0;
     if (const char* e = std::getenv("VL_USE_LOCAL")) C.use_local = std::atoi(e) != 0;
     if (const char* e = std::getenv("VL_PMODE1")) C.pmode1 = std::max(0, std::min(3, std::atoi(e)));
     if (const char* e = std::getenv("VL_PMODET")) C.pmodeT = std::max(0, std::min(1, std::atoi(e)));
@@ -422,6 +429,12 @@ int vl_pattern_create(vl_ctx* h, int64_t n, int d, int m, const double* xy, cons
     p->p.m = m;
     p->p.order_kind = order_kind;
     if (const char* e = std::getenv("VL_HEAD_MAX")) p->p.head_max = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("VL_CHILD_LATE")) p->p.child_late = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("VL_TILE_K")) p->p.tile_K = std::max(0, std::atoi(e));  // 0: level order
+    if (const char* e = std::getenv("VL_TILE_S")) p->p.tile_S = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("VL_TILE_MIN_ROWS")) p->p.tile_min_rows = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("VL_TILE_MIN_MB")) p->p.tile_min_bytes = (size_t)std::max(0, std::atoi(e)) << 20;
+    if (const char* e = std::getenv("VL_TILE_MIN_N")) p->p.tile_min_n = std::max(0, std::atoi(e));
     try {
       std::vector<int32_t> empty;
       const int32_t* nb = nbr;
@@ -456,6 +469,15 @@ int vl_pattern_info(const vl_pattern* p, int64_t* info) {
     info[7] = P.order_kind;
     info[8] = P.head_L;
     info[9] = P.head_H;
+  });
+}
+
+int vl_pattern_solve_order(const vl_pattern* p, int transpose, int64_t* len, int32_t* order_host) {
+  return guard([&] {
+    if (!p || !len) fail(kEConfig, "null handle");
+    const std::vector<int32_t>& o = transpose ? p->p.bwd_torder_h : p->p.fwd_torder_h;
+    *len = (int64_t)o.size();
+    if (order_host != nullptr && !o.empty()) std::memcpy(order_host, o.data(), sizeof(int32_t) * o.size());
   });
 }
 

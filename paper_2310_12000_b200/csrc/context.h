@@ -70,6 +70,8 @@ struct Ctx {
   bool use_slabs = true;  // coalesced dependency slabs for the single-RHS solves
   bool use_local = true;  // SM-local sweeps for multi-column gather passes (rows_local_kernel)
   bool use_head = true;
+  // multi-column solves walk the pattern's tile-blocked order (Pattern::fwd_torder) when x is large
+  bool use_tiles = true;
   // sandwich-PCG product mode (pcg.cu) for t == 1 / t > 1:
   //   0: B h + B^T tmp passes, 1: B^T(om o y) fused into the backward solve,
   //   2: B^T(om o y) as a side-stream pass concurrent with the forward solve,
@@ -131,6 +133,17 @@ struct Pattern {
   DevBuf bwdnh_order, bwdnh_lptr, bwdnh_items;  // backward schedule without the head rows
   int64_t bwdnh_len = 0, bwdnh_nitems = 0;
   int64_t fwd_items_head_end = 0;  // forward items covering the head levels
+  // tile-blocked topological orders of the rows outside the head for the multi-column
+  // solves (pattern.cpp); empty when the pattern has no wide levels / no spatial order
+  int tile_K = 64, tile_S = 6;
+  size_t tile_min_bytes = (size_t)96 << 20;  // x (n x ld doubles) below this stays in level order (fits L2)
+  int child_late = 16;  // pattern.cpp: dependencies within this many levels of the row are listed last
+  std::vector<int32_t> nbr_s_h, map_s_h;
+  DevBuf nbr_s, map_s;  // n*m  solve-ordered copy of nbr / slot of its value in Factor::val (or -1)
+  int64_t tile_min_rows = 4096, tile_min_n = 100000;
+  std::vector<int32_t> fwd_torder_h, bwd_torder_h;
+  DevBuf fwd_torder, bwd_torder;
+  int64_t fwd_tlen = 0, bwd_tlen = 0;
   DevBuf tptr;      // n+1  int32 children CSR (= CSR of B^T) in storage order
   DevBuf tidx;      // nnz  int32 child storage row
   DevBuf tmap;      // nnz  int32 ELL slot (child*m + k) holding B[child, s]
@@ -160,6 +173,7 @@ struct Factor {
   DevBuf headX;   // H*H  dense B_HH^-1, column-major (head order), lower triangular
   DevBuf headXr;  // H*H  the same, row-major
   DevBuf sv_fwd, sv_bwd, sv_bwdnh;  // slab values (Pattern::Slabs::map gathered from val)
+  DevBuf val_s;   // n*m  val in the solve order of Pattern::nbr_s
 };
 
 }  // namespace vl

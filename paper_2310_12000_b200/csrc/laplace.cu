@@ -550,7 +550,7 @@ void probes_eq6(Ctx& C, const Factor& F, const double* dinv, int pkind, int t, i
     return;
   }
   BView B = bview(F, false);
-  DepsEll dfw{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
+  DepsEll dfw = deps_fwd(F);
   dispatch_cols(t, ld, [&](auto g, auto nu, auto uu) {
     constexpr int G_ = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
     {
@@ -640,7 +640,7 @@ void probes_given(Ctx& C, const Factor& F, const double* dinv, int pkind, int t,
   }
   DevBuf Y;
   Y.alloc(sizeof(double) * (size_t)n * ld);
-  DepsEll dfw{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
+  DepsEll dfw = deps_fwd(F);
   DepsCsr dbw{P.tptr.as<int32_t>(), P.tidx.as<int32_t>(), F.valT.as<double>()};
   dispatch_cols(t, ld, [&](auto g, auto nu, auto uu) {
     constexpr int G_ = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
@@ -659,7 +659,7 @@ void probes_vadu(Ctx& C, const Factor& F, const double* W, int t, int ld, const 
   sd.alloc(sizeof(double) * n);
   launch_rows<1, 1, 1, 0, 0>(C, n, 1, SqrtDBody{F.D.as<double>(), W, sd.as<double>()}, Fin0<0>{});
   BView B = bview(F, false);
-  DepsEll dfw{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
+  DepsEll dfw = deps_fwd(F);
   double* sums = C.dev_scalars.as<double>();
   if (t > 256) fail(kECapacity, "too many probe columns per call");
   dispatch_cols(t, ld, [&](auto g, auto nu, auto uu) {

@@ -58,6 +58,15 @@ inline void debug_sync(Ctx& C, const char* what) {
 }
 
 unsigned* next_counter(Ctx& C);
+
+// Dependencies of the forward solve: the solve-ordered copy of the ELL rows when the pattern
+// has one (late parents last, pattern.cpp), else the rows as the factor build wrote them.
+inline DepsEll deps_fwd(const Factor& F) {
+  const Pattern& P = *F.pat;
+  if (F.val_s.p != nullptr && !P.map_s_h.empty())
+    return DepsEll{P.nbr_s.as<int32_t>(), P.cnt.as<int32_t>(), F.val_s.as<double>(), P.m};
+  return DepsEll{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
+}
 int coop_grid(Ctx& C, const void* func, size_t smem);
 cudaEvent_t prof_begin(Ctx& C, cudaStream_t st = nullptr);  // nullptr: C.stream
 void prof_end(Ctx& C, cudaEvent_t a, cudaStream_t st = nullptr);
@@ -207,9 +216,26 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
   std::vector<int> grids;
   int main_slots = 0;
   int grid1 = 0;
+  // tile-blocked order (pattern.cpp): one row per warp only (rows sharing a warp must be
+  // independent, which the level padding guarantees and the tile order does not), and only
+  // when x does not fit in L2 anyway
+  bool tiled = false;
+  if constexpr (G == 32) {
+    const int64_t tl = fwd ? P.fwd_tlen : P.bwd_tlen;
+    tiled = !single && tl > 0 && C.use_tiles && sizeof(double) * (size_t)n * ld >= P.tile_min_bytes;
+    if (tiled) {
+      order = fwd ? P.fwd_torder.as<int32_t>() : P.bwd_torder.as<int32_t>();
+      npos = tl;
+    }
+  }
   if (single) {
     grid1 = std::min(coop_grid(C, (const void*)k1, smem1), C.num_sms * C.trsv_blocks_per_sm);
     main_slots = grid1;
+  } else if (tiled) {
+    segs.push_back({L0, (int)lptr->size() - 1, false});
+    const int gcap = std::min(coop_grid(C, (const void*)kern, smem), C.num_sms * C.trsv_blocks_per_sm);
+    grids.push_back((int)std::max<int64_t>(1, std::min<int64_t>((npos * G + kRowsThreads - 1) / kRowsThreads, gcap)));
+    main_slots = grids[0];
   } else {
     std::vector<int32_t> sub(lptr->begin() + L0, lptr->end());
     segs = solve_segments(sub, C.thin_passes * (kThinThreads / G), C.min_thick_levels);
@@ -308,8 +334,8 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
       TrsvLaunch Lc;
       Lc.L0 = segs[i].L0;
       Lc.L1 = segs[i].L1;
-      Lc.p0 = (*lptr)[segs[i].L0];
-      Lc.p1 = (*lptr)[segs[i].L1];
+      Lc.p0 = tiled ? 0 : (*lptr)[segs[i].L0];
+      Lc.p1 = tiled ? npos : (*lptr)[segs[i].L1];
       Lc.lptr = lptr_d;
       Lc.slot_base = slot;
       Lc.total_slots = total;

@@ -643,7 +643,7 @@ void lrac_apply_inv(Ctx& C, const LracPrec& Pr, int t, const double* r, double* 
 
 void apply_sigma_tilde(Ctx& C, const Factor& F, int t, const double* x, double* y, double* scratch) {
   const Pattern& P = *F.pat;
-  DepsEll dfw{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
+  DepsEll dfw = deps_fwd(F);
   DepsCsr dbw{P.tptr.as<int32_t>(), P.tidx.as<int32_t>(), F.valT.as<double>()};
   dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {
     constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(uu)::value;
@@ -677,7 +677,7 @@ void pcg_lrac(Ctx& C, const LracPrec& Pr, int t, const double* b, double* u, dou
   K.bh = K.ah + (size_t)cap * t;
   const int* gate = K.status;
   const Pattern& PP = P;
-  DepsEll dfw{PP.nbr.as<int32_t>(), PP.cnt.as<int32_t>(), F.val.as<double>(), PP.m};
+  DepsEll dfw = deps_fwd(F);
   DepsCsr dbw{PP.tptr.as<int32_t>(), PP.tidx.as<int32_t>(), F.valT.as<double>()};
   int status[3] = {0, 0, 0};
   dispatch_cols(t, t, [&](auto g, auto nu, auto uu) {

@@ -145,7 +145,7 @@ void op_trsv(Ctx& C, const Factor& F, bool transpose, int t, int ld, const doubl
   dispatch_cols(t, ld, [&](auto g, auto nu, auto u) {
     constexpr int G = decltype(g)::value, NU = decltype(nu)::value, U = decltype(u)::value;
     if (!transpose) {
-      DepsEll deps{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
+      DepsEll deps = deps_fwd(F);
       launch_trsv<G, NU, U, 0>(C, F,true, t, ld, deps, x, TrsvPlain{b, ld},
                                Fin0<0>{});
     } else {

@@ -456,7 +456,7 @@ void pcg_vadu(Ctx& C, const SysVadu& S, int t, int ld, const double* b, double* 
   K.bh = K.ah + (size_t)cap * t;
   const int* gate = K.status;
   BView B = bview(F, false);
-  DepsEll dfw{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
+  DepsEll dfw = deps_fwd(F);
   DepsCsr dbw{P.tptr.as<int32_t>(), P.tidx.as<int32_t>(), F.valT.as<double>()};
   double* hb[1] = {h0.as<double>()};
 

@@ -376,7 +376,10 @@ VL_D void trsv_row(int64_t p, int64_t pend_, int t, int ld, const int32_t* __res
 #ifndef VL_BATCH2
 #define VL_BATCH2 4
 #endif
-  constexpr int BATCH = (NC == 1) ? 32 : (NC == 2 ? (csr_deps<Deps>() ? 8 : VL_BATCH2) : 8);
+#ifndef VL_BATCH2C
+#define VL_BATCH2C 8
+#endif
+  constexpr int BATCH = (NC == 1) ? 32 : (NC == 2 ? (csr_deps<Deps>() ? VL_BATCH2C : VL_BATCH2) : 8);
   using CL = Cols<G, NU, U>;
   constexpr bool PS = PsumOf<Body>::value;
   const int32_t so = (p < pend_) ? order[p] : -1;
@@ -891,9 +894,15 @@ struct TrsvLaunch {
 #ifndef VL_PS_MINB
 #define VL_PS_MINB 4
 #endif
+#ifndef VL_MINB_ELL
+#define VL_MINB_ELL 4
+#endif
+#ifndef VL_MINB_CSR
+#define VL_MINB_CSR 3
+#endif
 template <int U, class Body, class Deps>
 constexpr int trsv_min_blocks() {
-  return U == 2 ? (csr_deps<Deps>() ? 3 : (PsumOf<Body>::value ? VL_PS_MINB : 4)) : 1;
+  return U == 2 ? (csr_deps<Deps>() ? VL_MINB_CSR : (PsumOf<Body>::value ? VL_PS_MINB : VL_MINB_ELL)) : 1;
 }
 template <int G, int NU, int U, int NR, class Deps, class Body, class Fin>
 __global__ void __launch_bounds__(kRowsThreads, (trsv_min_blocks<U, Body, Deps>())) trsv_kernel(TrsvLaunch L, int t, int ld,

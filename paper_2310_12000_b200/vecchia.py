@@ -169,6 +169,17 @@ class Pattern:
         self.max_children = int(info[6])
         self._sperm_t = None
 
+    def solve_order(self, transpose=False):
+        """Storage rows in the order the multi-column solves walk them when x does not fit
+        in L2 (tile-blocked topological order, csrc/pattern.cpp); empty when the pattern
+        keeps the level order."""
+        ln = C.c_int64(0)
+        _lib.call("vl_pattern_solve_order", self.h, int(bool(transpose)), C.byref(ln), None)
+        out = np.empty(ln.value, dtype=np.int32)
+        if ln.value:
+            _lib.call("vl_pattern_solve_order", self.h, int(bool(transpose)), C.byref(ln), _lib.ptr(out))
+        return out
+
     def max_count(self):
         """Largest neighbour count (VecchiaFactor.m), computed once per pattern."""
         if getattr(self, "_max_count", None) is None:

@@ -52,7 +52,11 @@ def test_mode_matches_reference(vg, name):
     bar = 1e-6 if weak else (5e-8 if str(g["family"]) == "poisson" else 1e-8)
     assert _rel(st.b, g["b"]) <= bar
     assert _rel(st.W, g["W"]) <= bar
-    assert st.logp == pytest.approx(float(g["logp"]), rel=1e-8 if weak else 1e-10)
+    # logp alone is not stationary at the mode (d logp / d b = d1 != 0), so it inherits the
+    # mode's own bar scaled by |d1 . db| / |logp|: measured <= 1.1e-10 over these fixtures
+    # (gamma_vadu_n300 moved from 6e-11 to 1.02e-10 when the solves' in-row summation order
+    # changed with the late-dependency-last layout)
+    assert st.logp == pytest.approx(float(g["logp"]), rel=1e-8 if weak else 5e-10)
     assert st.quad == pytest.approx(float(g["quad"]), rel=1e-8)
 
 
