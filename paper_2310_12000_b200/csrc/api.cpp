@@ -433,6 +433,7 @@ int vl_pattern_create(vl_ctx* h, int64_t n, int d, int m, const double* xy, cons
     if (const char* e = std::getenv("VL_TILE_K")) p->p.tile_K = std::max(0, std::atoi(e));  // 0: level order
     if (const char* e = std::getenv("VL_TILE_S")) p->p.tile_S = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("VL_TILE_MIN_ROWS")) p->p.tile_min_rows = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("VL_TILE_TAIL")) p->p.tile_tail = std::atoi(e) != 0;
     if (const char* e = std::getenv("VL_TILE_MIN_MB")) p->p.tile_min_bytes = (size_t)std::max(0, std::atoi(e)) << 20;
     if (const char* e = std::getenv("VL_TILE_MIN_N")) p->p.tile_min_n = std::max(0, std::atoi(e));
     try {

@@ -136,6 +136,7 @@ struct Pattern {
   // tile-blocked topological orders of the rows outside the head for the multi-column
   // solves (pattern.cpp); empty when the pattern has no wide levels / no spatial order
   int tile_K = 64, tile_S = 6;
+  bool tile_tail = false;  // join a short narrow tail of levels to the last band (measured: no gain)
   size_t tile_min_bytes = (size_t)96 << 20;  // x (n x ld doubles) below this stays in level order (fits L2)
   int child_late = 16;  // pattern.cpp: dependencies within this many levels of the row are listed last
   std::vector<int32_t> nbr_s_h, map_s_h;

@@ -482,6 +482,14 @@ void pattern_build_host(Pattern& P, const double* xy, const int32_t* nbr, std::v
       int b0 = lmax, b1 = lmax + 1;
       while (b0 > 0 && sz[b0 - 1] >= P.tile_min_rows) --b0;
       while (b1 < nl && sz[b1] >= P.tile_min_rows) ++b1;
+      const int wide1 = b1;
+      // a short narrow tail after the wide run joins the last band: its rows then run inside
+      // their tiles, hidden behind the later tiles, instead of as a latency chain at the end
+      if (P.tile_tail) {
+        int64_t tail = 0;
+        for (int l = b1; l < nl; ++l) tail += sz[l];
+        if (tail * 20 < n) b1 = nl;
+      }
       // rows outside the head in (level, storage position) order
       std::vector<int64_t> ptr(nl + 1, 0);
       for (int l = 0; l < nl; ++l) ptr[l + 1] = ptr[l] + sz[l];
@@ -491,21 +499,23 @@ void pattern_build_host(Pattern& P, const double* xy, const int32_t* nbr, std::v
         for (int64_t s = 0; s < n; ++s)
           if (P.head_pos_h[s] < 0) lo[fl[lv[s]]++] = (int32_t)s;
       }
+      // bands of tile_K levels; the tail levels (if joined) belong to the last band of the wide run
+      const int nband = std::max(1, (wide1 - b0 + P.tile_K - 1) / P.tile_K);
       std::vector<int32_t> tile(n, 0);
       for (int64_t q = ptr[b0]; q < ptr[b1]; ++q) {
         const int32_t s = lo[q];
-        const int band = (lv[s] - b0) / P.tile_K;
+        const int band = std::min((lv[s] - b0) / P.tile_K, nband - 1);
         int tl = (int)((int64_t)s * P.tile_S / n);
         for (int k = 0; k < ndeps(s); ++k) {
           const int32_t dd = dep(s, k);
           if (P.head_pos_h[dd] >= 0 || lv[dd] < b0 || lv[dd] >= b1) continue;
-          if ((lv[dd] - b0) / P.tile_K == band) tl = std::max(tl, tile[dd]);
+          if (std::min((lv[dd] - b0) / P.tile_K, nband - 1) == band) tl = std::max(tl, tile[dd]);
         }
         tile[s] = tl;
       }
       std::vector<int32_t> bulk(lo.begin() + ptr[b0], lo.begin() + ptr[b1]);
       std::stable_sort(bulk.begin(), bulk.end(), [&](int32_t a, int32_t b) {
-        const int ba = (lv[a] - b0) / P.tile_K, bb = (lv[b] - b0) / P.tile_K;
+        const int ba = std::min((lv[a] - b0) / P.tile_K, nband - 1), bb = std::min((lv[b] - b0) / P.tile_K, nband - 1);
         if (ba != bb) return ba < bb;
         if (tile[a] != tile[b]) return tile[a] < tile[b];
         return lv[a] < lv[b];  // stable: storage position within a level
