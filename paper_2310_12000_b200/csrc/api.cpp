@@ -195,7 +195,10 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
   upload(C, P.bwd_lptr, P.bwd_level_ptr);
   // single-RHS work items: 32-row chunks, expanded to per-row (warp-per-row)
   // items on thin levels and for chunks holding a row with many dependencies
-  int heavy_rows = 64, heavy_deps = 64;
+  // (measured at n = 1e6, profiles/r2k_heavy_sweep.jsonl: level rows 64 / 128 / 256 / 512 / 1024 ->
+  // forward solve 0.344 / 0.338 / 0.327 / 0.323 / 0.328 ms; dependencies 32 / 64 / 128 ->
+  // backward solve 0.553 / 0.357 / 0.473 ms)
+  int heavy_rows = 512, heavy_deps = 64;
   if (const char* e = std::getenv("VL_HEAVY_LEVEL_ROWS")) heavy_rows = std::atoi(e);
   if (const char* e = std::getenv("VL_HEAVY_DEPS")) heavy_deps = std::atoi(e);
   bool slab_sort = false;
@@ -342,6 +345,7 @@ int vl_ctx_create(int device, void* stream, vl_ctx** out) {
     C.num_sms = prop.multiProcessorCount;
     if (const char* e = std::getenv("VL_TRSV_BPS")) C.trsv_blocks_per_sm = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("VL_SPIN_MAX_NS")) C.spin_max_ns = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("VL_SPIN_MAX_NS1")) C.spin_max_ns1 = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("VL_THIN_PASSES")) C.thin_passes = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("VL_MIN_THICK")) C.min_thick_levels = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("VL_USE_HEAD")) C.use_head = std::atoi(e) != 0;

@@ -63,6 +63,10 @@ struct Ctx {
   int trsv_blocks_per_sm = 4;
   // max nanosleep backoff while spinning on a dependency (0 = pure polling)
   int spin_max_ns = 64;
+  // the same for the single-RHS solves: pure polling (measured after the warp-per-row items
+  // took over the levels of <= 512 rows: 0 / 16 / 32 / 64 / 128 / 256 ns -> PCG iteration
+  // 0.787 / 0.797 / 0.799 / 0.804 / 0.815 / 0.839 ms; t = 50 is flat, 4.61-4.64 ms)
+  int spin_max_ns1 = 0;
   // thin solve levels: <= thin_passes * (1024 / G) rows run on a single CTA
   int thin_passes = 0;
   int min_thick_levels = 4;

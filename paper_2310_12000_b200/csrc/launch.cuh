@@ -262,7 +262,7 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
   VL_CUDA(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)n * ld, C.stream));
   double* partials = C.red_partial.as<double>();
   unsigned* counter = next_counter(C);
-  unsigned smax = (unsigned)C.spin_max_ns;
+  unsigned smax = (unsigned)(single ? C.spin_max_ns1 : C.spin_max_ns);
   long long* tstamp = C.debug_tstamp;
   double *Y = nullptr, *Xh = nullptr;
   const int ksplit = (t == 1) ? 1 : std::max(1, std::min(16, H / 256));

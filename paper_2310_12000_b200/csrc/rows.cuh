@@ -955,6 +955,12 @@ VL_D void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" :
 #define VL_HPREFETCH 0
 #endif
 
+#ifndef VL_HPOLL_THR
+#define VL_HPOLL_THR 0
+#endif
+#ifndef VL_HPOLL_NS
+#define VL_HPOLL_NS 100
+#endif
 template <int NR, class Deps, class Body, class Fin>
 __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int64_t npos,
                                                              const uint32_t* __restrict__ items,
@@ -1081,11 +1087,23 @@ __global__ void __launch_bounds__(kRowsThreads) trsv1_kernel(int64_t nitems, int
         bool pend = false;
 #pragma unroll
         for (int q = 0; q < HB; ++q) pend |= is_sentinel(v[q]);
+#if VL_HPOLL_THR > 0
+        // a row still missing many dependencies is far from the front: back off, so its polls
+        // do not load the L2 path of the rows one hop from completion
+        const unsigned pm = __ballot_sync(0xffffffffu, pend);
+        if (!pm) break;
+        if (__popc(pm) > VL_HPOLL_THR) __nanosleep(VL_HPOLL_NS);
+        else if (smax) {
+          __nanosleep(ns);
+          ns = ns < smax ? ns * 2 : smax;
+        }
+#else
         if (!__any_sync(0xffffffffu, pend)) break;
         if (smax) {
           __nanosleep(ns);
           ns = ns < smax ? ns * 2 : smax;
         }
+#endif
 #pragma unroll
         for (int q = 0; q < HB; ++q)
           if (is_sentinel(v[q])) ld_cg_unit<1>(x + (int64_t)j[q], &v[q]);
