@@ -508,7 +508,10 @@ def main():
     t0 = time.perf_counter()
     from paper_2310_12000_b200.laplace import find_mode, gradient, make_probes, neg_marginal_loglik
     from paper_2310_12000_b200.vecchia import build_factor
-    for _ in range(e2e_steps):
+    for k in range(e2e_steps + 1):
+        if k == 1:  # step 0 is an untimed warm-up of this call path (pinned staging buffers)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
         spec = vg.CovarianceSpec(1.0, a.rho, 1.5)
         fct = build_factor(obj.xy, spec, obj.pattern, want_grad=True)
         st = find_mode(fct, obj.lik0, y_host, F_host, cfg.backend)      # H2D: y, F (pinned staging)

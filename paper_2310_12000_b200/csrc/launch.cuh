@@ -216,9 +216,11 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
   std::vector<int> grids;
   int main_slots = 0;
   int grid1 = 0;
-  // tile-blocked order (pattern.cpp): one row per warp only (rows sharing a warp must be
-  // independent, which the level padding guarantees and the tile order does not), and only
-  // when x does not fit in L2 anyway
+  // tile-blocked order (pattern.cpp) of the multi-column solves, when x does not fit in L2 anyway.
+  // One row per warp only: with 32 / G > 1 rows per warp the rows in flight outnumber a
+  // (tile, level) cell several times and the walk turns into a latency chain (measured at
+  // t = 16, G = 8: B^-1 0.553 -> 0.660 ms, B^-T 0.967 -> 1.411 ms; the order itself is valid
+  // for any G, its level runs are padded to 32).
   bool tiled = false;
   if constexpr (G == 32) {
     const int64_t tl = fwd ? P.fwd_tlen : P.bwd_tlen;

@@ -520,9 +520,24 @@ void pattern_build_host(Pattern& P, const double* xy, const int32_t* nbr, std::v
         if (tile[a] != tile[b]) return tile[a] < tile[b];
         return lv[a] < lv[b];  // stable: storage position within a level
       });
-      out.assign(lo.begin(), lo.begin() + ptr[b0]);
-      out.insert(out.end(), bulk.begin(), bulk.end());
-      out.insert(out.end(), lo.begin() + ptr[b1], lo.end());
+      // every run of one level (inside one tile) is padded to 32 positions with -1, like the
+      // levels of the level order: the rows a warp takes together (32 / G of them) are then
+      // always independent, whatever G is
+      out.clear();
+      auto pad = [&]() { out.resize((out.size() + 31) / 32 * 32, -1); };
+      for (int l = 0; l < b0; ++l) {
+        out.insert(out.end(), lo.begin() + ptr[l], lo.begin() + ptr[l + 1]);
+        pad();
+      }
+      for (size_t q = 0; q < bulk.size(); ++q) {
+        if (q > 0 && (lv[bulk[q]] != lv[bulk[q - 1]] || tile[bulk[q]] != tile[bulk[q - 1]])) pad();
+        out.push_back(bulk[q]);
+      }
+      pad();
+      for (int l = b1; l < nl; ++l) {
+        out.insert(out.end(), lo.begin() + ptr[l], lo.begin() + ptr[l + 1]);
+        pad();
+      }
     };
     tiled(true, P.fwd_torder_h);
     tiled(false, P.bwd_torder_h);

@@ -29,6 +29,23 @@ def _pattern(xy, nbr, **env):
                 os.environ[k] = v
 
 
+def pat_levels(nbr, transpose):
+    """Dependency level (forward) or height (backward) of every factor row."""
+    n = nbr.shape[0]
+    lev = np.zeros(n, dtype=np.int64)
+    if not transpose:
+        for i in range(n):
+            r = nbr[i][nbr[i] >= 0]
+            if r.size:
+                lev[i] = lev[r].max() + 1
+    else:
+        for i in range(n - 1, -1, -1):
+            r = nbr[i][nbr[i] >= 0]
+            if r.size:
+                lev[r] = np.maximum(lev[r], lev[i] + 1)
+    return lev
+
+
 @pytest.fixture(scope="module")
 def data():
     import paper_2310_12000_b200 as vg
@@ -48,6 +65,14 @@ def test_tile_order_is_topological(data, K, S):
     par = np.where(nbr >= 0, spos[np.maximum(nbr, 0)], -1)   # factor row x m: storage rows of the parents
     for transpose in (False, True):
         order = pat.solve_order(transpose)
+        # runs of one level are padded to 32 positions with -1: the rows one warp takes
+        # together (32 / G of them, from an aligned group) then share a level
+        assert order.size % 32 == 0
+        lvl = pat_levels(nbr, transpose)[pat.sperm]          # level / height by storage row
+        grp = order.reshape(-1, 32)
+        for g in grp[:: max(1, grp.shape[0] // 500)]:
+            assert np.unique(lvl[g[g >= 0]]).size <= 1
+        order = order[order >= 0]
         assert order.size == n - pat.head_rows
         assert np.unique(order).size == order.size
         pos = np.full(n, -1, dtype=np.int64)
@@ -60,7 +85,7 @@ def test_tile_order_is_topological(data, K, S):
     assert np.count_nonzero(pos < 0) == pat.head_rows
 
 
-@pytest.mark.parametrize("t", [50, 64])
+@pytest.mark.parametrize("t", [3, 8, 13, 25, 50, 64])
 def test_tile_order_solves_vs_oracle(data, t):
     vg, xy, nbr = data
     spec = vg.CovarianceSpec(1.0, 0.05, 1.5)
