@@ -110,6 +110,14 @@ class Clocks:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def settle(self, timeout=4.0):
+        """Wait for nvidia-smi's first sample: its start-up (NVML attaching to the GPU) stays
+        outside the timed region; only samples taken after this point are summarised."""
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.lines and time.perf_counter() - t0 < timeout:
+            time.sleep(0.05)
+        self.start = len(self.lines)
+
     def __exit__(self, *exc):
         if self.proc is not None:
             self.proc.terminate()
@@ -121,7 +129,7 @@ class Clocks:
     def summary(self):
         sm, mx, reasons, util = [], 0, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[getattr(self, "start", 0):]:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
                 continue
@@ -451,6 +459,9 @@ def main():
 
     obj.on_phase = on_phase
     with Clocks(local) as clk:
+        clk.settle()
+        barrier()
+        torch.cuda.synchronize()
         e0.record()
         for _ in range(a.steps):
             val, grad = obj.evaluate(theta, beta, xi, want_grad=True)

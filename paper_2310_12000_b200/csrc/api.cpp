@@ -310,6 +310,7 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
   slabs(P.bwdnh_order_h, bni, false, P.bwdnh_sl);
   upload(C, P.nbr_s, P.nbr_s_h);
   upload(C, P.map_s, P.map_s_h);
+  P.has_solve_order = !P.map_s_h.empty();
   upload(C, P.fwd_torder, P.fwd_torder_h);
   upload(C, P.bwd_torder, P.bwd_torder_h);
   P.fwd_tlen = (int64_t)P.fwd_torder_h.size();
@@ -318,6 +319,8 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
   upload(C, P.bwd_items, bi);
   upload(C, P.bwdnh_items, bni);
   VL_CUDA(cudaStreamSynchronize(C.stream));
+  std::vector<int32_t>().swap(P.nbr_s_h);
+  std::vector<int32_t>().swap(P.map_s_h);
 }
 
 }  // namespace vl

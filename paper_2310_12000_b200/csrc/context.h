@@ -143,7 +143,8 @@ struct Pattern {
   bool tile_tail = false;  // join a short narrow tail of levels to the last band (measured: no gain)
   size_t tile_min_bytes = (size_t)96 << 20;  // x (n x ld doubles) below this stays in level order (fits L2)
   int child_late = 16;  // pattern.cpp: dependencies within this many levels of the row are listed last
-  std::vector<int32_t> nbr_s_h, map_s_h;
+  std::vector<int32_t> nbr_s_h, map_s_h;  // host staging, released after the upload
+  bool has_solve_order = false;
   DevBuf nbr_s, map_s;  // n*m  solve-ordered copy of nbr / slot of its value in Factor::val (or -1)
   int64_t tile_min_rows = 4096, tile_min_n = 100000;
   std::vector<int32_t> fwd_torder_h, bwd_torder_h;

@@ -335,7 +335,7 @@ void factor_refresh_transpose(Ctx& C, Factor& F) {
       VL_LAUNCH_CHECK();
     }
   };
-  if (!P.map_s_h.empty()) {
+  if (P.has_solve_order) {
     const int64_t ne = (int64_t)P.n * P.m;
     F.val_s.alloc(sizeof(double) * ne);
     slab_values_kernel<<<C.num_sms * 8, 256, 0, C.stream>>>(ne, P.map_s.as<int32_t>(), F.val.as<double>(),

@@ -63,7 +63,7 @@ unsigned* next_counter(Ctx& C);
 // has one (late parents last, pattern.cpp), else the rows as the factor build wrote them.
 inline DepsEll deps_fwd(const Factor& F) {
   const Pattern& P = *F.pat;
-  if (F.val_s.p != nullptr && !P.map_s_h.empty())
+  if (F.val_s.p != nullptr && P.has_solve_order)
     return DepsEll{P.nbr_s.as<int32_t>(), P.cnt.as<int32_t>(), F.val_s.as<double>(), P.m};
   return DepsEll{P.nbr.as<int32_t>(), P.cnt.as<int32_t>(), F.val.as<double>(), P.m};
 }
