@@ -203,35 +203,61 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
   if (const char* e = std::getenv("VL_HEAVY_DEPS")) heavy_deps = std::atoi(e);
   bool slab_sort = false;
   if (const char* e = std::getenv("VL_SLAB_SORT")) slab_sort = std::atoi(e) != 0;
-  auto items = [&](const std::vector<int32_t>& order, const std::vector<int32_t>& lptr, bool fwd_dir) {
+  // A chunk on a wide level whose rows all have <= heavy_deps dependencies is one light item.
+  // Rows above that become warp-per-row items of their own and are masked out of the chunk
+  // (mask[p] = 1: the light item skips position p), so their chunk-mates stay thread-per-row
+  // (VL_HEAVY_SPLIT=0: the whole chunk turns into warp-per-row items, as before).
+  bool heavy_split = true;
+  if (const char* e = std::getenv("VL_HEAVY_SPLIT")) heavy_split = std::atoi(e) != 0;
+  auto items = [&](const std::vector<int32_t>& order, const std::vector<int32_t>& lptr, bool fwd_dir,
+                   std::vector<char>& mask) {
     std::vector<uint32_t> it;
+    mask.assign(order.size(), 0);
     for (size_t L = 0; L + 1 < lptr.size(); ++L) {
       const int32_t q0 = lptr[L], q1 = lptr[L + 1];
       const bool thin = (q1 - q0) <= heavy_rows;
       for (int32_t c = q0; c < q1; c += 32) {
-        bool heavy = thin;
-        for (int32_t p = c; p < c + 32 && !heavy; ++p) {
+        int nheavy = 0, nrows = 0;
+        for (int32_t p = c; p < c + 32; ++p) {
           const int32_t s = order[p];
           if (s < 0) continue;
+          ++nrows;
           const int deg = fwd_dir ? cnt[s] : (tptr[s + 1] - tptr[s]);
-          if (deg > heavy_deps) heavy = true;
+          if (deg > heavy_deps) ++nheavy;
         }
-        if (!heavy) {
+        if (!thin && nheavy == 0) {
           it.push_back((uint32_t)c);
-        } else {
+        } else if (thin || !heavy_split) {
           for (int32_t p = c; p < c + 32; ++p)
             if (order[p] >= 0) it.push_back((uint32_t)p | 0x80000000u);
+        } else {
+          for (int32_t p = c; p < c + 32; ++p) {
+            const int32_t s = order[p];
+            if (s < 0) continue;
+            const int deg = fwd_dir ? cnt[s] : (tptr[s + 1] - tptr[s]);
+            if (deg > heavy_deps) {
+              it.push_back((uint32_t)p | 0x80000000u);
+              mask[p] = 1;
+            }
+          }
+          if (nheavy < nrows) it.push_back((uint32_t)c);
         }
       }
     }
     return it;
+  };
+  auto masked = [&](const std::vector<int32_t>& order, const std::vector<char>& mask) {
+    std::vector<int32_t> o(order);
+    for (size_t p = 0; p < o.size(); ++p)
+      if (mask[p]) o[p] = -1;
+    return o;
   };
   // Heavy items carry their row, dependency base and count in the item
   // descriptor (items = row | bit, off = ELL / CSR base, w = count), so the
   // solve issues their coalesced dependency loads without the order -> row
   // pointer chain.
   auto slabs = [&](const std::vector<int32_t>& order, std::vector<uint32_t>& its, bool fwd_dir,
-                   Pattern::Slabs& S) {
+                   Pattern::Slabs& S, const std::vector<char>& mask) {
     std::vector<uint32_t> off(std::max<size_t>(its.size(), 1), 0), w(std::max<size_t>(its.size(), 1), 0);
     int64_t tot = 0;
     auto deg = [&](int32_t s) { return fwd_dir ? cnt[s] : (tptr[s + 1] - tptr[s]); };
@@ -247,7 +273,7 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
       const int32_t c = (int32_t)its[k];
       int wk = 0;
       for (int32_t p = c; p < c + 32; ++p)
-        if (order[p] >= 0) wk = std::max(wk, deg(order[p]));
+        if (order[p] >= 0 && !mask[p]) wk = std::max(wk, deg(order[p]));
       off[k] = (uint32_t)tot;
       w[k] = (uint32_t)wk;
       tot += wk;
@@ -259,7 +285,7 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
       const int32_t c = (int32_t)its[k];
       for (int l = 0; l < 32; ++l) {
         const int32_t s = order[c + l];
-        if (s < 0) continue;
+        if (s < 0 || mask[c + l]) continue;
         const int d = deg(s);
         std::vector<std::pair<int32_t, int32_t>> ent(d);  // (dependency row, ELL slot of its value)
         for (int e = 0; e < d; ++e) {
@@ -288,8 +314,9 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
     upload(C, S.idx, idx);
     upload(C, S.map, map);
   };
-  auto fi = items(fwd, P.fwd_level_ptr, true);
-  auto bi = items(bwd, P.bwd_level_ptr, false);
+  std::vector<char> fmask, bmask, bnmask;
+  auto fi = items(fwd, P.fwd_level_ptr, true, fmask);
+  auto bi = items(bwd, P.bwd_level_ptr, false, bmask);
   P.fwd_nitems = (int64_t)fi.size();
   P.bwd_nitems = (int64_t)bi.size();
   // dense head block + backward schedule without it
@@ -303,11 +330,15 @@ void pattern_upload(Ctx& C, Pattern& P, const double* xy, const int32_t* nbr) {
   if (P.head_L > 0)
     for (uint32_t it : fi)
       if ((int64_t)(it & 0x7fffffffu) < P.fwd_level_ptr[P.head_L]) ++P.fwd_items_head_end;
-  auto bni = items(P.bwdnh_order_h, P.bwdnh_level_ptr, false);
+  auto bni = items(P.bwdnh_order_h, P.bwdnh_level_ptr, false, bnmask);
   P.bwdnh_nitems = (int64_t)bni.size();
-  slabs(fwd, fi, true, P.fwd_sl);
-  slabs(bwd, bi, false, P.bwd_sl);
-  slabs(P.bwdnh_order_h, bni, false, P.bwdnh_sl);
+  slabs(fwd, fi, true, P.fwd_sl, fmask);
+  slabs(bwd, bi, false, P.bwd_sl, bmask);
+  slabs(P.bwdnh_order_h, bni, false, P.bwdnh_sl, bnmask);
+  // the light items' view of the orders: positions of rows that run as their own items are -1
+  upload(C, P.fwd_order1, masked(fwd, fmask));
+  upload(C, P.bwd_order1, masked(bwd, bmask));
+  upload(C, P.bwdnh_order1, masked(P.bwdnh_order_h, bnmask));
   upload(C, P.nbr_s, P.nbr_s_h);
   upload(C, P.map_s, P.map_s_h);
   P.has_solve_order = !P.map_s_h.empty();

@@ -124,6 +124,7 @@ struct Pattern {
   int64_t fwd_len = 0, bwd_len = 0;
   DevBuf fwd_lptr, bwd_lptr;  // device copies of the padded level pointers
   DevBuf fwd_items, bwd_items;  // single-RHS work items (light 32-row chunks / heavy rows)
+  DevBuf fwd_order1, bwd_order1, bwdnh_order1;  // the orders as the light items see them (api.cpp)
   int64_t fwd_nitems = 0, bwd_nitems = 0;
   // dense head block (see pattern.cpp): rows of forward levels < head_L
   int64_t head_max = 3072;

@@ -205,6 +205,10 @@ void launch_trsv(Ctx& C, const Factor& F, bool fwd, int t, int ld, const Deps& d
     pick(P.bwd_sl, F.sv_bwd, 0);
   }
   const bool single = (G == 1 && NU == 1 && U == 1) && C.thin_passes == 0;
+  if (single) {  // light items skip the rows that run as warp-per-row items of their own
+    const DevBuf& o1 = fwd ? P.fwd_order1 : (head ? P.bwdnh_order1 : P.bwd_order1);
+    if (o1.p != nullptr) order = o1.as<int32_t>();
+  }
   // launch geometry and slot counts
   auto k1 = trsv1_kernel<NR, Deps, Body, Fin>;
   auto kern = trsv_kernel<G, NU, U, NR, Deps, Body, Fin>;

@@ -66,10 +66,17 @@ def _device_eval(coords, y, meta):
     assert _sha(nbr) == meta["nbr_sha256"], "neighbour sets differ from the reference's find_neighbors"
     f = build_factor(coords, vg.CovarianceSpec(1.0, rho, 1.5), nbr, perm)
     rank = meta["rank"]
+    fixed = meta.get("fixed_newton_steps")
     cfg = vg.BackendConfig(preconditioner=meta["precond"], t=meta["t"], cg_tol=1e-3, probe_seed=meta["probe_seed"],
-                           rank=None if rank < 0 else rank, newton_grad_tol=meta["newton_grad_tol"])
+                           rank=None if rank < 0 else rank, newton_grad_tol=meta["newton_grad_tol"],
+                           newton_max_iter=fixed or 100)
     lik = vg.get_likelihood("bernoulli-logit")
-    st = vg.find_mode(f, lik, y[perm], np.zeros(n), cfg)
+    try:
+        st = vg.find_mode(f, lik, y[perm], np.zeros(n), cfg)
+    except vg.ConvergenceError as e:
+        if not fixed:
+            raise
+        st = e.last_state.with_converged(True)   # the mode after exactly `fixed` Newton steps
     pr, P = vg.make_probes(f, st, cfg)
     nll = vg.neg_marginal_loglik(st, f, cfg, probes=pr, P=P)
     g = vg.gradient(st, f, lik, np.zeros((n, 0)), cfg, probes=pr, P=P)
@@ -243,11 +250,14 @@ def test_config3_bench_setting_matches_reference(c3):
 
 
 def test_config3_converged_mode_matches_reference_to_1e8(c3):
-    """Same dataset with the device Newton loop run to newton_grad_tol 4e-6
-    (it then stops after step 9): the mode the reference reached at its step 6
-    is reproduced -- NLL 4e-15, gradient 6e-10 relative (SURVEY 8(c) bar 1e-8)."""
+    """Same dataset with the device Newton loop run for exactly 8 steps (an unattainable
+    newton_grad_tol; the stopping test sits on its fp64 noise floor here, DESIGN 6, so the
+    step a given tolerance stops on moves with the rounding of the solves -- 5, 7, 9 and 10
+    were all seen at 4e-6): the mode the reference reached at its step 6 is reproduced --
+    NLL 3e-15, gradient 3e-10 relative (SURVEY 8(c) bar 1e-8)."""
     meta, coords, y = c3
-    f, st, pr, P, nll, g = _device_eval(coords, y, dict(meta, newton_grad_tol=4e-6))
+    f, st, pr, P, nll, g = _device_eval(coords, y, dict(meta, newton_grad_tol=1e-9, fixed_newton_steps=8))
+    assert st.newton_iters == 8
     assert np.abs(np.array(st.cg_iters[:5]) - np.array(meta["newton_cg"][:5])).max() <= 1
     assert np.abs(np.array([tr.order for tr in pr.tridiags]) - np.array(meta["probe_cg"])).max() <= 1
     assert abs(nll - meta["nll"]) <= 1e-8 * abs(meta["nll"])
